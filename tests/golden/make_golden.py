@@ -1,0 +1,270 @@
+"""Generate the golden fixtures from the REFERENCE package itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``splatlift`` from /root/reference/pkg/src, runs the reference's
+own projection (scene.py:252-312), binning (rasterizer.py:72-100),
+accumulation (contributions.py:90-160) and assignment (solver.py:111-172) on
+seeded inputs, and writes small ``.npz`` files next to this script.  Nothing
+at test time reads /root/reference; the GPU box only sees these files.
+
+Inputs of reference-generated fixtures are stored verbatim.  Inputs of the
+larger synthetic workloads come from ``paper_2409_08270_b200.synth`` (seeded
+numpy) and are stored as a sha256 digest plus the generator arguments.
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(ROOT))
+
+import splatlift as ref  # noqa: E402
+from splatlift import contributions as ref_contrib  # noqa: E402
+from splatlift import scene as ref_scene  # noqa: E402
+from splatlift import synth as ref_synth  # noqa: E402
+
+from paper_2409_08270_b200 import synth as my_synth  # noqa: E402
+
+
+def cam_row(v):
+    return np.concatenate([[v.width, v.height, v.fx, v.fy, v.cx, v.cy, v.near_clip],
+                           np.ravel(v.world_to_camera)]).astype(np.float64)
+
+
+def frontal_view(width=16, height=16, focal=24.0, near_clip=0.01, view_id=0):
+    # reference tests/conftest.py:12-25
+    return ref.CameraView(view_id=view_id, width=width, height=height, fx=focal, fy=focal,
+                          cx=width / 2.0 + 0.5, cy=height / 2.0 + 0.5,
+                          world_to_camera=np.eye(4), near_clip=near_clip)
+
+
+def random_scene(rng, n, box=1.2, depth_span=(2.5, 6.0)):
+    # reference tests/conftest.py:39-52
+    means = np.stack([rng.uniform(-box, box, n), rng.uniform(-box, box, n),
+                      rng.uniform(*depth_span, n)], axis=1)
+    quats = rng.normal(size=(n, 4))
+    quats /= np.linalg.norm(quats, axis=1, keepdims=True)
+    scales = rng.uniform(0.05, 0.35, size=(n, 3))
+    opac = rng.uniform(0.1, 0.95, size=n)
+    return ref.GaussianScene(means=means, rotations=quats, scales=scales, opacities=opac)
+
+
+def scene_arrays(scene):
+    return dict(means=scene.means, quats=scene.rotations, scales=scene.scales,
+                opac=scene.opacities)
+
+
+# ---------------------------------------------------------------- projection
+def gen_projection():
+    cases = {}
+    rng = np.random.default_rng(20240811)
+    s1 = random_scene(rng, 300)
+    views = [frontal_view(48, 48, 60.0), ref_synth.ring_view(0, 1.1, 4.0, 64, 64, 70.0, 0.8),
+             frontal_view(37, 23, 30.0, near_clip=3.0)]
+    # cull corner cases: behind, exactly at near clip, offscreen, on axis
+    s2 = ref.GaussianScene(
+        means=[[0, 0, 2.0], [0, 0, -3.0], [40.0, 0, 2.0], [0, 0, 0.5], [0, 0, 0.0],
+               [-50, 3, 2.0], [0.3, -0.2, 1.5]],
+        rotations=[[1, 0, 0, 0]] * 7, scales=[[0.05, 0.05, 0.05]] * 6 + [[0.4, 0.01, 0.2]],
+        opacities=[0.5] * 7)
+    k = 0
+    for scene in (s1, s2):
+        for v in views + [frontal_view(16, 16, 24.0, near_clip=0.5)]:
+            alive, mean2d, inv, z, radius, st = ref_scene._project_arrays(
+                scene.means, scene.rotations, scene.scales, v)
+            cases[f"c{k}"] = dict(
+                **{f"in_{a}": b for a, b in scene_arrays(scene).items()}, cam=cam_row(v),
+                alive=alive, mean2d=mean2d, conic=inv, depth=z, radius=radius,
+                stats=np.array([st.n_input, st.n_emitted, st.n_behind, st.n_degenerate,
+                                st.n_offscreen], np.int64))
+            k += 1
+    return cases
+
+
+# ------------------------------------------------------------------- binning
+def gen_binning():
+    cases = {}
+    rng = np.random.default_rng(7)
+    scenes = [random_scene(rng, 400)]
+    # heavy exact depth ties (frontal identity pose: camera z == world z)
+    n = 600
+    means = np.stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n),
+                      rng.choice([3.0, 3.5, 4.0], size=n)], axis=1)
+    q = rng.normal(size=(n, 4))
+    scenes.append(ref.GaussianScene(means=means, rotations=q,
+                                    scales=rng.uniform(0.02, 0.3, (n, 3)),
+                                    opacities=rng.uniform(0.1, 0.9, n)))
+    views = [frontal_view(48, 48, 60.0), frontal_view(100, 37, 50.0)]
+    k = 0
+    for scene in scenes:
+        for v in views:
+            splats, _ = ref.project_scene(scene, v)
+            b = ref.bin_gaussians_to_tiles(splats, v)
+            offs = np.zeros(len(b.tile_lists) + 1, np.int64)
+            offs[1:] = np.cumsum([len(x) for x in b.tile_lists])
+            items = (np.concatenate([b.indices[x] for x in b.tile_lists])
+                     if offs[-1] else np.zeros(0, np.int64))
+            cases[f"c{k}"] = dict(**{f"in_{a}": c for a, c in scene_arrays(scene).items()},
+                                  cam=cam_row(v), offsets=offs, items=items.astype(np.int64),
+                                  tiles=np.array([b.tiles_x, b.tiles_y]))
+            k += 1
+    # tile_range corner cases (rasterizer.py:106-113), incl. the empty range
+    tr = [(19.0, 8.0, 3, 1, 1), (-5.0, -5.0, 2, 4, 4), (63.9, 0.1, 1, 4, 4), (32.0, 16.0, 16, 4, 4),
+          (1000.0, 5.0, 3, 4, 4), (8.0, 8.0, 0, 1, 1), (15.99, 16.0, 0, 2, 2)]
+    cases["tile_range"] = dict(args=np.array(tr, np.float64),
+                               out=np.array([ref.rasterizer.tile_range(*t) for t in tr], np.int64))
+    return cases
+
+
+# -------------------------------------------------------------- accumulation
+def accumulate_case(scene, pairs, E, blend, store_inputs=True):
+    t0 = time.perf_counter()
+    A = ref.accumulate_contributions(scene, pairs, E, blend).values
+    total = np.zeros((E, len(scene)))
+    for v, m in pairs:
+        total += ref_contrib._accumulate_view(scene, v, m, E, blend)
+    dt = time.perf_counter() - t0
+    assert np.array_equal(total.astype(np.float32), A)
+    out = dict(A=A, A64=total, E=np.int64(E),
+               floors=np.array([blend.alpha_floor, blend.transmittance_floor]))
+    if store_inputs:
+        out.update({f"in_{a}": c for a, c in scene_arrays(scene).items()})
+        out["cams"] = np.stack([cam_row(v) for v, _ in pairs])
+        out["masks"] = np.stack([m.labels for _, m in pairs])
+    print(f"  accumulate N={len(scene)} V={len(pairs)} E={E}: {dt:.1f}s", flush=True)
+    return out
+
+
+def gen_accumulate():
+    D, X = ref.DEFAULT_BLEND, ref.EXACT_BLEND
+    cases = {}
+    # test_contributions.py:26-36 single-Gaussian known answer
+    v = frontal_view()
+    s = ref.GaussianScene.from_gaussians([ref.Gaussian(center=(0, 0, 2.0), rotation=(1, 0, 0, 0),
+                                                       scale=(0.15,) * 3, opacity=0.8)])
+    full = ref.LabelMask(0, np.ones((16, 16), np.uint16))
+    cases["kat_single_default"] = accumulate_case(s, [(v, full)], 2, D)
+    cases["kat_single_exact"] = accumulate_case(s, [(v, full)], 2, X)
+    # culled column (test_contributions.py:97-105)
+    s = ref.GaussianScene(means=[[0, 0, 2.0], [0, 0, -5.0]], rotations=[[1, 0, 0, 0]] * 2,
+                          scales=[[0.1] * 3] * 2, opacities=[0.5, 0.5])
+    cases["culled"] = accumulate_case(s, [(v, full)], 2, D)
+    # make_random fixtures used by the reference suite
+    for seed, n, nv, w, h, e, blend, tag in [
+            (11, 14, 2, 16, 16, 3, D, "d"), (5, 12, 4, 16, 16, 2, D, "d"),
+            (9, 20, 3, 16, 16, 2, D, "d"), (3, 8, 2, 12, 12, 2, X, "x"),
+            (100, 10, 2, 12, 12, 2, X, "x"), (501, 20, 2, 16, 16, 4, D, "d"),
+            (900, 40, 2, 24, 24, 2, D, "d"), (31, 15, 3, 16, 16, 2, D, "d")]:
+        fx = ref_synth.make_random(seed=seed, n_gaussians=n, n_views=nv, width=w, height=h,
+                                   num_objects=e)
+        cases[f"random_{seed}_{tag}"] = accumulate_case(fx.scene, fx.training_views(), e, blend)
+    # denser frontal scenes with random labels, both blends
+    rng = np.random.default_rng(20240811)
+    for i, blend in enumerate((D, X)):
+        sc = random_scene(rng, 60)
+        vv = frontal_view(40, 24, 40.0)
+        lab = rng.integers(0, 3, size=(24, 40), dtype=np.uint16)
+        cases[f"frontal_{i}"] = accumulate_case(sc, [(vv, ref.LabelMask(0, lab))], 3, blend)
+    # C1: make_two_cluster(seed=0, 10k, 8 views 128^2), all 8 GT masks
+    fx = ref_synth.make_two_cluster(seed=0, n_gaussians=10_000, n_views=8, width=128,
+                                    height=128, n_mask_views=8)
+    pairs = [(vw, fx.masks[vw.view_id]) for vw in fx.views]
+    cases["C1_default"] = accumulate_case(fx.scene, pairs, 2, D)
+    c1x = accumulate_case(fx.scene, pairs[:2], 2, X, store_inputs=False)
+    cases["C1_exact_2views"] = c1x
+    # C1 with 20% label noise (C5 at oracle scale)
+    nrng = np.random.default_rng(55)
+    noisy = []
+    for vw, m in pairs:
+        lab = m.labels.copy()
+        flip = nrng.random(lab.shape) < 0.2
+        lab[flip] = nrng.integers(0, 2, size=int(flip.sum()), dtype=np.uint16)
+        noisy.append((vw, ref.LabelMask(vw.view_id, lab)))
+    c = accumulate_case(fx.scene, noisy, 2, D, store_inputs=False)
+    c["masks"] = np.stack([m.labels for _, m in noisy])
+    cases["C1_noisy"] = c
+    # C2/C3-geometry synthetic workloads (inputs regenerated from seed; digest pinned)
+    for name, kw in [("synth_coherent", dict(seed=7, n_gaussians=20_000, n_views=2, width=256,
+                                              height=192, num_objects=8)),
+                     ("synth_iid", dict(seed=8, n_gaussians=20_000, n_views=1, width=256,
+                                        height=192, num_objects=4, iid_masks=True)),
+                     ("synth_dense", dict(seed=9, n_gaussians=50_000, n_views=1, width=504,
+                                          height=378, num_objects=8))]:
+        wl = my_synth.make_workload(**kw)
+        ref_scene_obj = ref.GaussianScene(means=wl.scene.means, rotations=wl.scene.rotations,
+                                          scales=wl.scene.scales, opacities=wl.scene.opacities)
+        ref_views = [ref.CameraView(view_id=v.view_id, width=v.width, height=v.height, fx=v.fx,
+                                    fy=v.fy, cx=v.cx, cy=v.cy, world_to_camera=v.world_to_camera,
+                                    near_clip=v.near_clip) for v in wl.views]
+        pairs = [(rv, ref.LabelMask(rv.view_id, wl.masks[i])) for i, rv in enumerate(ref_views)]
+        c = accumulate_case(ref_scene_obj, pairs, wl.num_objects, D, store_inputs=False)
+        c.pop("A64")
+        c["digest"] = np.frombuffer(wl.digest().encode(), dtype=np.uint8)
+        c["gen_args"] = np.frombuffer(repr(sorted(kw.items())).encode(), dtype=np.uint8)
+        cases[name] = c
+    return cases
+
+
+# ---------------------------------------------------------------- assignment
+def gen_assign(acc_cases):
+    rng = np.random.default_rng(4242)
+    mats = {
+        "rand2": (5.0 * rng.random((2, 500))).astype(np.float32),
+        "rand5": rng.random((5, 300)).astype(np.float32),
+        "rand16": rng.random((16, 2000), dtype=np.float32),
+        "kat": np.array([[0.3, 0.5, 0.0, 0.0, 0.2, 0.1, 0.10],
+                         [0.7, 0.5, 0.0, 0.4, 0.5, 0.8, 0.45]], np.float32),
+        "C1": acc_cases["C1_default"]["A"],
+        "C1_noisy": acc_cases["C1_noisy"]["A"],
+        "synth8": acc_cases["synth_coherent"]["A"],
+    }
+    m = mats["rand2"]
+    m[:, :40] = 0.0
+    m[:, 40:60] = np.float32(1e-13)  # below UNOBSERVED_EPS in f32
+    # near ties: columns whose one-vs-rest margin is within a few ulps
+    t = rng.random(200).astype(np.float32)
+    mats["ties"] = np.stack([t, t * np.float32(1.0000001)])
+    gammas = np.array([-1.0, -0.8, -0.4, -0.25, 0.0, 0.1, 0.2, 0.4, 0.5, 0.8, 1.0])
+    cases = {}
+    for name, A in mats.items():
+        A = np.ascontiguousarray(A, dtype=np.float32)
+        out = dict(A=A, gammas=gammas)
+        out["scene"] = np.stack([ref.assign_scene(ref.ContributionMatrix(A), g).membership
+                                 for g in gammas])
+        if A.shape[0] == 2:
+            out["binary"] = np.stack([ref.assign_binary(ref.ContributionMatrix(A), g).labels
+                                      for g in gammas])
+        cases[name] = out
+    return cases
+
+
+def save(name, cases):
+    flat = {}
+    for case, arrays in cases.items():
+        for k, v in arrays.items():
+            flat[f"{case}/{k}"] = np.asarray(v)
+    path = HERE / f"{name}.npz"
+    np.savez_compressed(path, **flat)
+    print(f"wrote {path} ({path.stat().st_size / 1e6:.2f} MB, {len(cases)} cases)")
+
+
+def main():
+    save("projection", gen_projection())
+    save("binning", gen_binning())
+    acc = gen_accumulate()
+    save("accumulate", acc)
+    save("assign", gen_assign(acc))
+
+
+if __name__ == "__main__":
+    main()
