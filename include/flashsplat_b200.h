@@ -1,0 +1,134 @@
+/*
+ * flashsplat_b200.h -- C ABI of the B200-native FlashSplat label solver.
+ *
+ * Plain C types only (no torch, no C++).  Every entry point replaces one
+ * function of the reference package's Python hot path (paths relative to
+ * /root/reference/pkg/src/splatlift); the Python mirror in
+ * paper_2409_08270_b200/ keeps the reference signatures and calls these
+ * through ctypes (see INTEGRATION.md for the bindings).
+ *
+ * Conventions
+ *   - return value: FS_OK (0) or an FS_E* code; fs_last_error() returns a
+ *     thread-local message for the last failing call on this thread;
+ *   - float64 host arrays are C-contiguous numpy layouts (N x 3 means,
+ *     N x 4 unit quaternions (w, x, y, z), N x 3 scales, N opacities);
+ *   - matrices are E x N row-major (ContributionMatrix.values layout,
+ *     contributions.py:52-55);
+ *   - "device" pointers are CUDA device addresses on the context's device.
+ */
+#ifndef FLASHSPLAT_B200_H
+#define FLASHSPLAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_OK 0
+#define FS_EINVAL 1   /* invalid argument (ValueError on the Python side) */
+#define FS_ECUDA 2    /* CUDA runtime failure (RuntimeError) */
+#define FS_ENOMEM 3   /* device or pinned allocation failed */
+
+#define FS_MODE_BINARY 0
+#define FS_MODE_SCENE 1
+
+typedef struct fs_context fs_context;
+
+/* Pinhole view, scene.py:164-203 (CameraView). */
+typedef struct {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double world_to_camera[16]; /* row-major 4x4 */
+    double near_clip;
+} fs_camera;
+
+/* Cull counters, scene.py:217-225 (ProjectionStats). */
+typedef struct {
+    int64_t n_input, n_emitted, n_behind, n_degenerate, n_offscreen;
+} fs_projection_stats;
+
+/* Totals of one fs_accumulate call (summed over views). */
+typedef struct {
+    int64_t views;
+    int64_t view_pixels;
+    int64_t emitted;          /* visible (view, gaussian) pairs */
+    int64_t instances;        /* (view, tile, gaussian) binning instances */
+    int64_t tile_steps;       /* list entries walked by the raster kernel */
+    int64_t exact_evals;      /* float64 alpha evaluations */
+    int64_t atomics;          /* float64 accumulator atomics */
+    int64_t retried_views;    /* views re-run after growing the instance buffers */
+    double gpu_ms;            /* CUDA-event time of the view loop on the device */
+    double raster_ms;         /* CUDA-event time of raster kernels (stream 0 only, sampled) */
+} fs_accumulate_stats;
+
+const char *fs_last_error(void);
+const char *fs_version(void);
+
+/* Context = one CUDA device + streams + workspaces.  Not thread-safe: one
+ * host thread per context (fs_assign is the reentrant exception). */
+int fs_create(int device, int n_streams, fs_context **out);
+void fs_destroy(fs_context *ctx);
+int fs_device_count(int *out);
+
+/* Device memory helpers for callers without their own allocator. */
+int fs_device_alloc(fs_context *ctx, uint64_t bytes, void **out);
+int fs_device_free(fs_context *ctx, void *ptr);
+int fs_memset_zero(fs_context *ctx, void *dev_ptr, uint64_t bytes);
+int fs_copy_to_device(fs_context *ctx, void *dst, const void *src, uint64_t bytes);
+int fs_copy_to_host(fs_context *ctx, void *dst, const void *src, uint64_t bytes);
+int fs_synchronize(fs_context *ctx);
+
+/* Upload a GaussianScene (scene.py:71-110, arrays already validated and the
+ * quaternions normalised).  Replaces the per-view f64 input handling of
+ * _project_arrays (scene.py:252-278). */
+int fs_set_scene(fs_context *ctx, int64_t n, const double *means, const double *quats,
+                 const double *scales, const double *opacities);
+
+/* _project_arrays (scene.py:252-312) over the resident scene; host outputs
+ * indexed by Gaussian (any may be NULL except alive). */
+int fs_project(fs_context *ctx, const fs_camera *cam, uint8_t *alive, double *mean2d,
+               double *conic, double *depth, int64_t *radius, fs_projection_stats *stats);
+
+/* TileBinning.__init__ (rasterizer.py:72-100): tile_offsets[ntiles + 1] CSR
+ * offsets and items[] Gaussian ids, each tile ordered by (depth, id).
+ * items may be NULL to query *n_items. */
+int fs_bin(fs_context *ctx, const fs_camera *cam, int64_t *tile_offsets, int64_t *items,
+           int64_t items_capacity, int64_t *n_items);
+
+/* TileBinning(view, projected) for an explicit splat list (rasterizer.py:72-100,
+ * e.g. hand-built ProjectedGaussian lists): k splats with mean2d (k x 2),
+ * depth, radius and gaussian index; items[] are positions in the list,
+ * ordered per tile by (depth, gaussian index) like np.lexsort((indices, depths)). */
+int fs_bin_splats(fs_context *ctx, int64_t k, const double *mean2d, const double *depth,
+                  const int64_t *radius, const int64_t *index, int width, int height,
+                  int64_t *tile_offsets, int64_t *items, int64_t items_capacity,
+                  int64_t *n_items);
+
+/* accumulate_contributions (contributions.py:90-116) / _accumulate_view
+ * (contributions.py:119-160) for n_views views: adds every view's alpha*T
+ * mass into acc (E x N float64, DEVICE pointer, caller-zeroed).  masks[v] is
+ * an H x W uint16 label grid, host or device (masks_on_device).  Labels must
+ * be < num_objects (validated by the caller, contributions.py:104-114). */
+int fs_accumulate(fs_context *ctx, int n_views, const fs_camera *cams,
+                  const uint16_t *const *masks, int masks_on_device, int num_objects,
+                  double alpha_floor, double transmittance_floor, double *acc,
+                  fs_accumulate_stats *stats);
+
+/* ContributionMatrix(total.astype(float32)) (contributions.py:116): float64
+ * device accumulator -> float32, written to host (out_on_device = 0) or
+ * device memory. */
+int fs_finalize(fs_context *ctx, const double *acc, int64_t count, float *out, int out_on_device);
+
+/* _one_vs_rest_wins + assign_binary / assign_scene (solver.py:118-172).
+ * A is E x N float32; out is N (binary) or E x N (scene) uint8.  Host or
+ * device pointers (on_device).  Reentrant: runs on the calling thread's
+ * default stream; ctx may be NULL (device 0 / current device). */
+int fs_assign(fs_context *ctx, const float *A, int64_t n, int num_objects, float gamma, int mode,
+              uint8_t *out, int on_device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASHSPLAT_B200_H */

@@ -1,0 +1,344 @@
+"""ctypes binding of the C ABI in include/flashsplat_b200.h.
+
+The shared library is built in-tree (``csrc/Makefile`` ->
+``_lib/libflashsplat_b200.so``) by ``__graft_entry__.build()``.  There is no
+fallback: if the library or a CUDA device is missing every compute call
+raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libflashsplat_b200.so"
+
+FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM = 0, 1, 2, 3
+MODE_BINARY, MODE_SCENE = 0, 1
+
+# Every symbol include/flashsplat_b200.h declares (checked by tests/test_capi.py).
+EXPORTS = (
+    "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
+    "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
+    "fs_copy_to_host", "fs_synchronize", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_accumulate", "fs_finalize", "fs_assign",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library is not built or no sm_100 device is usable."""
+
+
+class FsCamera(ctypes.Structure):
+    _fields_ = [
+        ("width", ctypes.c_int32), ("height", ctypes.c_int32),
+        ("fx", ctypes.c_double), ("fy", ctypes.c_double),
+        ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+        ("world_to_camera", ctypes.c_double * 16), ("near_clip", ctypes.c_double),
+    ]
+
+
+class FsProjectionStats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in
+                ("n_input", "n_emitted", "n_behind", "n_degenerate", "n_offscreen")]
+
+
+class FsAccumulateStats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in
+                ("views", "view_pixels", "emitted", "instances", "tile_steps", "exact_evals",
+                 "atomics", "retried_views")] + [("gpu_ms", ctypes.c_double),
+                                                 ("raster_ms", ctypes.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load() -> ctypes.CDLL:
+    """Load the library (once); raise NativeUnavailable if it is not built."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeUnavailable(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()')")
+        L = ctypes.CDLL(str(LIB_PATH))
+        P, I, I64, D, F = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double,
+                           ctypes.c_float)
+        sig = {
+            "fs_last_error": ([], ctypes.c_char_p),
+            "fs_version": ([], ctypes.c_char_p),
+            "fs_create": ([I, I, ctypes.POINTER(P)], I),
+            "fs_destroy": ([P], None),
+            "fs_device_count": ([ctypes.POINTER(I)], I),
+            "fs_device_alloc": ([P, ctypes.c_uint64, ctypes.POINTER(P)], I),
+            "fs_device_free": ([P, P], I),
+            "fs_memset_zero": ([P, P, ctypes.c_uint64], I),
+            "fs_copy_to_device": ([P, P, P, ctypes.c_uint64], I),
+            "fs_copy_to_host": ([P, P, P, ctypes.c_uint64], I),
+            "fs_synchronize": ([P], I),
+            "fs_set_scene": ([P, I64, P, P, P, P], I),
+            "fs_project": ([P, P, P, P, P, P, P, P], I),
+            "fs_bin": ([P, P, P, P, I64, ctypes.POINTER(I64)], I),
+            "fs_bin_splats": ([P, I64, P, P, P, P, I, I, P, P, I64, ctypes.POINTER(I64)], I),
+            "fs_accumulate": ([P, I, P, P, I, I, D, D, P, P], I),
+            "fs_finalize": ([P, P, I64, P, I], I),
+            "fs_assign": ([P, P, I64, I, F, I, P, I], I),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+def _check(rc: int) -> None:
+    if rc == FS_OK:
+        return
+    msg = load().fs_last_error().decode(errors="replace")
+    if rc == FS_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    rc = load().fs_device_count(ctypes.byref(c))
+    return c.value if rc == FS_OK else 0
+
+
+def camera_struct(view) -> FsCamera:
+    c = FsCamera()
+    c.width, c.height = int(view.width), int(view.height)
+    c.fx, c.fy, c.cx, c.cy = float(view.fx), float(view.fy), float(view.cx), float(view.cy)
+    w = np.ascontiguousarray(view.world_to_camera, dtype=np.float64).reshape(16)
+    ctypes.memmove(c.world_to_camera, w.ctypes.data, 16 * 8)
+    c.near_clip = float(view.near_clip)
+    return c
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class DeviceBuffer:
+    """A cudaMalloc'ed block owned by a Context (freed on release / GC)."""
+
+    def __init__(self, ctx: "Context", nbytes: int):
+        self.ctx = ctx
+        self.nbytes = int(nbytes)
+        ptr = ctypes.c_void_p()
+        _check(load().fs_device_alloc(ctx.handle, self.nbytes, ctypes.byref(ptr)))
+        self.ptr = ptr.value
+
+    def zero(self) -> "DeviceBuffer":
+        _check(load().fs_memset_zero(self.ctx.handle, self.ptr, self.nbytes))
+        return self
+
+    def to_host(self, out: np.ndarray) -> np.ndarray:
+        assert out.nbytes <= self.nbytes
+        _check(load().fs_copy_to_host(self.ctx.handle, _p(out), self.ptr, out.nbytes))
+        return out
+
+    def from_host(self, arr: np.ndarray) -> "DeviceBuffer":
+        arr = np.ascontiguousarray(arr)
+        assert arr.nbytes <= self.nbytes
+        _check(load().fs_copy_to_device(self.ctx.handle, self.ptr, _p(arr), arr.nbytes))
+        return self
+
+    def release(self) -> None:
+        if self.ptr and self.ctx.handle:
+            load().fs_device_free(self.ctx.handle, self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+class Context:
+    """fs_context: one device, its streams, workspaces and the resident scene."""
+
+    def __init__(self, device: int = 0, streams: int = 4):
+        L = load()
+        h = ctypes.c_void_p()
+        rc = L.fs_create(int(device), int(streams), ctypes.byref(h))
+        if rc != FS_OK:
+            raise NativeUnavailable(L.fs_last_error().decode(errors="replace"))
+        self.handle = h.value
+        self.device = int(device)
+        self._scene_key = None
+        self.n = 0
+        self.lock = threading.RLock()
+
+    def close(self) -> None:
+        if self.handle:
+            load().fs_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- scene ---------------------------------------------------------------
+    def set_scene(self, scene) -> None:
+        key = (id(scene), len(scene), scene.means.ctypes.data, scene.rotations.ctypes.data,
+               scene.scales.ctypes.data, scene.opacities.ctypes.data)
+        if key == self._scene_key:
+            return
+        m = np.ascontiguousarray(scene.means, dtype=np.float64)
+        q = np.ascontiguousarray(scene.rotations, dtype=np.float64)
+        s = np.ascontiguousarray(scene.scales, dtype=np.float64)
+        o = np.ascontiguousarray(scene.opacities, dtype=np.float64)
+        _check(load().fs_set_scene(self.handle, len(scene), _p(m), _p(q), _p(s), _p(o)))
+        self._scene_key = key
+        self._scene_ref = scene  # keep the id() stable while cached
+        self.n = len(scene)
+
+    def set_arrays(self, means, quats, scales, opac) -> None:
+        m = np.ascontiguousarray(means, dtype=np.float64).reshape(-1, 3)
+        n = m.shape[0]
+        q = np.ascontiguousarray(quats, dtype=np.float64).reshape(n, 4)
+        s = np.ascontiguousarray(scales, dtype=np.float64).reshape(n, 3)
+        o = np.ascontiguousarray(opac, dtype=np.float64).reshape(n)
+        _check(load().fs_set_scene(self.handle, n, _p(m), _p(q), _p(s), _p(o)))
+        self._scene_key = None
+        self.n = n
+
+    # -- stages --------------------------------------------------------------
+    def project(self, view):
+        n = self.n
+        alive = np.zeros(n, np.uint8)
+        mean2d = np.zeros((n, 2))
+        conic = np.zeros((n, 3))
+        depth = np.zeros(n)
+        radius = np.zeros(n, np.int64)
+        st = FsProjectionStats()
+        cam = camera_struct(view)
+        _check(load().fs_project(self.handle, ctypes.byref(cam), _p(alive), _p(mean2d),
+                                 _p(conic), _p(depth), _p(radius), ctypes.byref(st)))
+        stats = (st.n_input, st.n_emitted, st.n_behind, st.n_degenerate, st.n_offscreen)
+        return alive.astype(bool), mean2d, conic, depth, radius, stats
+
+    def bin(self, view):
+        cam = camera_struct(view)
+        ntiles = ((view.width + 15) // 16) * ((view.height + 15) // 16)
+        offs = np.zeros(ntiles + 1, np.int64)
+        count = ctypes.c_int64(0)
+        L = load()
+        _check(L.fs_bin(self.handle, ctypes.byref(cam), _p(offs), None, 0, ctypes.byref(count)))
+        items = np.zeros(max(count.value, 1), np.int64)
+        _check(L.fs_bin(self.handle, ctypes.byref(cam), _p(offs), _p(items), items.size,
+                        ctypes.byref(count)))
+        return offs, items[:count.value]
+
+    def accumulate(self, views, masks, num_objects: int, alpha_floor: float, t_floor: float,
+                   acc_ptr: int, masks_on_device: bool = False) -> dict:
+        """Add every view's alpha*T mass into the E x N float64 device buffer acc_ptr."""
+        nv = len(views)
+        cams = (FsCamera * max(nv, 1))(*[camera_struct(v) for v in views])
+        if masks_on_device:
+            ptrs = (ctypes.c_void_p * max(nv, 1))(*[int(m) for m in masks])
+        else:
+            keep = [np.ascontiguousarray(m, dtype=np.uint16) for m in masks]
+            ptrs = (ctypes.c_void_p * max(nv, 1))(*[k.ctypes.data for k in keep])
+        st = FsAccumulateStats()
+        _check(load().fs_accumulate(self.handle, nv, ctypes.byref(cams), ctypes.byref(ptrs),
+                                    1 if masks_on_device else 0, int(num_objects),
+                                    float(alpha_floor), float(t_floor), acc_ptr,
+                                    ctypes.byref(st)))
+        return st.as_dict()
+
+    def finalize(self, acc_ptr: int, count: int, out_ptr: int = None, out: np.ndarray = None):
+        if out is not None:
+            _check(load().fs_finalize(self.handle, acc_ptr, count, _p(out), 0))
+            return out
+        _check(load().fs_finalize(self.handle, acc_ptr, count, out_ptr, 1))
+        return None
+
+    def alloc(self, nbytes: int) -> DeviceBuffer:
+        return DeviceBuffer(self, nbytes)
+
+
+def assign(values: np.ndarray, gamma: float, mode: int, ctx: Context = None,
+           on_device_ptr: int = None, n: int = None, e: int = None, out_ptr: int = None):
+    """fs_assign on host arrays (returns uint8) or on device pointers (in place)."""
+    L = load()
+    h = ctx.handle if ctx is not None else None
+    if on_device_ptr is not None:
+        _check(L.fs_assign(h, on_device_ptr, int(n), int(e), float(gamma), int(mode),
+                           out_ptr, 1))
+        return None
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    e, n = values.shape
+    out = np.zeros(n if mode == MODE_BINARY else (e, n), np.uint8)
+    _check(L.fs_assign(h, _p(values), int(n), int(e), float(gamma), int(mode), _p(out), 0))
+    return out
+
+
+_contexts: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def default_device() -> int:
+    env = os.environ.get("LOCAL_RANK")
+    if env is not None and device_count() > 1:
+        return int(env) % device_count()
+    return 0
+
+
+def context(device: int = None) -> Context:
+    """Process-wide cached context per device."""
+    if device is None:
+        device = default_device()
+    with _ctx_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = Context(device)
+            _contexts[device] = ctx
+        return ctx
+
+
+def bin_splats(mean2d, depth, radius, index, width: int, height: int, device: int = None):
+    """fs_bin_splats: CSR tile lists (positions into the splat list)."""
+    ctx = context(device)
+    mean2d = np.ascontiguousarray(mean2d, dtype=np.float64).reshape(-1, 2)
+    k = mean2d.shape[0]
+    depth = np.ascontiguousarray(depth, dtype=np.float64).reshape(k)
+    radius = np.ascontiguousarray(radius, dtype=np.int64).reshape(k)
+    index = np.ascontiguousarray(index, dtype=np.int64).reshape(k)
+    ntiles = ((width + 15) // 16) * ((height + 15) // 16)
+    offs = np.zeros(ntiles + 1, np.int64)
+    count = ctypes.c_int64(0)
+    L = load()
+    with ctx.lock:
+        _check(L.fs_bin_splats(ctx.handle, k, _p(mean2d), _p(depth), _p(radius), _p(index),
+                               int(width), int(height), _p(offs), None, 0, ctypes.byref(count)))
+        items = np.zeros(max(count.value, 1), np.int64)
+        _check(L.fs_bin_splats(ctx.handle, k, _p(mean2d), _p(depth), _p(radius), _p(index),
+                               int(width), int(height), _p(offs), _p(items), items.size,
+                               ctypes.byref(count)))
+    return offs, items[:count.value]
+
+
+def project(means, quats, scales, view, device: int = None):
+    """Projection of an arbitrary (sub)set of Gaussians, for the stage API."""
+    ctx = context(device)
+    with ctx.lock:
+        n = np.asarray(means).reshape(-1, 3).shape[0]
+        ctx.set_arrays(means, quats, scales, np.ones(n))
+        return ctx.project(view)

@@ -1,0 +1,148 @@
+"""Contribution accumulation: the E x N alpha*T mass matrix on the GPU.
+
+``accumulate_contributions`` keeps the reference signature
+(``contributions.py:90-95``), validation order and messages
+(``contributions.py:104-114``) and result type; the work runs in the CUDA
+library (``fs_accumulate``: projection, depth/tile radix sorts and the
+raster-accumulate kernel per view, float64 accumulation on the device, one
+float32 cast at the end -- ``contributions.py:116``).
+
+Views are independent and A is additive over views
+(``contributions.py:103-116``), so with ``process_group`` set (a
+``torch.distributed`` group, one process per GPU) every rank accumulates a
+disjoint shard of the views and one all-reduce of the float64 accumulator
+joins them (``distributed.py``).
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .rasterizer import DEFAULT_BLEND, BlendConfig
+from .scene import CameraView, GaussianScene
+
+MATRIX_MAGIC = b"FSA1"  # reference contributions.py:26
+
+
+@dataclass
+class LabelMask:
+    """H x W uint16 object-id grid for one view; 0 is background (``contributions.py:29-43``)."""
+
+    view_id: int
+    labels: np.ndarray
+
+    def __post_init__(self) -> None:
+        self.labels = np.asarray(self.labels, dtype=np.uint16)
+        if self.labels.ndim != 2:
+            raise ValueError("mask labels must be a 2D grid")
+
+    @property
+    def num_objects(self) -> int:
+        return int(self.labels.max()) + 1 if self.labels.size else 1
+
+
+@dataclass
+class ContributionMatrix:
+    """Dense E x N float32 alpha*T mass per label (``contributions.py:46-87``)."""
+
+    values: np.ndarray
+
+    def __post_init__(self) -> None:
+        self.values = np.ascontiguousarray(self.values, dtype=np.float32)
+        if self.values.ndim != 2:
+            raise ValueError("contribution matrix must be 2D (E x N)")
+
+    @property
+    def num_objects(self) -> int:
+        return int(self.values.shape[0])
+
+    @property
+    def num_gaussians(self) -> int:
+        return int(self.values.shape[1])
+
+    @property
+    def observed(self) -> np.ndarray:
+        """Columns that received any mass (float64 column sum > 0)."""
+        return self.values.sum(axis=0, dtype=np.float64) > 0.0
+
+    def save(self, path) -> None:
+        e, n = self.values.shape
+        with open(path, "wb") as fh:
+            fh.write(MATRIX_MAGIC + struct.pack("<II", e, n))
+            self.values.tofile(fh)
+
+    @classmethod
+    def load(cls, path) -> "ContributionMatrix":
+        with open(path, "rb") as fh:
+            magic = fh.read(4)
+            if magic != MATRIX_MAGIC:
+                raise ValueError(f"{path}: bad magic {magic!r}")
+            e, n = struct.unpack("<II", fh.read(8))
+            data = np.fromfile(fh, dtype=np.float32, count=e * n)
+        if data.size != e * n:
+            raise ValueError(f"{path}: truncated contribution matrix")
+        return cls(values=data.reshape(e, n))
+
+
+def validate_views(views: Sequence, num_objects: int) -> None:
+    """Reference checks in view order (``contributions.py:104-114``)."""
+    for view, mask in views:
+        labels = mask.labels
+        if labels.shape != (view.height, view.width):
+            raise ValueError(
+                f"view {view.view_id}: mask shape {labels.shape} does not "
+                f"match view dimensions {(view.height, view.width)}")
+        top = int(labels.max()) if labels.size else 0
+        if top >= num_objects:
+            j, k = np.unravel_index(int(np.argmax(labels)), labels.shape)
+            raise ValueError(
+                f"view {view.view_id}: label {top} at pixel ({j}, {k}) "
+                f"exceeds object count {num_objects}")
+
+
+def accumulate_contributions(
+    scene: GaussianScene,
+    views: Sequence[tuple],
+    num_objects: int,
+    blend: BlendConfig = DEFAULT_BLEND,
+    *,
+    device: Optional[int] = None,
+    process_group=None,
+    stats: Optional[dict] = None,
+) -> ContributionMatrix:
+    """Scatter every pixel's surviving alpha*T samples into label rows, on the GPU.
+
+    ``device``: CUDA ordinal (default: ``LOCAL_RANK`` or 0).  ``process_group``:
+    shard the views over a ``torch.distributed`` group and all-reduce the
+    accumulator (every rank returns the full matrix).  ``stats``: filled with
+    the library's counters (instances, tile steps, exact evaluations, ...).
+    """
+    views = list(views)
+    num_objects = int(num_objects)
+    validate_views(views, num_objects)
+    if process_group is not None:
+        from .distributed import accumulate_sharded
+        values = accumulate_sharded(scene, views, num_objects, blend, process_group,
+                                    device=device, stats=stats)
+        return ContributionMatrix(values=values)
+    from . import _native
+
+    ctx = _native.context(device)
+    n = len(scene)
+    with ctx.lock:
+        ctx.set_scene(scene)
+        acc = ctx.alloc(8 * num_objects * max(n, 1)).zero()
+        st = ctx.accumulate([v for v, _ in views], [m.labels for _, m in views], num_objects,
+                            blend.alpha_floor, blend.transmittance_floor, acc.ptr)
+        out = np.empty((num_objects, n), dtype=np.float32)
+        if out.size:
+            ctx.finalize(acc.ptr, out.size, out=out)
+        acc.release()
+    if stats is not None:
+        stats.update(st)
+    return ContributionMatrix(values=out)

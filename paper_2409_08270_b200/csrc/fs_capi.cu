@@ -1,0 +1,749 @@
+// fs_capi.cu -- host runtime and C ABI of the FlashSplat B200 label solver.
+//
+// One fs_context owns a CUDA device, S streams and one workspace per stream.
+// fs_accumulate hands views out round-robin to the streams; each view runs
+// the device pipeline
+//     K1 project -> K2a depth radix sort -> K2b emit instances ->
+//     K2c tile radix sort -> K2d tile ranges -> K3 raster-accumulate
+// entirely on its stream with device-side counts (no host sync inside the
+// loop).  Host masks are staged through a pinned buffer per stream and
+// copied on the same stream, so the copy of view v+S overlaps the kernels of
+// views v+1..v+S-1.  After the loop the per-view counters are read back
+// once; views whose instance count overflowed the buffers are re-run after
+// growing them (the raster kernel skips an overflowed view, so nothing was
+// added for it).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "flashsplat_b200.h"
+#include "fs_common.cuh"
+#include "fs_kernels.cuh"
+
+namespace fs {
+
+namespace {
+thread_local std::string g_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    return code;
+}
+
+__global__ void view_end_kernel(const ViewCounters* vc, ViewCounters* log) {
+    if (threadIdx.x == 0) *log = *vc;
+}
+
+int bits_for(unsigned int v) {  // bits needed to represent values 0..v
+    int b = 0;
+    while (b < 32 && (v >> b) != 0u) ++b;
+    return b;
+}
+
+}  // namespace
+
+int set_cuda_error(cudaError_t e, const char* expr, const char* file, int line) {
+    return fail(FS_ECUDA, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+                cudaGetErrorString(e), file, line, expr);
+}
+
+struct Work {
+    cudaStream_t stream = nullptr;
+    long long n_cap = 0;
+    unsigned int inst_cap = 0;
+    int ntiles_cap = 0;
+    size_t mask_cap = 0;
+    unsigned long long* dkeys[2] = {nullptr, nullptr};
+    unsigned int* dvals[2] = {nullptr, nullptr};
+    unsigned long long* rect = nullptr;
+    Rec32* r32 = nullptr;
+    Rec64* r64 = nullptr;
+    unsigned int* block_sums = nullptr;
+    unsigned int* hist = nullptr;
+    unsigned int* ikeys[2] = {nullptr, nullptr};
+    unsigned int* ivals[2] = {nullptr, nullptr};
+    unsigned int* tile_start = nullptr;
+    ViewCounters* vc = nullptr;
+    unsigned long long* idx_oa = nullptr;  // OR/AND of the secondary (index) keys
+    uint16_t* mask_dev = nullptr;
+    uint16_t* pinned = nullptr;
+    cudaEvent_t h2d_done = nullptr;
+    bool h2d_pending = false;
+    cudaEvent_t done = nullptr;
+};
+
+}  // namespace fs
+
+struct fs_context {
+    int device = 0;
+    int num_sms = 148;
+    long long n = 0;
+    double* mx = nullptr;
+    double* my = nullptr;
+    double* mz = nullptr;
+    double* sig = nullptr;
+    double* opac = nullptr;
+    unsigned long long* tile_oa_table = nullptr;  // [33][2] = {(1<<b)-1, 0}
+    fs::ViewCounters* view_log = nullptr;
+    int view_log_cap = 0;
+    std::vector<fs::Work> work;
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+};
+
+using fs::fail;
+
+namespace {
+
+#define CK(expr)                                                                  \
+    do {                                                                          \
+        cudaError_t _e = (expr);                                                  \
+        if (_e != cudaSuccess) return fs::set_cuda_error(_e, #expr, __FILE__, __LINE__); \
+    } while (0)
+
+template <typename T>
+int dev_alloc(T** p, size_t count) {
+    if (*p) {
+        cudaFree(*p);
+        *p = nullptr;
+    }
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FS_ENOMEM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
+                    cudaGetErrorString(e));
+    }
+    return FS_OK;
+}
+
+void free_work(fs::Work& w) {
+    auto f = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    f(w.dkeys[0]); f(w.dkeys[1]); f(w.dvals[0]); f(w.dvals[1]); f(w.rect); f(w.r32); f(w.r64);
+    f(w.block_sums); f(w.hist); f(w.ikeys[0]); f(w.ikeys[1]); f(w.ivals[0]); f(w.ivals[1]);
+    f(w.tile_start); f(w.vc); f(w.idx_oa); f(w.mask_dev);
+    if (w.pinned) cudaFreeHost(w.pinned);
+    if (w.h2d_done) cudaEventDestroy(w.h2d_done);
+    if (w.done) cudaEventDestroy(w.done);
+    if (w.stream) cudaStreamDestroy(w.stream);
+    w = fs::Work{};
+}
+
+// Size a workspace for n Gaussians, ntiles tiles, inst instances, mask_px pixels.
+int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned int inst,
+                size_t mask_px) {
+    int rc;
+    if (n > w.n_cap) {
+        for (int k = 0; k < 2; ++k) {
+            if ((rc = dev_alloc(&w.dkeys[k], n))) return rc;
+            if ((rc = dev_alloc(&w.dvals[k], n))) return rc;
+        }
+        if ((rc = dev_alloc(&w.rect, n))) return rc;
+        if ((rc = dev_alloc(&w.r32, n))) return rc;
+        if ((rc = dev_alloc(&w.r64, n))) return rc;
+        w.n_cap = n;
+    }
+    if (!w.block_sums) {
+        if ((rc = dev_alloc(&w.block_sums, (size_t)fs::sort_grid(ctx->num_sms)))) return rc;
+        if ((rc = dev_alloc(&w.hist, fs::sort_hist_entries(ctx->num_sms)))) return rc;
+        if ((rc = dev_alloc(&w.vc, 1))) return rc;
+        if ((rc = dev_alloc(&w.idx_oa, 2))) return rc;
+    }
+    if (inst > w.inst_cap) {
+        for (int k = 0; k < 2; ++k) {
+            if ((rc = dev_alloc(&w.ikeys[k], inst))) return rc;
+            if ((rc = dev_alloc(&w.ivals[k], inst))) return rc;
+        }
+        w.inst_cap = inst;
+    }
+    if (ntiles > w.ntiles_cap) {
+        if ((rc = dev_alloc(&w.tile_start, (size_t)ntiles + 1))) return rc;
+        w.ntiles_cap = ntiles;
+    }
+    if (mask_px > w.mask_cap) {
+        if ((rc = dev_alloc(&w.mask_dev, mask_px))) return rc;
+        if (w.pinned) cudaFreeHost(w.pinned);
+        w.pinned = nullptr;
+        CK(cudaMallocHost(reinterpret_cast<void**>(&w.pinned), mask_px * sizeof(uint16_t)));
+        w.mask_cap = mask_px;
+    }
+    return FS_OK;
+}
+
+fs::Camera to_cam(const fs_camera& c) {
+    fs::Camera k;
+    k.width = c.width;
+    k.height = c.height;
+    k.fx = c.fx;
+    k.fy = c.fy;
+    k.cx = c.cx;
+    k.cy = c.cy;
+    for (int i = 0; i < 16; ++i) k.w2c[i] = c.world_to_camera[i];
+    k.near_clip = c.near_clip;
+    return k;
+}
+
+int check_cam(const fs_camera& c, int idx) {
+    if (c.width < 1 || c.height < 1)
+        return fail(FS_EINVAL, "view %d: image dimensions must be >= 1, got %dx%d", idx, c.width,
+                    c.height);
+    long long tiles = (long long)fs::tiles_x_of(c.width) * fs::tiles_y_of(c.height);
+    if (tiles > (1 << 24)) return fail(FS_EINVAL, "view %d: image too large (%lld tiles)", idx, tiles);
+    if (fs::tiles_x_of(c.width) > 65535 || fs::tiles_y_of(c.height) > 65535)
+        return fail(FS_EINVAL, "view %d: image too large", idx);
+    return FS_OK;
+}
+
+// Projection + depth sort + binning of one view on workspace w.
+void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
+                 int cull_floor, fs::ProjectExport ex) {
+    const int n = (int)ctx->n;
+    fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
+                       cull_floor, w.dkeys[0], w.dvals[0], w.rect, w.r32, w.r64, w.vc, ex,
+                       ctx->num_sms, w.stream);
+    fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
+                                              nullptr, (unsigned)n, &w.vc->key_or, 8, w.hist,
+                                              ctx->num_sms, w.stream);
+    const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
+    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
+    fs::BinBuffers b;
+    b.dkeys[0] = w.dkeys[0];
+    b.dkeys[1] = w.dkeys[1];
+    b.dvals[0] = w.dvals[0];
+    b.dvals[1] = w.dvals[1];
+    b.depth_or_and = &w.vc->key_or;
+    b.rect = w.rect;
+    b.block_sums = w.block_sums;
+    b.ikeys[0] = w.ikeys[0];
+    b.ikeys[1] = w.ikeys[1];
+    b.ivals[0] = w.ivals[0];
+    b.ivals[1] = w.ivals[1];
+    b.tile_or_and = ctx->tile_oa_table + 2 * bits;
+    b.hist = w.hist;
+    b.tile_start = w.tile_start;
+    b.capacity = w.inst_cap;
+    fs::launch_bin(n, ntiles, tx, (bits + 7) / 8, b, w.vc, ctx->num_sms, w.stream);
+}
+
+void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
+                  int num_objects, double alpha_floor, double t_floor, double* acc,
+                  fs::ViewCounters* log) {
+    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{});
+    const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
+    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
+    fs::RasterArgs ra;
+    ra.width = cam.width;
+    ra.height = cam.height;
+    ra.tiles_x = tx;
+    ra.ntiles = ntiles;
+    ra.num_objects = num_objects;
+    ra.n_gaussians = ctx->n;
+    ra.alpha_floor = alpha_floor;
+    ra.t_floor = t_floor;
+    ra.mask = mask;
+    ra.tile_start = w.tile_start;
+    ra.inst_gid[0] = w.ivals[0];
+    ra.inst_gid[1] = w.ivals[1];
+    ra.tile_passes = (bits + 7) / 8;
+    ra.tile_or_and = ctx->tile_oa_table + 2 * bits;
+    ra.r32 = w.r32;
+    ra.r64 = w.r64;
+    ra.acc = acc;
+    ra.vc = w.vc;
+    fs::launch_raster(ra, w.stream);
+    if (log) fs::view_end_kernel<<<1, 32, 0, w.stream>>>(w.vc, log);
+}
+
+unsigned int initial_inst_cap(long long n) {
+    long long c = std::max<long long>(1 << 22, 4 * n);
+    return (unsigned int)std::min<long long>(c, 0x7fffffffLL);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fs_last_error(void) { return fs::g_error.c_str(); }
+
+const char* fs_version(void) { return "flashsplat-b200 0.1.0 (sm_100a)"; }
+
+int fs_device_count(int* out) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;
+        return fs::set_cuda_error(e, "cudaGetDeviceCount", __FILE__, __LINE__);
+    }
+    *out = c;
+    return FS_OK;
+}
+
+int fs_create(int device, int n_streams, fs_context** out) {
+    if (!out) return fail(FS_EINVAL, "fs_create: out is NULL");
+    *out = nullptr;
+    if (n_streams < 1) n_streams = 1;
+    if (n_streams > 16) n_streams = 16;
+    CK(cudaSetDevice(device));
+    fs_context* ctx = new fs_context();
+    ctx->device = device;
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return fs::set_cuda_error(e, "cudaGetDeviceProperties", __FILE__, __LINE__);
+    }
+    if (prop.major < 10) {
+        delete ctx;
+        return fail(FS_ECUDA, "device %d (%s, sm_%d%d) is not sm_100: this library is built for "
+                              "B200 (sm_100a) only", device, prop.name, prop.major, prop.minor);
+    }
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->work.resize(n_streams);
+    for (auto& w : ctx->work) {
+        CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&w.h2d_done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
+    }
+    CK(cudaEventCreate(&ctx->ev_start));
+    CK(cudaEventCreate(&ctx->ev_stop));
+    unsigned long long table[33 * 2];
+    for (int b = 0; b <= 32; ++b) {
+        table[2 * b] = b == 32 ? 0xFFFFFFFFull : ((1ull << b) - 1ull);
+        table[2 * b + 1] = 0ull;
+    }
+    int rc = dev_alloc(&ctx->tile_oa_table, 66);
+    if (rc) {
+        fs_destroy(ctx);
+        return rc;
+    }
+    CK(cudaMemcpy(ctx->tile_oa_table, table, sizeof(table), cudaMemcpyHostToDevice));
+    *out = ctx;
+    return FS_OK;
+}
+
+void fs_destroy(fs_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (auto& w : ctx->work) free_work(w);
+    for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
+                    (void*)ctx->opac, (void*)ctx->tile_oa_table, (void*)ctx->view_log})
+        if (p) cudaFree(p);
+    if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+    if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
+    delete ctx;
+}
+
+int fs_device_alloc(fs_context* ctx, uint64_t bytes, void** out) {
+    if (!ctx || !out) return fail(FS_EINVAL, "fs_device_alloc: NULL argument");
+    CK(cudaSetDevice(ctx->device));
+    cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FS_ENOMEM, "cudaMalloc of %llu bytes failed", (unsigned long long)bytes);
+    }
+    return FS_OK;
+}
+
+int fs_device_free(fs_context* ctx, void* ptr) {
+    if (!ctx) return fail(FS_EINVAL, "fs_device_free: NULL context");
+    CK(cudaSetDevice(ctx->device));
+    if (ptr) CK(cudaFree(ptr));
+    return FS_OK;
+}
+
+int fs_memset_zero(fs_context* ctx, void* p, uint64_t bytes) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemset(p, 0, bytes));
+    return FS_OK;
+}
+
+int fs_copy_to_device(fs_context* ctx, void* dst, const void* src, uint64_t bytes) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return FS_OK;
+}
+
+int fs_copy_to_host(fs_context* ctx, void* dst, const void* src, uint64_t bytes) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return FS_OK;
+}
+
+int fs_synchronize(fs_context* ctx) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    return FS_OK;
+}
+
+int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* quats,
+                 const double* scales, const double* opacities) {
+    if (!ctx) return fail(FS_EINVAL, "fs_set_scene: NULL context");
+    if (n < 0 || n > 0x7fffffffLL) return fail(FS_EINVAL, "fs_set_scene: bad Gaussian count %lld", (long long)n);
+    if (n > 0 && (!means || !quats || !scales || !opacities))
+        return fail(FS_EINVAL, "fs_set_scene: NULL array");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    int rc;
+    if ((rc = dev_alloc(&ctx->mx, n)) || (rc = dev_alloc(&ctx->my, n)) ||
+        (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
+        (rc = dev_alloc(&ctx->opac, n)))
+        return rc;
+    ctx->n = n;
+    if (n == 0) return FS_OK;
+    double *d_means = nullptr, *d_quats = nullptr, *d_scales = nullptr;
+    if ((rc = dev_alloc(&d_means, 3 * (size_t)n)) || (rc = dev_alloc(&d_quats, 4 * (size_t)n)) ||
+        (rc = dev_alloc(&d_scales, 3 * (size_t)n)))
+        return rc;
+    CK(cudaMemcpy(d_means, means, 24 * (size_t)n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_quats, quats, 32 * (size_t)n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_scales, scales, 24 * (size_t)n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->opac, opacities, 8 * (size_t)n, cudaMemcpyHostToDevice));
+    fs::launch_scene_setup((int)n, d_means, d_quats, d_scales, ctx->mx, ctx->my, ctx->mz, ctx->sig, 0);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    cudaFree(d_means);
+    cudaFree(d_quats);
+    cudaFree(d_scales);
+    return FS_OK;
+}
+
+int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* mean2d,
+               double* conic, double* depth, int64_t* radius, fs_projection_stats* stats) {
+    if (!ctx || !cam || !alive) return fail(FS_EINVAL, "fs_project: NULL argument");
+    int rc = check_cam(*cam, 0);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    fs::Work& w = ctx->work[0];
+    const long long n = ctx->n;
+    if ((rc = ensure_work(ctx, w, n, 1, 1, 1))) return rc;
+    fs::ProjectExport ex{};
+    size_t n1 = (size_t)std::max<long long>(n, 1);
+    if ((rc = dev_alloc(&ex.alive, n1)) || (rc = dev_alloc(&ex.mean2d, 2 * n1)) ||
+        (rc = dev_alloc(&ex.conic, 3 * n1)) || (rc = dev_alloc(&ex.depth, n1)) ||
+        (rc = dev_alloc(&ex.radius, n1)))
+        return rc;
+    fs::launch_project((int)n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, to_cam(*cam), 0.0,
+                       0, w.dkeys[0], w.dvals[0], w.rect, w.r32, w.r64, w.vc, ex, ctx->num_sms,
+                       w.stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(w.stream));
+    CK(cudaMemcpy(alive, ex.alive, (size_t)n, cudaMemcpyDeviceToHost));
+    if (mean2d) CK(cudaMemcpy(mean2d, ex.mean2d, 16 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (conic) CK(cudaMemcpy(conic, ex.conic, 24 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (depth) CK(cudaMemcpy(depth, ex.depth, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (radius) CK(cudaMemcpy(radius, ex.radius, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    if (stats) {
+        fs::ViewCounters vc;
+        CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
+        stats->n_input = n;
+        stats->n_emitted = vc.n_emitted;
+        stats->n_behind = vc.n_behind;
+        stats->n_degenerate = vc.n_degenerate;
+        stats->n_offscreen = vc.n_offscreen;
+    }
+    cudaFree(ex.alive);
+    cudaFree(ex.mean2d);
+    cudaFree(ex.conic);
+    cudaFree(ex.depth);
+    cudaFree(ex.radius);
+    return FS_OK;
+}
+
+int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t* items,
+           int64_t items_capacity, int64_t* n_items) {
+    if (!ctx || !cam || !tile_offsets || !n_items) return fail(FS_EINVAL, "fs_bin: NULL argument");
+    int rc = check_cam(*cam, 0);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    fs::Work& w = ctx->work[0];
+    const fs::Camera k = to_cam(*cam);
+    const int ntiles = fs::tiles_x_of(k.width) * fs::tiles_y_of(k.height);
+    unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
+    fs::ViewCounters vc;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((rc = ensure_work(ctx, w, ctx->n, ntiles, cap, 1))) return rc;
+        enqueue_bin(ctx, w, k, 0.0, 0, fs::ProjectExport{});
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(w.stream));
+        CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
+        if (!vc.overflow) break;
+        cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull, (unsigned long long)vc.n_instances + 1024);
+    }
+    if (vc.overflow) return fail(FS_ENOMEM, "fs_bin: instance buffer overflow");
+    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
+    const int passes = (bits + 7) / 8;
+    // result parity: executed passes = passes (tile mask covers every digit)
+    const unsigned int* gids = w.ivals[passes & 1];
+    std::vector<unsigned int> starts(ntiles + 1);
+    CK(cudaMemcpy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost));
+    for (int t = 0; t <= ntiles; ++t) tile_offsets[t] = starts[t];
+    *n_items = vc.n_valid;
+    if (items) {
+        if (items_capacity < (int64_t)vc.n_valid) return fail(FS_EINVAL, "fs_bin: items buffer too small");
+        std::vector<unsigned int> g(vc.n_valid);
+        if (vc.n_valid)
+            CK(cudaMemcpy(g.data(), gids, sizeof(unsigned int) * vc.n_valid, cudaMemcpyDeviceToHost));
+        for (unsigned int i = 0; i < vc.n_valid; ++i) items[i] = g[i];
+    }
+    return FS_OK;
+}
+
+int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double* depth,
+                  const int64_t* radius, const int64_t* index, int width, int height,
+                  int64_t* tile_offsets, int64_t* items, int64_t items_capacity, int64_t* n_items) {
+    if (!ctx || !tile_offsets || !n_items || (k > 0 && (!mean2d || !depth || !radius || !index)))
+        return fail(FS_EINVAL, "fs_bin_splats: NULL argument");
+    if (k < 0 || k > 0x7fffffffLL) return fail(FS_EINVAL, "fs_bin_splats: bad splat count");
+    fs_camera c{};
+    c.width = width;
+    c.height = height;
+    int rc = check_cam(c, 0);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    fs::Work& w = ctx->work[0];
+    const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
+    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
+    const int passes = (bits + 7) / 8;
+    unsigned int cap = std::max(w.inst_cap, initial_inst_cap(k));
+    double *d_mean = nullptr, *d_depth = nullptr;
+    long long *d_rad = nullptr, *d_idx = nullptr;
+    const size_t k1 = (size_t)std::max<int64_t>(k, 1);
+    if ((rc = dev_alloc(&d_mean, 2 * k1)) || (rc = dev_alloc(&d_depth, k1)) ||
+        (rc = dev_alloc(&d_rad, k1)) || (rc = dev_alloc(&d_idx, k1)))
+        return rc;
+    if (k > 0) {
+        CK(cudaMemcpy(d_mean, mean2d, 16 * (size_t)k, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_depth, depth, 8 * (size_t)k, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_rad, radius, 8 * (size_t)k, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d_idx, index, 8 * (size_t)k, cudaMemcpyHostToDevice));
+    }
+    fs::ViewCounters vc{};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((rc = ensure_work(ctx, w, std::max<long long>(k, 1), ntiles, cap, 1))) return rc;
+        const unsigned long long init[2] = {0ull, ~0ull};
+        CK(cudaMemcpyAsync(w.idx_oa, init, sizeof(init), cudaMemcpyHostToDevice, w.stream));
+        fs::launch_view_begin(w.vc, w.stream);
+        fs::launch_bin_splats_keys((int)k, d_idx, d_mean, d_rad, d_depth, width, height, w.dkeys[0],
+                                   w.dvals[0], w.dkeys[1], w.dvals[1], w.rect, w.idx_oa, w.hist, w.vc,
+                                   ctx->num_sms, w.stream);
+        fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
+                                                  nullptr, (unsigned)k, &w.vc->key_or, 8, w.hist,
+                                                  ctx->num_sms, w.stream);
+        fs::BinBuffers b;
+        b.dkeys[0] = w.dkeys[0];
+        b.dkeys[1] = w.dkeys[1];
+        b.dvals[0] = w.dvals[0];
+        b.dvals[1] = w.dvals[1];
+        b.depth_or_and = &w.vc->key_or;
+        b.rect = w.rect;
+        b.block_sums = w.block_sums;
+        b.ikeys[0] = w.ikeys[0];
+        b.ikeys[1] = w.ikeys[1];
+        b.ivals[0] = w.ivals[0];
+        b.ivals[1] = w.ivals[1];
+        b.tile_or_and = ctx->tile_oa_table + 2 * bits;
+        b.hist = w.hist;
+        b.tile_start = w.tile_start;
+        b.capacity = w.inst_cap;
+        fs::launch_bin((int)k, ntiles, tx, passes, b, w.vc, ctx->num_sms, w.stream);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(w.stream));
+        CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
+        if (!vc.overflow) break;
+        cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull, (unsigned long long)vc.n_instances + 1024);
+    }
+    cudaFree(d_mean);
+    cudaFree(d_depth);
+    cudaFree(d_rad);
+    cudaFree(d_idx);
+    if (vc.overflow) return fail(FS_ENOMEM, "fs_bin_splats: instance buffer overflow");
+    std::vector<unsigned int> starts(ntiles + 1);
+    CK(cudaMemcpy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost));
+    for (int t = 0; t <= ntiles; ++t) tile_offsets[t] = starts[t];
+    *n_items = vc.n_valid;
+    if (items) {
+        if (items_capacity < (int64_t)vc.n_valid) return fail(FS_EINVAL, "fs_bin_splats: items buffer too small");
+        std::vector<unsigned int> g(vc.n_valid);
+        if (vc.n_valid)
+            CK(cudaMemcpy(g.data(), w.ivals[passes & 1], sizeof(unsigned int) * vc.n_valid,
+                          cudaMemcpyDeviceToHost));
+        for (unsigned int i = 0; i < vc.n_valid; ++i) items[i] = g[i];
+    }
+    return FS_OK;
+}
+
+int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uint16_t* const* masks,
+                  int masks_on_device, int num_objects, double alpha_floor, double t_floor,
+                  double* acc, fs_accumulate_stats* stats) {
+    if (!ctx) return fail(FS_EINVAL, "fs_accumulate: NULL context");
+    if (n_views < 0 || (n_views > 0 && (!cams || !masks)))
+        return fail(FS_EINVAL, "fs_accumulate: bad view arguments");
+    if (num_objects < 1 || num_objects > 65536)
+        return fail(FS_EINVAL, "fs_accumulate: num_objects must be in [1, 65536], got %d", num_objects);
+    if (!acc && ctx->n > 0) return fail(FS_EINVAL, "fs_accumulate: NULL accumulator");
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (n_views == 0 || ctx->n == 0) return FS_OK;
+    int rc;
+    int max_tiles = 1;
+    size_t max_px = 1;
+    long long view_px = 0;
+    for (int v = 0; v < n_views; ++v) {
+        if ((rc = check_cam(cams[v], v))) return rc;
+        if (!masks[v]) return fail(FS_EINVAL, "view %d: NULL mask", v);
+        max_tiles = std::max(max_tiles, fs::tiles_x_of(cams[v].width) * fs::tiles_y_of(cams[v].height));
+        max_px = std::max(max_px, (size_t)cams[v].width * cams[v].height);
+        view_px += (long long)cams[v].width * cams[v].height;
+    }
+    CK(cudaSetDevice(ctx->device));
+    for (auto& w : ctx->work) {
+        unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
+        if ((rc = ensure_work(ctx, w, ctx->n, max_tiles, cap, masks_on_device ? 1 : max_px))) return rc;
+    }
+    if (n_views > ctx->view_log_cap) {
+        if ((rc = dev_alloc(&ctx->view_log, (size_t)n_views))) return rc;
+        ctx->view_log_cap = n_views;
+    }
+    const int S = (int)ctx->work.size();
+    fs::Work& w0 = ctx->work[0];
+    CK(cudaEventRecord(ctx->ev_start, w0.stream));
+    for (int s = 1; s < S; ++s) CK(cudaStreamWaitEvent(ctx->work[s].stream, ctx->ev_start, 0));
+    for (int v = 0; v < n_views; ++v) {
+        fs::Work& w = ctx->work[v % S];
+        const uint16_t* mask = masks[v];
+        if (!masks_on_device) {
+            const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
+            if (w.h2d_pending) CK(cudaEventSynchronize(w.h2d_done));
+            memcpy(w.pinned, masks[v], bytes);
+            CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
+            CK(cudaEventRecord(w.h2d_done, w.stream));
+            w.h2d_pending = true;
+            mask = w.mask_dev;
+        }
+        enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
+                     ctx->view_log + v);
+    }
+    CK(cudaGetLastError());
+    for (int s = 1; s < S; ++s) {
+        CK(cudaEventRecord(ctx->work[s].done, ctx->work[s].stream));
+        CK(cudaStreamWaitEvent(w0.stream, ctx->work[s].done, 0));
+    }
+    CK(cudaEventRecord(ctx->ev_stop, w0.stream));
+    CK(cudaEventSynchronize(ctx->ev_stop));
+    for (auto& w : ctx->work) w.h2d_pending = false;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_stop));
+
+    std::vector<fs::ViewCounters> log(n_views);
+    CK(cudaMemcpy(log.data(), ctx->view_log, sizeof(fs::ViewCounters) * n_views, cudaMemcpyDeviceToHost));
+    // re-run views that overflowed the instance buffers (they contributed nothing)
+    long long retried = 0;
+    for (int v = 0; v < n_views; ++v) {
+        if (!log[v].overflow) continue;
+        fs::Work& w = w0;
+        unsigned int need = (unsigned int)std::min<unsigned long long>(
+            0x7fffffffull, (unsigned long long)log[v].n_instances + log[v].n_instances / 4 + 1024);
+        if ((rc = ensure_work(ctx, w, ctx->n, max_tiles, need, masks_on_device ? 1 : max_px))) return rc;
+        for (auto& o : ctx->work)  // later calls start with the grown capacity
+            if (o.inst_cap < need && (rc = ensure_work(ctx, o, ctx->n, max_tiles, need, 1))) return rc;
+        const uint16_t* mask = masks[v];
+        if (!masks_on_device) {
+            const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
+            memcpy(w.pinned, masks[v], bytes);
+            CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
+            mask = w.mask_dev;
+        }
+        enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
+                     ctx->view_log + v);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(w.stream));
+        CK(cudaMemcpy(&log[v], ctx->view_log + v, sizeof(fs::ViewCounters), cudaMemcpyDeviceToHost));
+        if (log[v].overflow) return fail(FS_ENOMEM, "view %d: instance buffer overflow after retry", v);
+        ++retried;
+    }
+    if (stats) {
+        stats->views = n_views;
+        stats->view_pixels = view_px;
+        for (const auto& l : log) {
+            stats->emitted += l.n_emitted;
+            stats->instances += l.n_instances;
+            stats->tile_steps += (int64_t)l.tile_steps;
+            stats->exact_evals += (int64_t)l.exact_evals;
+            stats->atomics += (int64_t)l.atomics;
+        }
+        stats->retried_views = retried;
+        stats->gpu_ms = ms;
+    }
+    return FS_OK;
+}
+
+int fs_finalize(fs_context* ctx, const double* acc, int64_t count, float* out, int out_on_device) {
+    if (!ctx || (!acc && count) || (!out && count)) return fail(FS_EINVAL, "fs_finalize: NULL argument");
+    if (count == 0) return FS_OK;
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->work[0].stream;
+    float* dst = out;
+    if (!out_on_device) {
+        int rc = dev_alloc(&dst, (size_t)count);
+        if (rc) return rc;
+    }
+    fs::launch_finalize(acc, dst, count, st);
+    CK(cudaGetLastError());
+    if (!out_on_device) {
+        CK(cudaMemcpyAsync(out, dst, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFree(dst);
+    } else {
+        CK(cudaStreamSynchronize(st));
+    }
+    return FS_OK;
+}
+
+int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float gamma, int mode,
+              uint8_t* out, int on_device) {
+    if ((!A || !out) && n > 0) return fail(FS_EINVAL, "fs_assign: NULL argument");
+    if (mode != FS_MODE_BINARY && mode != FS_MODE_SCENE) return fail(FS_EINVAL, "fs_assign: bad mode %d", mode);
+    if (mode == FS_MODE_BINARY && num_objects != 2)
+        return fail(FS_EINVAL, "binary assignment requires E=2, got E=%d", num_objects);
+    if (mode == FS_MODE_SCENE && num_objects < 2)
+        return fail(FS_EINVAL, "scene assignment requires E>=2, got E=%d", num_objects);
+    if (!(gamma >= -1.0f && gamma <= 1.0f)) return fail(FS_EINVAL, "gamma must lie in [-1, 1], got %g", (double)gamma);
+    if (n <= 0) return FS_OK;
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t in_bytes = sizeof(float) * (size_t)num_objects * n;
+    const size_t out_bytes = (mode == FS_MODE_BINARY ? 1 : (size_t)num_objects) * n;
+    const float* dA = A;
+    uint8_t* dout = out;
+    void *tmpA = nullptr, *tmpO = nullptr;
+    if (!on_device) {
+        CK(cudaMallocAsync(&tmpA, in_bytes, st));
+        CK(cudaMallocAsync(&tmpO, out_bytes, st));
+        CK(cudaMemcpyAsync(tmpA, A, in_bytes, cudaMemcpyHostToDevice, st));
+        dA = static_cast<const float*>(tmpA);
+        dout = static_cast<uint8_t*>(tmpO);
+    }
+    fs::launch_assign(dA, n, num_objects, gamma, mode, dout, st);
+    CK(cudaGetLastError());
+    if (!on_device) {
+        CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(tmpA, st));
+        CK(cudaFreeAsync(tmpO, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return FS_OK;
+}
+
+}  // extern "C"

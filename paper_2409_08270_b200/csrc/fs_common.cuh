@@ -1,0 +1,95 @@
+// fs_common.cuh -- shared device types and helpers for the FlashSplat B200 label solver.
+//
+// Numerics contract: every quantity that feeds a
+// discrete decision of the reference (cull, radius, tile range, depth order,
+// alpha floor, transmittance floor) or a contribution weight is computed in
+// float64 with the reference's operation order and without FMA contraction
+// (explicit __d*_rn intrinsics or -fmad=false).  float32 is only used for a
+// conservative pre-screen that rejects samples whose alpha is certainly
+// below the floor.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fs {
+
+constexpr int kTile = 16;             // rasterizer.py:31
+constexpr int kTilePixels = kTile * kTile;
+constexpr double kDilation = 0.3;     // scene.py:25
+constexpr double kAlphaClamp = 0.99;  // scene.py:26
+constexpr double kDegenerateDet = 1e-12;  // scene.py:27
+
+// Per-view camera, passed by value to kernels (scene.py:164-203).
+struct Camera {
+    int32_t width, height;
+    double fx, fy, cx, cy;
+    double w2c[16];
+    double near_clip;
+};
+
+// float32 screen record of one projected Gaussian (32 B, one per gid).
+// cut: power threshold below which alpha < alpha_floor for sure;
+// hx, hy: half extents of the alpha-floor ellipse (pixel units, inflated).
+struct __align__(16) Rec32 {
+    float mx, my, a, b, c, cut, hx, hy;
+};
+
+// float64 record used for the exact contribution (48 B, one per gid).
+struct __align__(16) Rec64 {
+    double mx, my, a, b, c, o;
+};
+
+// Per-view device counters (reset at the start of every view).
+struct ViewCounters {
+    unsigned long long key_or;   // OR of visible depth keys
+    unsigned long long key_and;  // AND of visible depth keys
+    unsigned int n_emitted;      // visible after all culls (scene.py:311)
+    unsigned int n_behind;
+    unsigned int n_degenerate;
+    unsigned int n_offscreen;
+    unsigned int n_instances;    // (tile, gaussian) pairs emitted
+    unsigned int n_valid;        // n_instances, or 0 when it overflowed the buffers
+    unsigned int overflow;       // instances exceeded capacity -> view skipped
+    unsigned long long tile_steps;   // list entries walked by the raster kernel
+    unsigned long long exact_evals;  // float64 alpha evaluations
+    unsigned long long atomics;      // global accumulator atomics issued
+};
+
+// Device-side projection export for the stage-level API (scene.py:252-312).
+struct ProjectExport {
+    uint8_t* alive;
+    double* mean2d;  // N x 2
+    double* conic;   // N x 3
+    double* depth;   // N
+    int64_t* radius; // N
+};
+
+__host__ __device__ inline int tiles_x_of(int w) { return (w + kTile - 1) / kTile; }
+__host__ __device__ inline int tiles_y_of(int h) { return (h + kTile - 1) / kTile; }
+
+// Order-preserving map of a float64 to uint64 (valid for all non-NaN values).
+__device__ __forceinline__ unsigned long long f64_sort_key(double z) {
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(z));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Packed inclusive tile rectangle: tx0 | tx1 << 16 | ty0 << 32 | ty1 << 48.
+// Empty rectangles (tx0 > tx1 or ty0 > ty1) are stored as 0xFFFF... -> count 0.
+__device__ __forceinline__ unsigned int rect_count(unsigned long long r) {
+    if (r == ~0ull) return 0u;
+    unsigned int tx0 = r & 0xFFFF, tx1 = (r >> 16) & 0xFFFF;
+    unsigned int ty0 = (r >> 32) & 0xFFFF, ty1 = (r >> 48) & 0xFFFF;
+    return (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+}
+
+// Records a CUDA failure as the thread's last error; returns FS_ECUDA.
+int set_cuda_error(cudaError_t e, const char* expr, const char* file, int line);
+
+}  // namespace fs
+
+#define FS_CUDA_CHECK(expr)                                                    \
+    do {                                                                       \
+        cudaError_t _e = (expr);                                               \
+        if (_e != cudaSuccess) return fs::set_cuda_error(_e, #expr, __FILE__, __LINE__); \
+    } while (0)

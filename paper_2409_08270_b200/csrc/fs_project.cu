@@ -1,0 +1,292 @@
+// fs_project.cu -- K0 scene setup and K1 EWA projection (reference scene.py:228-312).
+//
+// Compiled with -fmad=false: every float64 expression below is evaluated in
+// the same operation order as the numpy code it restates, with no FMA
+// contraction, so the projected means / conics / depths / radii agree with the
+// reference to the last ulp except where the reference's BLAS 3x3 matmul
+// orders its sums differently.
+//
+// Layout: the resident scene is structure-of-arrays float64 (means x/y/z,
+// the six unique entries of the world covariance, opacity) so a warp reads
+// 32 consecutive doubles per field (coalesced 256 B).  The covariance is
+// view-independent (scene.py:245-249) and is computed once per scene.
+#include "fs_common.cuh"
+#include "fs_kernels.cuh"
+
+namespace fs {
+
+// K0: AoS host layout (means N x 3, unit quats N x 4, scales N x 3) -> SoA
+// means + world covariance Sigma = (R S)(R S)^T (scene.py:228-249).
+__global__ void scene_setup_kernel(int n, const double* __restrict__ means_aos,
+                                   const double* __restrict__ quats_aos,
+                                   const double* __restrict__ scales_aos, double* __restrict__ mx,
+                                   double* __restrict__ my, double* __restrict__ mz,
+                                   double* __restrict__ sig /* 6 x n */) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        mx[i] = means_aos[3 * i + 0];
+        my[i] = means_aos[3 * i + 1];
+        mz[i] = means_aos[3 * i + 2];
+        double w = quats_aos[4 * i + 0], x = quats_aos[4 * i + 1];
+        double y = quats_aos[4 * i + 2], z = quats_aos[4 * i + 3];
+        double r[9];
+        r[0] = 1.0 - 2.0 * (y * y + z * z);
+        r[1] = 2.0 * (x * y - w * z);
+        r[2] = 2.0 * (x * z + w * y);
+        r[3] = 2.0 * (x * y + w * z);
+        r[4] = 1.0 - 2.0 * (x * x + z * z);
+        r[5] = 2.0 * (y * z - w * x);
+        r[6] = 2.0 * (x * z - w * y);
+        r[7] = 2.0 * (y * z + w * x);
+        r[8] = 1.0 - 2.0 * (x * x + y * y);
+        double s0 = scales_aos[3 * i + 0], s1 = scales_aos[3 * i + 1], s2 = scales_aos[3 * i + 2];
+        double m[9];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            m[3 * k + 0] = r[3 * k + 0] * s0;
+            m[3 * k + 1] = r[3 * k + 1] * s1;
+            m[3 * k + 2] = r[3 * k + 2] * s2;
+        }
+        // Sigma[i][j] = sum_k m[i][k] m[j][k]; symmetric bit-for-bit (same products, same order)
+        auto dot = [&](int a, int b) {
+            return m[3 * a + 0] * m[3 * b + 0] + m[3 * a + 1] * m[3 * b + 1] + m[3 * a + 2] * m[3 * b + 2];
+        };
+        sig[0 * (size_t)n + i] = dot(0, 0);
+        sig[1 * (size_t)n + i] = dot(0, 1);
+        sig[2 * (size_t)n + i] = dot(0, 2);
+        sig[3 * (size_t)n + i] = dot(1, 1);
+        sig[4 * (size_t)n + i] = dot(1, 2);
+        sig[5 * (size_t)n + i] = dot(2, 2);
+    }
+}
+
+__device__ __forceinline__ void warp_or_and(unsigned long long& o, unsigned long long& a) {
+    unsigned int olo = __reduce_or_sync(0xffffffffu, (unsigned int)o);
+    unsigned int ohi = __reduce_or_sync(0xffffffffu, (unsigned int)(o >> 32));
+    unsigned int alo = __reduce_and_sync(0xffffffffu, (unsigned int)a);
+    unsigned int ahi = __reduce_and_sync(0xffffffffu, (unsigned int)(a >> 32));
+    o = ((unsigned long long)ohi << 32) | olo;
+    a = ((unsigned long long)ahi << 32) | alo;
+}
+
+// K1: one thread per Gaussian.  Mirrors _project_arrays (scene.py:252-312)
+// and tile_range (rasterizer.py:106-113); emits the depth sort key, the tile
+// rectangle and the walk records.  cull_floor > 0 additionally drops (from
+// binning only) Gaussians whose opacity is below the alpha floor: they can
+// never pass `alpha >= alpha_floor` (contributions.py:148), so they touch no
+// pixel.  Stats keep the reference's meaning regardless.
+__global__ void __launch_bounds__(256) project_kernel(
+    int n, const double* __restrict__ gmx, const double* __restrict__ gmy,
+    const double* __restrict__ gmz, const double* __restrict__ sig,
+    const double* __restrict__ opac, Camera cam, double alpha_floor, int cull_floor,
+    unsigned long long* __restrict__ keys, unsigned int* __restrict__ vals,
+    unsigned long long* __restrict__ rect, Rec32* __restrict__ r32, Rec64* __restrict__ r64,
+    ViewCounters* __restrict__ vc, ProjectExport ex) {
+    const double* W = cam.w2c;
+    const int tx_n = tiles_x_of(cam.width), ty_n = tiles_y_of(cam.height);
+    __shared__ unsigned long long s_or[8], s_and[8];
+    __shared__ unsigned int s_cnt[4];
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long k_or = 0, k_and = ~0ull;
+    unsigned int c_emit = 0, c_behind = 0, c_deg = 0, c_off = 0;
+    // grid-stride, but every thread runs the same number of iterations so the
+    // warp reductions below stay convergent
+    const int stride = gridDim.x * blockDim.x;
+    const int iters = (n + stride - 1) / stride;
+    for (int it = 0; it < iters; ++it) {
+        const int i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+        if (i < n) {
+            double m0 = gmx[i], m1 = gmy[i], m2 = gmz[i];
+            // cam = means @ rot.T + t   (scene.py:266)
+            double x = (m0 * W[0] + m1 * W[1] + m2 * W[2]) + W[3];
+            double y = (m0 * W[4] + m1 * W[5] + m2 * W[6]) + W[7];
+            double z = (m0 * W[8] + m1 * W[9] + m2 * W[10]) + W[11];
+            bool alive = z > cam.near_clip;  // :268
+            if (!alive) ++c_behind;
+            double zs = alive ? z : 1.0;      // :272
+            double mxp = cam.fx * x / zs + cam.cx;  // :274-275
+            double myp = cam.fy * y / zs + cam.cy;
+            double S[9];
+            S[0] = sig[i];
+            S[1] = sig[(size_t)n + i];
+            S[2] = sig[2 * (size_t)n + i];
+            S[4] = sig[3 * (size_t)n + i];
+            S[5] = sig[4 * (size_t)n + i];
+            S[8] = sig[5 * (size_t)n + i];
+            S[3] = S[1];
+            S[6] = S[2];
+            S[7] = S[5];
+            // sigma_cam = rot @ sigma @ rot.T  (:278)
+            double T[9], C[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    T[3 * a + b] = W[4 * a + 0] * S[0 + b] + W[4 * a + 1] * S[3 + b] + W[4 * a + 2] * S[6 + b];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b)
+                    C[3 * a + b] = T[3 * a + 0] * W[4 * b + 0] + T[3 * a + 1] * W[4 * b + 1] + T[3 * a + 2] * W[4 * b + 2];
+            // J (:280-284) and cov2d = J C J^T (:285)
+            double j00 = cam.fx / zs, j02 = -cam.fx * x / (zs * zs);
+            double j11 = cam.fy / zs, j12 = -cam.fy * y / (zs * zs);
+            double js0[3], js1[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                js0[c] = j00 * C[0 + c] + 0.0 * C[3 + c] + j02 * C[6 + c];
+                js1[c] = 0.0 * C[0 + c] + j11 * C[3 + c] + j12 * C[6 + c];
+            }
+            double c00 = js0[0] * j00 + js0[1] * 0.0 + js0[2] * j02;
+            double c01 = js0[0] * 0.0 + js0[1] * j11 + js0[2] * j12;
+            double c11 = js1[0] * 0.0 + js1[1] * j11 + js1[2] * j12;
+            double a = c00 + kDilation, b = c01, c = c11 + kDilation;  // :286-288
+            double det = a * c - b * b;                                // :290
+            if (alive && det <= kDegenerateDet) {
+                ++c_deg;
+                alive = false;
+            }
+            double ds = det > kDegenerateDet ? det : 1.0;  // :295
+            double ia = c / ds, ib = -b / ds, ic = a / ds; // :296
+            double mid = 0.5 * (a + c);                     // :298-301
+            double disc = sqrt(fmax(0.25 * ((a - c) * (a - c)) + b * b, 0.0));
+            double lam = fmax(mid + disc, 0.0);
+            double rad = ceil(3.0 * sqrt(lam));
+            if (alive && ((mxp + rad < 0.0) || (mxp - rad > (double)cam.width) ||
+                          (myp + rad < 0.0) || (myp - rad > (double)cam.height))) {
+                ++c_off;  // :303-310
+                alive = false;
+            }
+            double o = opac[i];
+            unsigned long long key = ~0ull, rc = ~0ull;
+            if (alive) {
+                ++c_emit;
+                key = f64_sort_key(z);
+                k_or |= key;
+                k_and &= key;
+                // tile_range (rasterizer.py:106-113), inclusive floor box
+                double fx0 = floor((mxp - rad) / kTile), fx1 = floor((mxp + rad) / kTile);
+                double fy0 = floor((myp - rad) / kTile), fy1 = floor((myp + rad) / kTile);
+                int tx0 = fx0 < 0.0 ? 0 : (fx0 > tx_n ? tx_n : (int)fx0);
+                int tx1 = fx1 > tx_n - 1 ? tx_n - 1 : (fx1 < -1.0 ? -1 : (int)fx1);
+                int ty0 = fy0 < 0.0 ? 0 : (fy0 > ty_n ? ty_n : (int)fy0);
+                int ty1 = fy1 > ty_n - 1 ? ty_n - 1 : (fy1 < -1.0 ? -1 : (int)fy1);
+                bool transparent = cull_floor && alpha_floor > 0.0 && !(o >= alpha_floor);
+                if (tx0 <= tx1 && ty0 <= ty1 && !transparent)
+                    rc = (unsigned long long)tx0 | ((unsigned long long)tx1 << 16) |
+                         ((unsigned long long)ty0 << 32) | ((unsigned long long)ty1 << 48);
+            }
+            keys[i] = key;
+            vals[i] = (unsigned int)i;
+            rect[i] = rc;
+            // walk records (float64 exact, float32 screen)
+            Rec64 q;
+            q.mx = mxp;
+            q.my = myp;
+            q.a = ia;
+            q.b = ib;
+            q.c = ic;
+            q.o = o;
+            r64[i] = q;
+            Rec32 s;
+            s.mx = (float)mxp;
+            s.my = (float)myp;
+            s.a = (float)ia;
+            s.b = (float)ib;
+            s.c = (float)ic;
+            if (alpha_floor > 0.0 && o >= alpha_floor && alive) {
+                // alpha >= floor  <=>  power >= log(floor / o)  <=>  d^T conic d <= qmax
+                double qmax = 2.0 * log(o / alpha_floor);
+                double hx = sqrt(qmax * a) * (1.0 + 1e-5) + 0.01;
+                double hy = sqrt(qmax * c) * (1.0 + 1e-5) + 0.01;
+                double spread = (fabs(ia) + fabs(ic) + 2.0 * fabs(ib)) * (hx * hx + hy * hy);
+                double margin = 0.02 + 1e-6 * spread;
+                s.cut = (float)(log(alpha_floor / o) - margin);
+                s.hx = (float)hx;
+                s.hy = (float)hy;
+            } else if (alpha_floor > 0.0) {
+                s.cut = __int_as_float(0x7f800000);  // +inf: never passes
+                s.hx = 0.0f;
+                s.hy = 0.0f;
+            } else {
+                s.cut = __int_as_float(0xff800000);  // -inf: exact blend, no screen
+                s.hx = __int_as_float(0x7f800000);
+                s.hy = __int_as_float(0x7f800000);
+            }
+            r32[i] = s;
+            if (ex.alive) {
+                ex.alive[i] = alive ? 1 : 0;
+                ex.mean2d[2 * i] = mxp;
+                ex.mean2d[2 * i + 1] = myp;
+                ex.conic[3 * i] = ia;
+                ex.conic[3 * i + 1] = ib;
+                ex.conic[3 * i + 2] = ic;
+                ex.depth[i] = z;
+                ex.radius[i] = (int64_t)rad;
+            }
+        }
+    }
+    // block reduction of the counters and of the key OR/AND
+    warp_or_and(k_or, k_and);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        s_or[warp] = k_or;
+        s_and[warp] = k_and;
+    }
+    atomicAdd(&s_cnt[0], c_emit);
+    atomicAdd(&s_cnt[1], c_behind);
+    atomicAdd(&s_cnt[2], c_deg);
+    atomicAdd(&s_cnt[3], c_off);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long o = 0, a = ~0ull;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            o |= s_or[w];
+            a &= s_and[w];
+        }
+        if (s_cnt[0]) {
+            atomicOr(&vc->key_or, o);
+            atomicAnd(&vc->key_and, a);
+            atomicAdd(&vc->n_emitted, s_cnt[0]);
+        }
+        if (s_cnt[1]) atomicAdd(&vc->n_behind, s_cnt[1]);
+        if (s_cnt[2]) atomicAdd(&vc->n_degenerate, s_cnt[2]);
+        if (s_cnt[3]) atomicAdd(&vc->n_offscreen, s_cnt[3]);
+    }
+}
+
+// Resets the per-view counters (first node of every view).
+__global__ void view_begin_kernel(ViewCounters* vc) {
+    if (threadIdx.x == 0) {
+        ViewCounters z{};
+        z.key_or = 0;
+        z.key_and = ~0ull;
+        *vc = z;
+    }
+}
+
+void launch_view_begin(ViewCounters* vc, cudaStream_t st) { view_begin_kernel<<<1, 32, 0, st>>>(vc); }
+
+void launch_scene_setup(int n, const double* means, const double* quats, const double* scales,
+                        double* mx, double* my, double* mz, double* sig, cudaStream_t st) {
+    if (n <= 0) return;
+    int grid = (n + 255) / 256;
+    if (grid > 4096) grid = 4096;
+    scene_setup_kernel<<<grid, 256, 0, st>>>(n, means, quats, scales, mx, my, mz, sig);
+}
+
+void launch_project(int n, const double* mx, const double* my, const double* mz,
+                    const double* sig, const double* opac, const Camera& cam, double alpha_floor,
+                    int cull_floor, unsigned long long* keys, unsigned int* vals,
+                    unsigned long long* rect, Rec32* r32, Rec64* r64, ViewCounters* vc,
+                    ProjectExport ex, int num_sms, cudaStream_t st) {
+    view_begin_kernel<<<1, 32, 0, st>>>(vc);
+    if (n <= 0) return;
+    int grid = (n + 255) / 256;
+    int cap = num_sms * 8;
+    if (grid > cap) grid = cap;
+    project_kernel<<<grid, 256, 0, st>>>(n, mx, my, mz, sig, opac, cam, alpha_floor, cull_floor,
+                                         keys, vals, rect, r32, r64, vc, ex);
+}
+
+}  // namespace fs

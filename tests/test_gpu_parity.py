@@ -1,0 +1,325 @@
+"""GPU parity: the CUDA library (through its C ABI) against the reference's
+golden vectors and the pinned CPU oracle on the same seeded inputs."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import cam_from_row, load_golden
+
+pytestmark = pytest.mark.gpu
+
+fs = pytest.importorskip("paper_2409_08270_b200")
+from paper_2409_08270_b200 import (  # noqa: E402
+    DEFAULT_BLEND,
+    EXACT_BLEND,
+    ContributionMatrix,
+    GaussianScene,
+    LabelMask,
+    LabelSolver,
+    ProjectedGaussian,
+    accumulate_contributions,
+    assign_binary,
+    assign_scene,
+    bin_gaussians_to_tiles,
+    project_scene,
+)
+from paper_2409_08270_b200 import _native, synth  # noqa: E402
+
+PROJ = load_golden("projection")
+BIN = load_golden("binning")
+ACC = load_golden("accumulate")
+ASG = load_golden("assign")
+
+
+def scene_from(c, prefix="in_"):
+    return GaussianScene(c[prefix + "means"], c[prefix + "quats"], c[prefix + "scales"],
+                         c.get(prefix + "opac", np.full(len(c[prefix + "means"]), 0.5)))
+
+
+def views_masks(c):
+    src = c if "cams" in c else ACC["C1_default"]
+    masks = c["masks"] if "masks" in c else ACC["C1_default"]["masks"]
+    cams = [cam_from_row(r, i) for i, r in enumerate(src["cams"])]
+    return cams, masks
+
+
+# ----------------------------------------------------------------- projection
+@pytest.mark.parametrize("case", sorted(PROJ))
+def test_projection_matches_reference(case):
+    c = PROJ[case]
+    ctx = _native.context(0)
+    with ctx.lock:
+        ctx.set_arrays(c["in_means"], c["in_quats"], c["in_scales"], c["in_opac"])
+        alive, mean2d, conic, depth, radius, stats = ctx.project(cam_from_row(c["cam"]))
+    assert np.array_equal(alive, c["alive"])
+    assert np.array_equal(np.array(stats), c["stats"])
+    a = c["alive"]
+    assert np.array_equal(radius[a], c["radius"][a])
+    np.testing.assert_allclose(mean2d[a], c["mean2d"][a], rtol=1e-13, atol=1e-12)
+    np.testing.assert_allclose(conic[a], c["conic"][a], rtol=1e-11, atol=1e-14)
+    np.testing.assert_allclose(depth, c["depth"], rtol=1e-15, atol=0)
+
+
+def test_projection_bit_identical_to_oracle(rng):
+    wl = synth.make_workload(seed=3, n_gaussians=20000, n_views=2, width=200, height=150,
+                             num_objects=2, scale_range=(0.01, 0.1))
+    ctx = _native.context(0)
+    for v in wl.views:
+        with ctx.lock:
+            ctx.set_scene(wl.scene)
+            g = ctx.project(v)
+        o = oracle.project(wl.scene.means, wl.scene.rotations, wl.scene.scales, oracle.camera_of(v))
+        assert np.array_equal(g[0], o[0])
+        for k in (1, 2, 3, 4):
+            assert np.array_equal(g[k][g[0]], o[k][o[0]]), k  # same op order, no FMA
+        assert list(g[5]) == list(o[5])
+
+
+def test_project_scene_api_and_member_subset():
+    c = PROJ["c0"]
+    scene = scene_from(c)
+    view = cam_from_row(c["cam"])
+    splats, stats = project_scene(scene, view)
+    idx = np.flatnonzero(c["alive"])
+    assert [p.gaussian_index for p in splats] == idx.tolist()
+    assert stats.n_emitted == len(splats)
+    member = np.zeros(len(scene), bool)
+    member[::3] = True
+    sub, _ = project_scene(scene, view, member_mask=member)
+    assert [p.gaussian_index for p in sub] == [i for i in idx.tolist() if i % 3 == 0]
+
+
+# -------------------------------------------------------------------- binning
+@pytest.mark.parametrize("case", sorted(k for k in BIN if k != "tile_range"))
+def test_scene_binning_matches_reference(case):
+    c = BIN[case]
+    ctx = _native.context(0)
+    with ctx.lock:
+        ctx.set_arrays(c["in_means"], c["in_quats"], c["in_scales"], c["in_opac"])
+        offs, items = ctx.bin(cam_from_row(c["cam"]))
+    assert np.array_equal(offs, c["offsets"])
+    assert np.array_equal(items, c["items"])
+
+
+@pytest.mark.parametrize("case", sorted(k for k in BIN if k != "tile_range"))
+def test_tilebinning_api_matches_reference(case):
+    c = BIN[case]
+    scene = scene_from(c)
+    view = cam_from_row(c["cam"])
+    splats, _ = project_scene(scene, view)
+    b = bin_gaussians_to_tiles(splats, view)
+    got = [b.indices[lst] for lst in b.tile_lists]
+    offs = c["offsets"]
+    want = [c["items"][offs[t]:offs[t + 1]] for t in range(len(offs) - 1)]
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def _splat(i, mx, my, depth, radius):
+    return ProjectedGaussian(gaussian_index=i, mean2d=np.array([mx, my], float),
+                             inv_cov2d=np.eye(2), depth=depth, radius=radius)
+
+
+def test_binning_known_answers():
+    # reference tests/test_rasterizer.py:28-50
+    from paper_2409_08270_b200 import CameraView
+    v = CameraView(0, 40, 24, 24.0, 24.0, 20.5, 12.5, np.eye(4))
+    b = bin_gaussians_to_tiles([_splat(0, 20.0, 12.0, 1.0, 64)], v)
+    assert (b.tiles_x, b.tiles_y) == (3, 2)
+    assert all(len(lst) == 1 for lst in b.tile_lists)
+    v = CameraView(0, 16, 16, 24.0, 24.0, 8.5, 8.5, np.eye(4))
+    b = bin_gaussians_to_tiles([_splat(0, 8.0, 8.0, 2.0, 2), _splat(1, 9.0, 8.0, 1.0, 2)], v)
+    assert b.depths[b.tile_lists[0][0]] == 1.0 and b.depths[b.tile_lists[0][1]] == 2.0
+    b = bin_gaussians_to_tiles([_splat(5, 8.0, 8.0, 1.0, 2), _splat(2, 9.0, 8.0, 1.0, 2)], v)
+    assert b.indices[b.tile_lists[0][0]] == 2 and b.indices[b.tile_lists[0][1]] == 5
+    # empty tile range (rasterizer.py:106-113): mx - r == W
+    b = bin_gaussians_to_tiles([_splat(0, 19.0, 8.0, 1.0, 3)], v)
+    assert sum(len(lst) for lst in b.tile_lists) == 0
+
+
+def test_binning_heavy_ties_matches_oracle():
+    rng = np.random.default_rng(5)
+    n = 30000
+    means = np.stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n),
+                      rng.choice([3.0, 3.25, 3.5], size=n)], axis=1)
+    q = rng.normal(size=(n, 4))
+    scene = GaussianScene(means, q, rng.uniform(0.005, 0.05, (n, 3)), rng.uniform(0.1, 0.9, n))
+    from paper_2409_08270_b200 import CameraView
+    view = CameraView(0, 333, 250, 300.0, 300.0, 166.5, 125.5, np.eye(4))
+    ctx = _native.context(0)
+    with ctx.lock:
+        ctx.set_scene(scene)
+        offs, items = ctx.bin(view)
+    alive, mean2d, _, depth, radius, _ = oracle.project(scene.means, scene.rotations, scene.scales,
+                                                       oracle.camera_of(view))
+    o_offs, o_items = oracle.bin_tiles(alive, mean2d, depth, radius, view.width, view.height)
+    assert np.array_equal(offs, o_offs)
+    assert np.array_equal(items, o_items)
+
+
+# --------------------------------------------------------------- accumulation
+def _golden_inputs(case):
+    c = ACC[case]
+    src = c if "in_means" in c else ACC["C1_default"]
+    scene = GaussianScene(src["in_means"], src["in_quats"], src["in_scales"], src["in_opac"])
+    cams, masks = views_masks(c)
+    if case == "C1_exact_2views":
+        cams, masks = cams[:2], masks[:2]
+    blend = fs.BlendConfig(float(c["floors"][0]), float(c["floors"][1]))
+    pairs = [(v, LabelMask(v.view_id, m)) for v, m in zip(cams, masks)]
+    return c, scene, pairs, blend
+
+
+@pytest.mark.parametrize("case", sorted(k for k in ACC if not k.startswith("synth")))
+def test_accumulate_matches_reference_golden(case):
+    c, scene, pairs, blend = _golden_inputs(case)
+    A = accumulate_contributions(scene, pairs, int(c["E"]), blend).values
+    ref = c["A"]
+    # float64 walk + float64 accumulation: only the summation order differs
+    np.testing.assert_allclose(A, c["A64"], rtol=1e-6, atol=1e-9)
+    differ = int(np.count_nonzero(A != ref))
+    assert differ <= max(2, ref.size // 1000), f"{differ} of {ref.size} entries not bit-identical"
+
+
+@pytest.mark.parametrize("name", ["synth_coherent", "synth_iid", "synth_dense"])
+def test_accumulate_synthetic_matches_reference_golden(name):
+    c = ACC[name]
+    kw = dict(eval(bytes(c["gen_args"]).decode()))
+    wl = synth.make_workload(**kw)
+    assert wl.digest() == bytes(c["digest"]).decode()
+    A = accumulate_contributions(wl.scene, wl.pairs(), wl.num_objects).values
+    np.testing.assert_allclose(A, c["A"], rtol=1e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("blend", [DEFAULT_BLEND, EXACT_BLEND], ids=["default", "exact"])
+@pytest.mark.parametrize("iid", [False, True], ids=["coherent", "iid"])
+def test_accumulate_matches_oracle_medium(blend, iid):
+    wl = synth.make_workload(seed=21, n_gaussians=40000, n_views=3, width=320, height=240,
+                             num_objects=6, iid_masks=iid)
+    A = accumulate_contributions(wl.scene, wl.pairs(), 6, blend).values
+    cams = [oracle.camera_of(v) for v in wl.views]
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, cams, list(wl.masks), 6, blend.alpha_floor,
+                            blend.transmittance_floor, threads=8, as_float32=False)
+    np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+
+
+def test_kat_single_gaussian():
+    # reference tests/test_contributions.py:26-36
+    c, scene, pairs, blend = _golden_inputs("kat_single_default")
+    A = accumulate_contributions(scene, pairs, 2).values
+    assert A[1, 0] == pytest.approx(17.71578278407129, abs=1e-4)
+    assert A[0, 0] == 0.0
+
+
+def test_reference_contract_properties(rng):
+    wl = synth.make_workload(seed=4, n_gaussians=3000, n_views=4, width=64, height=48,
+                             num_objects=3, iid_masks=True)
+    pairs = wl.pairs()
+    whole = accumulate_contributions(wl.scene, pairs, 3).values
+    a = accumulate_contributions(wl.scene, pairs[:2], 3).values
+    b = accumulate_contributions(wl.scene, pairs[2:], 3).values
+    assert np.abs(a + b - whole).max() < 1e-5                      # additivity (:79-87)
+    back = accumulate_contributions(wl.scene, pairs[::-1], 3).values
+    assert np.abs(back - whole).max() < 1e-5                       # permutation (:89-95)
+    assert np.all(whole >= 0.0)                                    # (:124-131)
+    assert whole.sum() <= wl.view_pixels() + 1e-3
+    again = accumulate_contributions(wl.scene, pairs, 3).values
+    assert again.tobytes() == whole.tobytes()                      # rerun determinism (:160-168)
+    bg = [(v, LabelMask(v.view_id, np.zeros_like(m.labels))) for v, m in pairs]
+    only0 = accumulate_contributions(wl.scene, bg, 3).values
+    assert only0[0].sum() > 0 and np.all(only0[1:] == 0.0)         # (:38-43)
+
+
+def test_validation_messages():
+    c, scene, pairs, _ = _golden_inputs("random_11_d")
+    v, m = pairs[0]
+    with pytest.raises(ValueError, match="does not match"):
+        accumulate_contributions(scene, [(v, LabelMask(v.view_id, m.labels[:8]))], 3)
+    lab = np.zeros_like(m.labels)
+    lab[3, 7] = 5
+    with pytest.raises(ValueError, match=r"view 0.*label 5.*\(3, 7\)"):
+        accumulate_contributions(scene, [(v, LabelMask(v.view_id, lab))], 3)
+
+
+def test_edge_cases():
+    from paper_2409_08270_b200 import CameraView
+    empty = GaussianScene(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0))
+    v = CameraView(0, 17, 9, 20.0, 20.0, 8.5, 4.5, np.eye(4))
+    m = LabelMask(0, np.ones((9, 17), np.uint16))
+    assert accumulate_contributions(empty, [(v, m)], 2).values.shape == (2, 0)
+    # nothing visible: everything behind the camera
+    behind = GaussianScene([[0, 0, -2.0]] * 5, [[1, 0, 0, 0]] * 5, [[0.1] * 3] * 5, [0.5] * 5)
+    assert np.all(accumulate_contributions(behind, [(v, m)], 2).values == 0)
+    # 1 x 1 image, no views, many labels
+    one = CameraView(0, 1, 1, 2.0, 2.0, 0.5, 0.5, np.eye(4))
+    g = GaussianScene([[0, 0, 2.0]], [[1, 0, 0, 0]], [[0.3] * 3], [0.9])
+    A = accumulate_contributions(g, [(one, LabelMask(0, np.full((1, 1), 299, np.uint16)))], 300)
+    assert A.values.shape == (300, 1) and A.values[299, 0] > 0 and A.values[:299].sum() == 0
+    assert accumulate_contributions(g, [], 2).values.sum() == 0
+
+
+def test_instance_overflow_retry():
+    # 1500 Gaussians covering a 4K image: 1500 x 8160 tiles > initial capacity
+    from paper_2409_08270_b200 import CameraView
+    n = 1500
+    rng = np.random.default_rng(0)
+    scene = GaussianScene(np.c_[rng.uniform(-0.1, 0.1, (n, 2)), rng.uniform(2, 3, n)],
+                          np.tile([1.0, 0, 0, 0], (n, 1)), np.full((n, 3), 2.0),
+                          rng.uniform(0.01, 0.02, n))
+    v = CameraView(0, 1920, 1088, 1000.0, 1000.0, 960.0, 544.0, np.eye(4))
+    m = LabelMask(0, rng.integers(0, 2, (1088, 1920), dtype=np.uint16))
+    st = {}
+    A = accumulate_contributions(scene, [(v, m)], 2, stats=st).values
+    assert st["instances"] > 4 * n
+    cams = [oracle.camera_of(v)]
+    ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities, cams,
+                            [m.labels], 2, threads=8)
+    np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+
+
+# ----------------------------------------------------------------- assignment
+@pytest.mark.parametrize("case", sorted(ASG))
+def test_assign_bit_exact_vs_reference(case):
+    c = ASG[case]
+    M = ContributionMatrix(c["A"])
+    for i, g in enumerate(c["gammas"]):
+        assert np.array_equal(assign_scene(M, g).membership, c["scene"][i]), (case, g)
+        if "binary" in c:
+            assert np.array_equal(assign_binary(M, g).labels, c["binary"][i]), (case, g)
+
+
+def test_assign_large_random_vs_oracle(rng):
+    for e in (2, 5, 32):
+        A = (rng.random((e, 300_001)) * rng.choice([1e-13, 1e-3, 1.0, 1e4], (1, 300_001))).astype(np.float32)
+        A[:, :100] = 0
+        for g in (-0.7, 0.0, 0.25):
+            assert np.array_equal(assign_scene(ContributionMatrix(A), g).membership,
+                                  oracle.assign_scene(A, g))
+            if e == 2:
+                assert np.array_equal(assign_binary(ContributionMatrix(A), g).labels,
+                                      oracle.assign_binary(A, g))
+
+
+def test_assign_errors():
+    with pytest.raises(ValueError, match="E=2"):
+        assign_binary(ContributionMatrix(np.zeros((3, 4), np.float32)), 0.0)
+    with pytest.raises(ValueError, match="gamma"):
+        assign_binary(ContributionMatrix(np.zeros((2, 4), np.float32)), 1.5)
+    with pytest.raises(ValueError, match="E>=2"):
+        assign_scene(ContributionMatrix(np.zeros((1, 4), np.float32)), 0.0)
+
+
+def test_label_solver_resident_matrix():
+    wl = synth.make_workload(seed=8, n_gaussians=20000, n_views=3, width=160, height=120,
+                             num_objects=4)
+    s = LabelSolver(wl.scene)
+    M = s.accumulate(wl.pairs(), 4)
+    for g in (-0.4, 0.0, 0.5):
+        assert np.array_equal(s.assign(g, "scene").membership, oracle.assign_scene(M.values, g))
+    wl2 = synth.make_workload(seed=8, n_gaussians=5000, n_views=2, width=96, height=64,
+                              num_objects=2)
+    M2, asn = fs.solve(wl2.scene, wl2.pairs(), 2, gamma=0.2)
+    assert np.array_equal(asn.labels, oracle.assign_binary(M2.values, 0.2))

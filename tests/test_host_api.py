@@ -1,0 +1,115 @@
+"""Host-side logic of the package: types, validation order and messages,
+serialisation formats, tile_range, view sharding.  No GPU needed."""
+
+import numpy as np
+import pytest
+
+from paper_2409_08270_b200 import (
+    Assignment,
+    BlendConfig,
+    CameraView,
+    ContributionMatrix,
+    DEFAULT_BLEND,
+    EXACT_BLEND,
+    GaussianScene,
+    LabelMask,
+    SceneDataError,
+    tile_range,
+)
+from paper_2409_08270_b200.contributions import validate_views
+from paper_2409_08270_b200.distributed import shard_views
+from paper_2409_08270_b200.solver import _check_gamma
+
+
+def frontal(w=16, h=16, f=24.0):
+    return CameraView(0, w, h, f, f, w / 2 + 0.5, h / 2 + 0.5, np.eye(4))
+
+
+def test_blend_constants():
+    assert DEFAULT_BLEND.alpha_floor == 1.0 / 255.0
+    assert DEFAULT_BLEND.transmittance_floor == 1e-4
+    assert EXACT_BLEND == BlendConfig(0.0, 0.0)
+
+
+def test_scene_validation_messages():
+    with pytest.raises(SceneDataError, match="quaternion 1"):
+        GaussianScene([[0, 0, 1]] * 2, [[1, 0, 0, 0], [0, 0, 0, 0]], [[1] * 3] * 2, [0.5] * 2)
+    with pytest.raises(SceneDataError, match="gaussian 0 has non-positive scale"):
+        GaussianScene([[0, 0, 1]], [[1, 0, 0, 0]], [[0, 1, 1]], [0.5])
+    with pytest.raises(SceneDataError, match="gaussian 0 has opacity outside"):
+        GaussianScene([[0, 0, 1]], [[1, 0, 0, 0]], [[1, 1, 1]], [1.5])
+    s = GaussianScene([[0, 0, 1]], [[2, 0, 0, 0]], [[1, 1, 1]], [0.5])
+    assert np.allclose(s.rotations, [[1, 0, 0, 0]])
+
+
+def test_camera_validation():
+    with pytest.raises(ValueError, match="orthonormal"):
+        CameraView(3, 4, 4, 1.0, 1.0, 2, 2, np.diag([2.0, 1, 1, 1]))
+    with pytest.raises(ValueError, match="focal"):
+        CameraView(0, 4, 4, 0.0, 1.0, 2, 2, np.eye(4))
+
+
+def test_validate_views_order_and_messages():
+    v = frontal()
+    good = LabelMask(0, np.zeros((16, 16), np.uint16))
+    bad_shape = LabelMask(0, np.zeros((8, 16), np.uint16))
+    lab = np.zeros((16, 16), np.uint16)
+    lab[3, 7] = 5
+    with pytest.raises(ValueError, match=r"view 0: mask shape \(8, 16\) does not match"):
+        validate_views([(v, good), (v, bad_shape)], 2)
+    with pytest.raises(ValueError, match=r"view 0: label 5 at pixel \(3, 7\) exceeds object count 2"):
+        validate_views([(v, LabelMask(0, lab))], 2)
+    validate_views([(v, good)], 1)
+
+
+def test_contribution_matrix_file_roundtrip(tmp_path, rng):
+    m = ContributionMatrix(rng.random((3, 7)).astype(np.float32))
+    p = tmp_path / "A.bin"
+    m.save(p)
+    assert p.read_bytes()[:4] == b"FSA1"
+    assert np.array_equal(ContributionMatrix.load(p).values, m.values)
+    p.write_bytes(p.read_bytes()[:-4])
+    with pytest.raises(ValueError, match="truncated"):
+        ContributionMatrix.load(p)
+    p.write_bytes(b"NOPE" + bytes(16))
+    with pytest.raises(ValueError, match="magic"):
+        ContributionMatrix.load(p)
+    z = ContributionMatrix(np.array([[0, 1.0], [0, 0]], np.float32))
+    assert z.observed.tolist() == [False, True]
+
+
+def test_assignment_roundtrip(tmp_path, rng):
+    a = Assignment("binary", 0.25, labels=rng.integers(0, 2, 17))
+    a.save(tmp_path / "a.bin")
+    b = Assignment.load(tmp_path / "a.bin")
+    assert b.mode == "binary" and b.gamma == 0.25 and np.array_equal(a.labels, b.labels)
+    mem = rng.integers(0, 2, (4, 9)).astype(np.uint8)
+    s = Assignment("scene", -0.4, membership=mem)
+    s.save(tmp_path / "s.bin")
+    t = Assignment.load(tmp_path / "s.bin")
+    assert np.array_equal(t.membership, mem) and t.member_counts() == mem.sum(1).tolist()
+    with pytest.raises(ValueError):
+        Assignment("weird", 0.0)
+
+
+def test_gamma_check():
+    assert _check_gamma(-1) == -1.0
+    with pytest.raises(ValueError, match=r"gamma must lie in \[-1, 1\], got 1.5"):
+        _check_gamma(1.5)
+
+
+def test_tile_range_matches_golden():
+    from conftest import load_golden
+    c = load_golden("binning")["tile_range"]
+    for args, expect in zip(c["args"], c["out"]):
+        mx, my, r, tx, ty = args
+        assert tile_range(mx, my, int(r), int(tx), int(ty)) == tuple(expect)
+
+
+def test_shard_views_partition():
+    for n in (0, 1, 7, 200):
+        for world in (1, 2, 3, 8):
+            shards = [shard_views(n, r, world) for r in range(world)]
+            flat = [i for s in shards for i in s]
+            assert flat == list(range(n))
+            assert max(map(len, shards)) - min(map(len, shards)) <= 1
