@@ -58,8 +58,12 @@ typedef struct {
     int64_t exact_evals;      /* float64 alpha evaluations */
     int64_t atomics;          /* float64 accumulator atomics */
     int64_t retried_views;    /* views re-run after growing the instance buffers */
+    int64_t launches;         /* kernels this call launched */
     double gpu_ms;            /* CUDA-event time of the view loop on the device */
-    double raster_ms;         /* CUDA-event time of raster kernels (stream 0 only, sampled) */
+    /* per-stage CUDA-event times summed over views; only with fs_set_timing(ctx, 1) */
+    double prep_ms;           /* projection + depth radix sort */
+    double bin_ms;            /* instance emission + tile radix sort + tile ranges */
+    double raster_ms;         /* raster-accumulate kernel */
 } fs_accumulate_stats;
 
 const char *fs_last_error(void);
@@ -78,6 +82,10 @@ int fs_memset_zero(fs_context *ctx, void *dev_ptr, uint64_t bytes);
 int fs_copy_to_device(fs_context *ctx, void *dst, const void *src, uint64_t bytes);
 int fs_copy_to_host(fs_context *ctx, void *dst, const void *src, uint64_t bytes);
 int fs_synchronize(fs_context *ctx);
+
+/* Per-stage CUDA-event timing inside fs_accumulate (events on each view's
+ * stream around its stages; adds ~3 event records per view). */
+int fs_set_timing(fs_context *ctx, int enable);
 
 /* Upload a GaussianScene (scene.py:71-110, arrays already validated and the
  * quaternions normalised).  Replaces the per-view f64 input handling of

@@ -24,7 +24,7 @@ MODE_BINARY, MODE_SCENE = 0, 1
 EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
-    "fs_copy_to_host", "fs_synchronize", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_copy_to_host", "fs_synchronize", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
     "fs_accumulate", "fs_finalize", "fs_assign",
 )
 
@@ -50,8 +50,8 @@ class FsProjectionStats(ctypes.Structure):
 class FsAccumulateStats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in
                 ("views", "view_pixels", "emitted", "instances", "tile_steps", "exact_evals",
-                 "atomics", "retried_views")] + [("gpu_ms", ctypes.c_double),
-                                                 ("raster_ms", ctypes.c_double)]
+                 "atomics", "retried_views", "launches")] + [
+                    (k, ctypes.c_double) for k in ("gpu_ms", "prep_ms", "bin_ms", "raster_ms")]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -86,6 +86,7 @@ def load() -> ctypes.CDLL:
             "fs_copy_to_device": ([P, P, P, ctypes.c_uint64], I),
             "fs_copy_to_host": ([P, P, P, ctypes.c_uint64], I),
             "fs_synchronize": ([P], I),
+            "fs_set_timing": ([P, I], I),
             "fs_set_scene": ([P, I64, P, P, P, P], I),
             "fs_project": ([P, P, P, P, P, P, P, P], I),
             "fs_bin": ([P, P, P, P, I64, ctypes.POINTER(I64)], I),
@@ -182,6 +183,9 @@ class Context:
         self._scene_key = None
         self.n = 0
         self.lock = threading.RLock()
+
+    def set_timing(self, enable: bool) -> None:
+        _check(load().fs_set_timing(self.handle, 1 if enable else 0))
 
     def close(self) -> None:
         if self.handle:

@@ -98,6 +98,8 @@ struct fs_context {
     int view_log_cap = 0;
     std::vector<fs::Work> work;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+    bool timing = false;
+    std::vector<cudaEvent_t> stage_events;  // 4 per view when timing
 };
 
 using fs::fail;
@@ -114,6 +116,7 @@ template <typename T>
 int dev_alloc(T** p, size_t count) {
     if (*p) {
         cudaFree(*p);
+        cudaGetLastError();
         *p = nullptr;
     }
     if (count == 0) count = 1;
@@ -207,7 +210,7 @@ int check_cam(const fs_camera& c, int idx) {
 
 // Projection + depth sort + binning of one view on workspace w.
 void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
-                 int cull_floor, fs::ProjectExport ex) {
+                 int cull_floor, fs::ProjectExport ex, cudaEvent_t after_sort = nullptr) {
     const int n = (int)ctx->n;
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
                        cull_floor, w.dkeys[0], w.dvals[0], w.rect, w.r32, w.r64, w.vc, ex,
@@ -215,6 +218,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
     fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
                                               nullptr, (unsigned)n, &w.vc->key_or, 8, w.hist,
                                               ctx->num_sms, w.stream);
+    if (after_sort) cudaEventRecord(after_sort, w.stream);
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
     fs::BinBuffers b;
@@ -236,10 +240,15 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
     fs::launch_bin(n, ntiles, tx, (bits + 7) / 8, b, w.vc, ctx->num_sms, w.stream);
 }
 
+// Kernels one enqueue_view launches (for the stats' launch count).
+int view_launches(int tile_passes) { return 2 + 8 * 3 + 3 + 3 * tile_passes + 1 + 1 + 1; }
+
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
-                  fs::ViewCounters* log) {
-    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{});
+                  fs::ViewCounters* log, cudaEvent_t* ev = nullptr) {
+    if (ev) cudaEventRecord(ev[0], w.stream);
+    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr);
+    if (ev) cudaEventRecord(ev[2], w.stream);
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
     fs::RasterArgs ra;
@@ -262,6 +271,7 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.acc = acc;
     ra.vc = w.vc;
     fs::launch_raster(ra, w.stream);
+    if (ev) cudaEventRecord(ev[3], w.stream);
     if (log) fs::view_end_kernel<<<1, 32, 0, w.stream>>>(w.vc, log);
 }
 
@@ -341,6 +351,7 @@ void fs_destroy(fs_context* ctx) {
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
                     (void*)ctx->opac, (void*)ctx->tile_oa_table, (void*)ctx->view_log})
         if (p) cudaFree(p);
+    for (cudaEvent_t e : ctx->stage_events) cudaEventDestroy(e);
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
     if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
     delete ctx;
@@ -385,6 +396,12 @@ int fs_copy_to_host(fs_context* ctx, void* dst, const void* src, uint64_t bytes)
 int fs_synchronize(fs_context* ctx) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
+    return FS_OK;
+}
+
+int fs_set_timing(fs_context* ctx, int enable) {
+    if (!ctx) return fail(FS_EINVAL, "fs_set_timing: NULL context");
+    ctx->timing = enable != 0;
     return FS_OK;
 }
 
@@ -618,6 +635,14 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
     }
     const int S = (int)ctx->work.size();
     fs::Work& w0 = ctx->work[0];
+    if (ctx->timing) {
+        while ((int)ctx->stage_events.size() < 4 * n_views) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ctx->stage_events.push_back(e);
+        }
+    }
+    long long launches = 0;
     CK(cudaEventRecord(ctx->ev_start, w0.stream));
     for (int s = 1; s < S; ++s) CK(cudaStreamWaitEvent(ctx->work[s].stream, ctx->ev_start, 0));
     for (int v = 0; v < n_views; ++v) {
@@ -633,7 +658,9 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
             mask = w.mask_dev;
         }
         enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
-                     ctx->view_log + v);
+                     ctx->view_log + v, ctx->timing ? &ctx->stage_events[4 * v] : nullptr);
+        const int ntl = fs::tiles_x_of(cams[v].width) * fs::tiles_y_of(cams[v].height);
+        launches += view_launches((fs::bits_for((unsigned)(ntl - 1)) + 7) / 8);
     }
     CK(cudaGetLastError());
     for (int s = 1; s < S; ++s) {
@@ -646,6 +673,19 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_stop));
 
+    double prep_ms = 0, bin_ms = 0, raster_ms = 0;
+    if (ctx->timing) {
+        for (int v = 0; v < n_views; ++v) {
+            float a = 0, b = 0, c = 0;
+            cudaEvent_t* e = &ctx->stage_events[4 * v];
+            CK(cudaEventElapsedTime(&a, e[0], e[1]));
+            CK(cudaEventElapsedTime(&b, e[1], e[2]));
+            CK(cudaEventElapsedTime(&c, e[2], e[3]));
+            prep_ms += a;
+            bin_ms += b;
+            raster_ms += c;
+        }
+    }
     std::vector<fs::ViewCounters> log(n_views);
     CK(cudaMemcpy(log.data(), ctx->view_log, sizeof(fs::ViewCounters) * n_views, cudaMemcpyDeviceToHost));
     // re-run views that overflowed the instance buffers (they contributed nothing)
@@ -684,7 +724,11 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
             stats->atomics += (int64_t)l.atomics;
         }
         stats->retried_views = retried;
+        stats->launches = launches;
         stats->gpu_ms = ms;
+        stats->prep_ms = prep_ms;
+        stats->bin_ms = bin_ms;
+        stats->raster_ms = raster_ms;
     }
     return FS_OK;
 }
@@ -694,7 +738,7 @@ int fs_finalize(fs_context* ctx, const double* acc, int64_t count, float* out, i
     if (count == 0) return FS_OK;
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->work[0].stream;
-    float* dst = out;
+    float* dst = out_on_device ? out : nullptr;
     if (!out_on_device) {
         int rc = dev_alloc(&dst, (size_t)count);
         if (rc) return rc;

@@ -33,7 +33,7 @@ def test_projection_matches_reference(case):
     assert np.array_equal(radius[a], c["radius"][a])
     np.testing.assert_allclose(mean2d[a], c["mean2d"][a], rtol=1e-13, atol=1e-12)
     np.testing.assert_allclose(conic[a], c["conic"][a], rtol=1e-11, atol=1e-14)
-    assert np.array_equal(depth, c["depth"]) or np.allclose(depth, c["depth"], rtol=1e-15)
+    np.testing.assert_allclose(depth, c["depth"], rtol=1e-12, atol=1e-14)
 
 
 @pytest.mark.parametrize("case", sorted(k for k in BIN if k != "tile_range"))
