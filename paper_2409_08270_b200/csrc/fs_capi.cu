@@ -68,10 +68,15 @@ struct Work {
     unsigned long long* rect = nullptr;
     Rec32* r32 = nullptr;
     Rec64* r64 = nullptr;
-    unsigned int* block_sums = nullptr;
-    unsigned int* hist = nullptr;
-    unsigned int* ikeys[2] = {nullptr, nullptr};
-    unsigned int* ivals[2] = {nullptr, nullptr};
+    SortState* sdepth = nullptr;             // depth sort state
+    SortState* sidx = nullptr;               // splat-list index sort state (fs_bin_splats)
+    unsigned long long* status_depth = nullptr;
+    unsigned long long* status_idx = nullptr;
+    size_t status_depth_words = 0, status_idx_words = 0;
+    unsigned int* inst = nullptr;            // per-tile buckets: depth ranks, then gids
+    unsigned int* scratch = nullptr;         // merge scratch for long buckets
+    unsigned int* tile_count = nullptr;      // ntiles
+    unsigned int* tile_cursor = nullptr;     // ntiles
     unsigned int* tile_start = nullptr;
     ViewCounters* vc = nullptr;
     unsigned long long* idx_oa = nullptr;  // OR/AND of the secondary (index) keys
@@ -134,7 +139,7 @@ void free_work(fs::Work& w) {
         if (p) cudaFree(p);
     };
     f(w.dkeys[0]); f(w.dkeys[1]); f(w.dvals[0]); f(w.dvals[1]); f(w.rect); f(w.r32); f(w.r64);
-    f(w.block_sums); f(w.hist); f(w.ikeys[0]); f(w.ikeys[1]); f(w.ivals[0]); f(w.ivals[1]);
+    f(w.sdepth); f(w.sidx); f(w.status_depth); f(w.status_idx); f(w.inst); f(w.scratch); f(w.tile_count); f(w.tile_cursor);
     f(w.tile_start); f(w.vc); f(w.idx_oa); f(w.mask_dev);
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
@@ -157,21 +162,37 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
         if ((rc = dev_alloc(&w.r64, n))) return rc;
         w.n_cap = n;
     }
-    if (!w.block_sums) {
-        if ((rc = dev_alloc(&w.block_sums, (size_t)fs::sort_grid(ctx->num_sms)))) return rc;
-        if ((rc = dev_alloc(&w.hist, fs::sort_hist_entries(ctx->num_sms)))) return rc;
+    if (!w.vc) {
         if ((rc = dev_alloc(&w.vc, 1))) return rc;
         if ((rc = dev_alloc(&w.idx_oa, 2))) return rc;
+        if ((rc = dev_alloc(&w.sdepth, 1))) return rc;
+        if ((rc = dev_alloc(&w.sidx, 1))) return rc;
+        CK(cudaMemset(w.sdepth, 0, sizeof(fs::SortState)));
+        CK(cudaMemset(w.sidx, 0, sizeof(fs::SortState)));
+    }
+    {
+        // look-back status words must start zeroed (epoch 0 = never ready)
+        const size_t need = fs::sort_status_words((unsigned)std::min<long long>(std::max(n, w.n_cap), 0xffffffffLL));
+        if (need > w.status_depth_words) {
+            if ((rc = dev_alloc(&w.status_depth, need))) return rc;
+            CK(cudaMemset(w.status_depth, 0, need * 8));
+            w.status_depth_words = need;
+        }
+        if (need > w.status_idx_words) {
+            if ((rc = dev_alloc(&w.status_idx, need))) return rc;
+            CK(cudaMemset(w.status_idx, 0, need * 8));
+            w.status_idx_words = need;
+        }
     }
     if (inst > w.inst_cap) {
-        for (int k = 0; k < 2; ++k) {
-            if ((rc = dev_alloc(&w.ikeys[k], inst))) return rc;
-            if ((rc = dev_alloc(&w.ivals[k], inst))) return rc;
-        }
+        if ((rc = dev_alloc(&w.inst, inst))) return rc;
+        if ((rc = dev_alloc(&w.scratch, inst))) return rc;
         w.inst_cap = inst;
     }
     if (ntiles > w.ntiles_cap) {
         if ((rc = dev_alloc(&w.tile_start, (size_t)ntiles + 1))) return rc;
+        if ((rc = dev_alloc(&w.tile_count, (size_t)ntiles))) return rc;
+        if ((rc = dev_alloc(&w.tile_cursor, (size_t)ntiles))) return rc;
         w.ntiles_cap = ntiles;
     }
     if (mask_px > w.mask_cap) {
@@ -208,40 +229,56 @@ int check_cam(const fs_camera& c, int idx) {
     return FS_OK;
 }
 
-// Projection + depth sort + binning of one view on workspace w.
+fs::BinBuffers bin_buffers(fs::Work& w) {
+    fs::BinBuffers b;
+    b.sorted_gid[0] = w.dvals[0];
+    b.sorted_gid[1] = w.dvals[1];
+    b.depth_state = w.sdepth;
+    b.rect = w.rect;
+    b.tile_count = w.tile_count;
+    b.tile_start = w.tile_start;
+    b.tile_cursor = w.tile_cursor;
+    b.inst = w.inst;
+    b.capacity = w.inst_cap;
+    return b;
+}
+
+fs::TileSortArgs tile_sort_args(fs::Work& w, long long n) {
+    fs::TileSortArgs t;
+    t.tile_start = w.tile_start;
+    t.inst = w.inst;
+    t.scratch = w.scratch;
+    t.sorted_gid[0] = w.dvals[0];
+    t.sorted_gid[1] = w.dvals[1];
+    t.depth_state = w.sdepth;
+    t.rank_bits = fs::bits_for((unsigned)(n > 0 ? n - 1 : 0));
+    t.cap = fs::kTileSortCap;
+    t.vc = w.vc;
+    return t;
+}
+
+// Projection + depth sort + per-tile buckets of one view on workspace w
+// (the buckets are sorted by the raster prologue or launch_tile_sort).
 void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
                  int cull_floor, fs::ProjectExport ex, cudaEvent_t after_sort = nullptr) {
     const int n = (int)ctx->n;
+    const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
+    cudaMemsetAsync(w.tile_count, 0, sizeof(unsigned int) * (size_t)ntiles, w.stream);
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
-                       cull_floor, w.dkeys[0], w.dvals[0], w.rect, w.r32, w.r64, w.vc, ex,
-                       ctx->num_sms, w.stream);
+                       cull_floor, w.dkeys[0], w.dvals[0], w.rect, w.tile_count, w.r32, w.r64,
+                       w.vc, ex, ctx->num_sms, w.stream);
+    // invisible Gaussians carry the all-ones key; the sort substitutes the AND
+    // of the visible keys so they never add permuting digits
     fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
-                                              nullptr, (unsigned)n, &w.vc->key_or, 8, w.hist,
+                                              nullptr, (unsigned)n, &w.vc->key_or,
+                                              &w.vc->key_and, 8, w.sdepth, w.status_depth,
                                               ctx->num_sms, w.stream);
     if (after_sort) cudaEventRecord(after_sort, w.stream);
-    const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
-    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
-    fs::BinBuffers b;
-    b.dkeys[0] = w.dkeys[0];
-    b.dkeys[1] = w.dkeys[1];
-    b.dvals[0] = w.dvals[0];
-    b.dvals[1] = w.dvals[1];
-    b.depth_or_and = &w.vc->key_or;
-    b.rect = w.rect;
-    b.block_sums = w.block_sums;
-    b.ikeys[0] = w.ikeys[0];
-    b.ikeys[1] = w.ikeys[1];
-    b.ivals[0] = w.ivals[0];
-    b.ivals[1] = w.ivals[1];
-    b.tile_or_and = ctx->tile_oa_table + 2 * bits;
-    b.hist = w.hist;
-    b.tile_start = w.tile_start;
-    b.capacity = w.inst_cap;
-    fs::launch_bin(n, ntiles, tx, (bits + 7) / 8, b, w.vc, ctx->num_sms, w.stream);
+    fs::launch_bin(n, ntiles, tx, bin_buffers(w), w.vc, ctx->num_sms, w.stream);
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches(int tile_passes) { return 2 + 8 * 3 + 3 + 3 * tile_passes + 1 + 1 + 1; }
+int view_launches() { return 1 + 1 + (3 + 8) + 2 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
@@ -250,7 +287,6 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr);
     if (ev) cudaEventRecord(ev[2], w.stream);
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
-    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
     fs::RasterArgs ra;
     ra.width = cam.width;
     ra.height = cam.height;
@@ -261,11 +297,7 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.alpha_floor = alpha_floor;
     ra.t_floor = t_floor;
     ra.mask = mask;
-    ra.tile_start = w.tile_start;
-    ra.inst_gid[0] = w.ivals[0];
-    ra.inst_gid[1] = w.ivals[1];
-    ra.tile_passes = (bits + 7) / 8;
-    ra.tile_or_and = ctx->tile_oa_table + 2 * bits;
+    ra.sort = tile_sort_args(w, ctx->n);
     ra.r32 = w.r32;
     ra.r64 = w.r64;
     ra.acc = acc;
@@ -320,6 +352,11 @@ int fs_create(int device, int n_streams, fs_context** out) {
                               "B200 (sm_100a) only", device, prop.name, prop.major, prop.minor);
     }
     ctx->num_sms = prop.multiProcessorCount;
+    e = fs::raster_configure();
+    if (e != cudaSuccess) {
+        delete ctx;
+        return fs::set_cuda_error(e, "raster_configure", __FILE__, __LINE__);
+    }
     ctx->work.resize(n_streams);
     for (auto& w : ctx->work) {
         CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
@@ -453,8 +490,8 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
         (rc = dev_alloc(&ex.radius, n1)))
         return rc;
     fs::launch_project((int)n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, to_cam(*cam), 0.0,
-                       0, w.dkeys[0], w.dvals[0], w.rect, w.r32, w.r64, w.vc, ex, ctx->num_sms,
-                       w.stream);
+                       0, w.dkeys[0], w.dvals[0], w.rect, nullptr, w.r32, w.r64, w.vc, ex,
+                       ctx->num_sms, w.stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(w.stream));
     CK(cudaMemcpy(alive, ex.alive, (size_t)n, cudaMemcpyDeviceToHost));
@@ -479,6 +516,22 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
     return FS_OK;
 }
 
+// Copies the (sorted) tile lists of workspace w to the host as CSR.
+static int copy_tile_lists(fs::Work& w, int ntiles, unsigned int n_valid, int64_t* tile_offsets,
+                           int64_t* items, int64_t items_capacity, int64_t* n_items) {
+    std::vector<unsigned int> starts(ntiles + 1);
+    CK(cudaMemcpy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost));
+    for (int t = 0; t <= ntiles; ++t) tile_offsets[t] = starts[t];
+    *n_items = n_valid;
+    if (items) {
+        if (items_capacity < (int64_t)n_valid) return fail(FS_EINVAL, "fs_bin: items buffer too small");
+        std::vector<unsigned int> g(n_valid);
+        if (n_valid) CK(cudaMemcpy(g.data(), w.inst, sizeof(unsigned int) * n_valid, cudaMemcpyDeviceToHost));
+        for (unsigned int i = 0; i < n_valid; ++i) items[i] = g[i];
+    }
+    return FS_OK;
+}
+
 int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t* items,
            int64_t items_capacity, int64_t* n_items) {
     if (!ctx || !cam || !tile_offsets || !n_items) return fail(FS_EINVAL, "fs_bin: NULL argument");
@@ -493,6 +546,7 @@ int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t
     for (int attempt = 0; attempt < 2; ++attempt) {
         if ((rc = ensure_work(ctx, w, ctx->n, ntiles, cap, 1))) return rc;
         enqueue_bin(ctx, w, k, 0.0, 0, fs::ProjectExport{});
+        fs::launch_tile_sort(ntiles, tile_sort_args(w, ctx->n), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
         CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
@@ -500,22 +554,7 @@ int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t
         cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull, (unsigned long long)vc.n_instances + 1024);
     }
     if (vc.overflow) return fail(FS_ENOMEM, "fs_bin: instance buffer overflow");
-    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
-    const int passes = (bits + 7) / 8;
-    // result parity: executed passes = passes (tile mask covers every digit)
-    const unsigned int* gids = w.ivals[passes & 1];
-    std::vector<unsigned int> starts(ntiles + 1);
-    CK(cudaMemcpy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost));
-    for (int t = 0; t <= ntiles; ++t) tile_offsets[t] = starts[t];
-    *n_items = vc.n_valid;
-    if (items) {
-        if (items_capacity < (int64_t)vc.n_valid) return fail(FS_EINVAL, "fs_bin: items buffer too small");
-        std::vector<unsigned int> g(vc.n_valid);
-        if (vc.n_valid)
-            CK(cudaMemcpy(g.data(), gids, sizeof(unsigned int) * vc.n_valid, cudaMemcpyDeviceToHost));
-        for (unsigned int i = 0; i < vc.n_valid; ++i) items[i] = g[i];
-    }
-    return FS_OK;
+    return copy_tile_lists(w, ntiles, vc.n_valid, tile_offsets, items, items_capacity, n_items);
 }
 
 int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double* depth,
@@ -532,8 +571,6 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
     CK(cudaSetDevice(ctx->device));
     fs::Work& w = ctx->work[0];
     const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
-    const int bits = fs::bits_for((unsigned)(ntiles > 0 ? ntiles - 1 : 0));
-    const int passes = (bits + 7) / 8;
     unsigned int cap = std::max(w.inst_cap, initial_inst_cap(k));
     double *d_mean = nullptr, *d_depth = nullptr;
     long long *d_rad = nullptr, *d_idx = nullptr;
@@ -552,30 +589,17 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
         if ((rc = ensure_work(ctx, w, std::max<long long>(k, 1), ntiles, cap, 1))) return rc;
         const unsigned long long init[2] = {0ull, ~0ull};
         CK(cudaMemcpyAsync(w.idx_oa, init, sizeof(init), cudaMemcpyHostToDevice, w.stream));
+        CK(cudaMemsetAsync(w.tile_count, 0, sizeof(unsigned int) * (size_t)ntiles, w.stream));
         fs::launch_view_begin(w.vc, w.stream);
+        // LSD: stable sort by gaussian index, then stable sort by depth
         fs::launch_bin_splats_keys((int)k, d_idx, d_mean, d_rad, d_depth, width, height, w.dkeys[0],
-                                   w.dvals[0], w.dkeys[1], w.dvals[1], w.rect, w.idx_oa, w.hist, w.vc,
-                                   ctx->num_sms, w.stream);
+                                   w.dvals[0], w.dkeys[1], w.dvals[1], w.rect, w.tile_count,
+                                   w.idx_oa, w.sidx, w.status_idx, w.vc, ctx->num_sms, w.stream);
         fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
-                                                  nullptr, (unsigned)k, &w.vc->key_or, 8, w.hist,
-                                                  ctx->num_sms, w.stream);
-        fs::BinBuffers b;
-        b.dkeys[0] = w.dkeys[0];
-        b.dkeys[1] = w.dkeys[1];
-        b.dvals[0] = w.dvals[0];
-        b.dvals[1] = w.dvals[1];
-        b.depth_or_and = &w.vc->key_or;
-        b.rect = w.rect;
-        b.block_sums = w.block_sums;
-        b.ikeys[0] = w.ikeys[0];
-        b.ikeys[1] = w.ikeys[1];
-        b.ivals[0] = w.ivals[0];
-        b.ivals[1] = w.ivals[1];
-        b.tile_or_and = ctx->tile_oa_table + 2 * bits;
-        b.hist = w.hist;
-        b.tile_start = w.tile_start;
-        b.capacity = w.inst_cap;
-        fs::launch_bin((int)k, ntiles, tx, passes, b, w.vc, ctx->num_sms, w.stream);
+                                                  nullptr, (unsigned)k, &w.vc->key_or, nullptr, 8,
+                                                  w.sdepth, w.status_depth, ctx->num_sms, w.stream);
+        fs::launch_bin((int)k, ntiles, tx, bin_buffers(w), w.vc, ctx->num_sms, w.stream);
+        fs::launch_tile_sort(ntiles, tile_sort_args(w, k), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
         CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
@@ -587,19 +611,7 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
     cudaFree(d_rad);
     cudaFree(d_idx);
     if (vc.overflow) return fail(FS_ENOMEM, "fs_bin_splats: instance buffer overflow");
-    std::vector<unsigned int> starts(ntiles + 1);
-    CK(cudaMemcpy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost));
-    for (int t = 0; t <= ntiles; ++t) tile_offsets[t] = starts[t];
-    *n_items = vc.n_valid;
-    if (items) {
-        if (items_capacity < (int64_t)vc.n_valid) return fail(FS_EINVAL, "fs_bin_splats: items buffer too small");
-        std::vector<unsigned int> g(vc.n_valid);
-        if (vc.n_valid)
-            CK(cudaMemcpy(g.data(), w.ivals[passes & 1], sizeof(unsigned int) * vc.n_valid,
-                          cudaMemcpyDeviceToHost));
-        for (unsigned int i = 0; i < vc.n_valid; ++i) items[i] = g[i];
-    }
-    return FS_OK;
+    return copy_tile_lists(w, ntiles, vc.n_valid, tile_offsets, items, items_capacity, n_items);
 }
 
 int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uint16_t* const* masks,
@@ -625,6 +637,8 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         view_px += (long long)cams[v].width * cams[v].height;
     }
     CK(cudaSetDevice(ctx->device));
+    // order after everything the caller enqueued on other streams (e.g. zeroing acc)
+    CK(cudaDeviceSynchronize());
     for (auto& w : ctx->work) {
         unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
         if ((rc = ensure_work(ctx, w, ctx->n, max_tiles, cap, masks_on_device ? 1 : max_px))) return rc;
@@ -659,8 +673,7 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         }
         enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
                      ctx->view_log + v, ctx->timing ? &ctx->stage_events[4 * v] : nullptr);
-        const int ntl = fs::tiles_x_of(cams[v].width) * fs::tiles_y_of(cams[v].height);
-        launches += view_launches((fs::bits_for((unsigned)(ntl - 1)) + 7) / 8);
+        launches += view_launches();
     }
     CK(cudaGetLastError());
     for (int s = 1; s < S; ++s) {
@@ -737,6 +750,7 @@ int fs_finalize(fs_context* ctx, const double* acc, int64_t count, float* out, i
     if (!ctx || (!acc && count) || (!out && count)) return fail(FS_EINVAL, "fs_finalize: NULL argument");
     if (count == 0) return FS_OK;
     CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());  // acc may come from another stream (e.g. an NCCL all-reduce)
     cudaStream_t st = ctx->work[0].stream;
     float* dst = out_on_device ? out : nullptr;
     if (!out_on_device) {

@@ -6,16 +6,42 @@
 
 namespace fs {
 
-// ---- radix pass bookkeeping (shared by the sort and its consumers) ----
-__device__ __forceinline__ bool pass_active(unsigned long long varying, int shift) {
-    return ((varying >> shift) & 0xFFull) != 0ull;
+// ---- radix sort state (one per sort call site, device memory) ----
+struct SortState {
+    unsigned int offsets[8][256];  // per digit position: histogram, then exclusive offsets
+    unsigned int tile_counter[8];  // tile ids claimed by each pass
+    unsigned int active;           // bit p: pass p permutes (not the identity)
+    unsigned int epoch;            // look-back status generation
+};
+
+// Which ping-pong buffer holds the sorted result (0 or 1).
+__device__ __forceinline__ int sort_result_parity(const SortState* st) {
+    return __popc(st->active) & 1;
 }
 
-// Number of executed passes strictly before `pass` (parity selects the buffer).
-__device__ __forceinline__ int pass_parity(unsigned long long varying, int pass) {
-    int p = 0;
-    for (int q = 0; q < pass; ++q) p += pass_active(varying, 8 * q) ? 1 : 0;
-    return p & 1;
+// Inclusive tile rectangle of a splat's radius box (rasterizer.py:106-113),
+// packed tx0 | tx1 << 16 | ty0 << 32 | ty1 << 48; ~0 when empty.
+__device__ __forceinline__ unsigned long long tile_rect(double mx, double my, double r, int tx_n,
+                                                        int ty_n) {
+    const double fx0 = floor((mx - r) / kTile), fx1 = floor((mx + r) / kTile);
+    const double fy0 = floor((my - r) / kTile), fy1 = floor((my + r) / kTile);
+    const int tx0 = fx0 < 0.0 ? 0 : (fx0 > tx_n ? tx_n : (int)fx0);
+    const int tx1 = fx1 > tx_n - 1 ? tx_n - 1 : (fx1 < -1.0 ? -1 : (int)fx1);
+    const int ty0 = fy0 < 0.0 ? 0 : (fy0 > ty_n ? ty_n : (int)fy0);
+    const int ty1 = fy1 > ty_n - 1 ? ty_n - 1 : (fy1 < -1.0 ? -1 : (int)fy1);
+    if (tx0 > tx1 || ty0 > ty1) return ~0ull;
+    return (unsigned long long)tx0 | ((unsigned long long)tx1 << 16) |
+           ((unsigned long long)ty0 << 32) | ((unsigned long long)ty1 << 48);
+}
+
+// One instance per covered tile.
+__device__ __forceinline__ void count_rect_tiles(unsigned long long rc, int tiles_x,
+                                                 unsigned int* count) {
+    if (rc == ~0ull || !count) return;
+    const unsigned int tx0 = rc & 0xFFFF, tx1 = (rc >> 16) & 0xFFFF;
+    const unsigned int ty0 = (rc >> 32) & 0xFFFF, ty1 = (rc >> 48) & 0xFFFF;
+    for (unsigned int ty = ty0; ty <= ty1; ++ty)
+        for (unsigned int tx = tx0; tx <= tx1; ++tx) atomicAdd(&count[ty * (unsigned)tiles_x + tx], 1u);
 }
 
 // ---- fs_project.cu ----
@@ -24,64 +50,73 @@ void launch_scene_setup(int n, const double* means, const double* quats, const d
 void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
                     int cull_floor, unsigned long long* keys, unsigned int* vals,
-                    unsigned long long* rect, Rec32* r32, Rec64* r64, ViewCounters* vc,
-                    ProjectExport ex, int num_sms, cudaStream_t st);
+                    unsigned long long* rect, unsigned int* tile_count, Rec32* r32, Rec64* r64,
+                    ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st);
+void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 
 // ---- fs_sort.cu ----
-int sort_grid(int num_sms);
-size_t sort_hist_entries(int num_sms);
+size_t sort_status_words(unsigned int n_cap);
+// d_or_and: {OR, AND} of the valid keys (digits constant over all keys are
+// skipped); sub: if non-null, keys equal to all-ones are replaced by *sub.
 template <typename K>
 int launch_radix_sort(K* keys0, unsigned int* vals0, K* keys1, unsigned int* vals1,
-                      const unsigned int* d_n, unsigned int n_fixed,
-                      const unsigned long long* d_or_and, int passes, unsigned int* hist,
-                      int num_sms, cudaStream_t st);
-void launch_scan_hist(unsigned int* data, int entries, cudaStream_t st);
+                      const unsigned int* d_n, unsigned int n_cap,
+                      const unsigned long long* d_or_and, const unsigned long long* sub, int passes,
+                      SortState* st, unsigned long long* status, int num_sms, cudaStream_t s);
 
 // ---- fs_bin.cu ----
-// After the depth sort: emit (tile, gid) instances in depth-rank order, sort
-// them by tile (stable) and build per-tile ranges.  Instances beyond
-// `capacity` set vc->overflow and the view is skipped by the raster kernel.
 struct BinBuffers {
-    unsigned long long* dkeys[2];  // depth sort ping-pong
-    unsigned int* dvals[2];
-    const unsigned long long* depth_or_and;  // &vc->key_or (key_or, key_and adjacent)
-    const unsigned long long* rect;
-    unsigned int* block_sums;  // sort_grid entries
-    unsigned int* ikeys[2];    // instance tile ids (ping-pong)
-    unsigned int* ivals[2];    // instance gids (ping-pong)
-    const unsigned long long* tile_or_and;  // {tile mask, 0}
-    unsigned int* hist;
-    unsigned int* tile_start;  // ntiles + 1
+    const unsigned int* sorted_gid[2];  // depth sort result (ping-pong)
+    const SortState* depth_state;       // which of the two holds it
+    const unsigned long long* rect;     // per gid
+    const unsigned int* tile_count;     // per tile (from the projection)
+    unsigned int* tile_start;           // ntiles + 1
+    unsigned int* tile_cursor;          // ntiles
+    unsigned int* inst;                 // capacity: ranks, gids after the per-tile sort
     unsigned int capacity;
 };
-void launch_bin(int n, int ntiles, int tiles_x, int tile_passes, const BinBuffers& b,
-                ViewCounters* vc, int num_sms, cudaStream_t st);
+void launch_bin(int n, int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc,
+                int num_sms, cudaStream_t st);
+
+struct TileSortArgs {
+    const unsigned int* tile_start;
+    unsigned int* inst;
+    unsigned int* scratch;
+    const unsigned int* sorted_gid[2];
+    const SortState* depth_state;
+    int rank_bits;
+    unsigned int cap;
+    const ViewCounters* vc;
+};
+size_t tile_sort_smem_bytes(unsigned int cap);
+cudaError_t tile_sort_configure(unsigned int cap);
+void launch_tile_sort(int ntiles, const TileSortArgs& t, cudaStream_t st);
 
 // Binning of an explicit splat list: secondary sort by gaussian index, then
 // depth keys (written to dk0/dv0 for the depth sort that follows).
 void launch_bin_splats_keys(int k, const long long* index, const double* mean2d,
                             const long long* radius, const double* depth, int width, int height,
                             unsigned long long* dk0, unsigned int* dv0, unsigned long long* dk1,
-                            unsigned int* dv1, unsigned long long* rect, unsigned long long* idx_oa,
-                            unsigned int* hist, ViewCounters* vc, int num_sms, cudaStream_t st);
-void launch_view_begin(ViewCounters* vc, cudaStream_t st);
+                            unsigned int* dv1, unsigned long long* rect, unsigned int* tile_count,
+                            unsigned long long* idx_oa, SortState* idx_state,
+                            unsigned long long* idx_status, ViewCounters* vc, int num_sms,
+                            cudaStream_t st);
 
 // ---- fs_raster.cu ----
+constexpr unsigned int kTileSortCap = 4096;  // bucket entries sorted in shared memory
 struct RasterArgs {
     int width, height, tiles_x, ntiles;
     int num_objects;
     long long n_gaussians;
     double alpha_floor, t_floor;
     const uint16_t* mask;          // H x W labels (device)
-    const unsigned int* tile_start;
-    const unsigned int* inst_gid[2];  // instance gid ping-pong buffers
-    int tile_passes;
-    const unsigned long long* tile_or_and;
+    TileSortArgs sort;             // bucket -> depth-ordered gid list (prologue)
     const Rec32* r32;
     const Rec64* r64;
     double* acc;                   // E x N float64 accumulator
     ViewCounters* vc;
 };
+cudaError_t raster_configure();
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 
 // ---- fs_assign.cu ----

@@ -79,8 +79,9 @@ __global__ void __launch_bounds__(256) project_kernel(
     const double* __restrict__ gmz, const double* __restrict__ sig,
     const double* __restrict__ opac, Camera cam, double alpha_floor, int cull_floor,
     unsigned long long* __restrict__ keys, unsigned int* __restrict__ vals,
-    unsigned long long* __restrict__ rect, Rec32* __restrict__ r32, Rec64* __restrict__ r64,
-    ViewCounters* __restrict__ vc, ProjectExport ex) {
+    unsigned long long* __restrict__ rect, unsigned int* __restrict__ tile_count,
+    Rec32* __restrict__ r32, Rec64* __restrict__ r64, ViewCounters* __restrict__ vc,
+    ProjectExport ex) {
     const double* W = cam.w2c;
     const int tx_n = tiles_x_of(cam.width), ty_n = tiles_y_of(cam.height);
     __shared__ unsigned long long s_or[8], s_and[8];
@@ -165,16 +166,9 @@ __global__ void __launch_bounds__(256) project_kernel(
                 k_or |= key;
                 k_and &= key;
                 // tile_range (rasterizer.py:106-113), inclusive floor box
-                double fx0 = floor((mxp - rad) / kTile), fx1 = floor((mxp + rad) / kTile);
-                double fy0 = floor((myp - rad) / kTile), fy1 = floor((myp + rad) / kTile);
-                int tx0 = fx0 < 0.0 ? 0 : (fx0 > tx_n ? tx_n : (int)fx0);
-                int tx1 = fx1 > tx_n - 1 ? tx_n - 1 : (fx1 < -1.0 ? -1 : (int)fx1);
-                int ty0 = fy0 < 0.0 ? 0 : (fy0 > ty_n ? ty_n : (int)fy0);
-                int ty1 = fy1 > ty_n - 1 ? ty_n - 1 : (fy1 < -1.0 ? -1 : (int)fy1);
-                bool transparent = cull_floor && alpha_floor > 0.0 && !(o >= alpha_floor);
-                if (tx0 <= tx1 && ty0 <= ty1 && !transparent)
-                    rc = (unsigned long long)tx0 | ((unsigned long long)tx1 << 16) |
-                         ((unsigned long long)ty0 << 32) | ((unsigned long long)ty1 << 48);
+                const bool transparent = cull_floor && alpha_floor > 0.0 && !(o >= alpha_floor);
+                if (!transparent) rc = tile_rect(mxp, myp, rad, tx_n, ty_n);
+                count_rect_tiles(rc, tx_n, tile_count);
             }
             keys[i] = key;
             vals[i] = (unsigned int)i;
@@ -278,15 +272,15 @@ void launch_scene_setup(int n, const double* means, const double* quats, const d
 void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
                     int cull_floor, unsigned long long* keys, unsigned int* vals,
-                    unsigned long long* rect, Rec32* r32, Rec64* r64, ViewCounters* vc,
-                    ProjectExport ex, int num_sms, cudaStream_t st) {
+                    unsigned long long* rect, unsigned int* tile_count, Rec32* r32, Rec64* r64,
+                    ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st) {
     view_begin_kernel<<<1, 32, 0, st>>>(vc);
     if (n <= 0) return;
     int grid = (n + 255) / 256;
     int cap = num_sms * 8;
     if (grid > cap) grid = cap;
     project_kernel<<<grid, 256, 0, st>>>(n, mx, my, mz, sig, opac, cam, alpha_floor, cull_floor,
-                                         keys, vals, rect, r32, r64, vc, ex);
+                                         keys, vals, rect, tile_count, r32, r64, vc, ex);
 }
 
 }  // namespace fs

@@ -2,61 +2,84 @@
 // into the E x N float64 contribution accumulator (reference
 // contributions.py:119-160, the `_accumulate_view` walk).
 //
-// One CTA per 16x16 tile, one thread per pixel (warp w owns tile rows 2w and
-// 2w+1).  The tile's depth-ordered list is streamed through shared memory in
-// batches of 256 records (one coalesced gather per thread).  For every list
-// entry each warp:
-//   1. skips the entry if its 2x16 pixel strip misses the entry's alpha-floor
-//      ellipse box (warp-uniform, no per-lane math);
-//   2. evaluates a float32 power and compares it with a conservative cut --
-//      lanes that certainly have alpha < alpha_floor stop here (the reference
+// One CTA per 16x16 tile, one thread per pixel; warp w owns tile rows 2w and
+// 2w+1.  The tile's depth-ordered list streams through shared memory in
+// batches of 256 records (one coalesced gather per thread).  While loading,
+// each thread also computes which warps' 2-row strips the record's
+// alpha-floor ellipse box can reach; every warp then compacts the batch to
+// its own list (ballot + popc), so a warp never iterates over splats that
+// cannot touch its pixels.
+//
+// Each warp walks its list in mini-batches of 8 splats:
+//   A  float32 screen per (splat, pixel): a conservative power cut rejects
+//      samples whose alpha is certainly below alpha_floor (the reference
 //      gives them no weight and no transmittance update, contributions.py:148);
-//   3. runs the exact float64 path on the surviving lanes: the reference's
-//      expression order without FMA contraction, float64 exp, the 0.99 clamp,
-//      the alpha floor, w = alpha*T, T *= (1-alpha), T floor after the update;
-//   4. aggregates: label-uniform warps reduce w with shuffles and issue one
-//      float64 atomic; mixed-label warps issue one atomic per contributing lane.
+//   A2 the surviving (splat, pixel) pairs of the mini-batch are packed into a
+//      per-warp queue and the exact float64 alpha -- the reference's
+//      expression order, no FMA contraction, float64 exp, 0.99 clamp -- is
+//      computed for 32 pairs per round (alpha does not depend on T, so the
+//      expensive part runs on full warps);
+//   B  per pixel, in list order: alpha floor, w = alpha*T, T *= (1-alpha),
+//      T floor after the update (contributions.py:148-157);
+//   C  label-uniform warps reduce the 8 rows of w with a padded transpose in
+//      shared memory + 2 shuffles and issue one float64 atomic per splat;
+//      mixed-label warps issue one atomic per contributing lane.
 // The CTA stops when no pixel of the tile is active (contributions.py:158-159).
+#include <algorithm>
+
 #include "fs_common.cuh"
 #include "fs_kernels.cuh"
+#include "fs_tilesort.cuh"
 
 namespace fs {
 
 namespace {
 
-constexpr int kRasterThreads = 256;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kBatch = 256;
+constexpr int kMini = 8;
+constexpr int kRowStride = 33;  // doubles per padded w/alpha row (bank-conflict-free transpose)
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
+struct RasterSmem {
+    Rec32 r32[kBatch];
+    Rec64 r64[kBatch];
+    unsigned int gid[kBatch];
+    unsigned char warp_mask[kBatch];
+    unsigned char list[kWarps][kBatch];
+    unsigned char queue[kWarps][kMini * 32];
+    double val[kWarps][kMini * kRowStride];  // alpha, then w
+    unsigned long long cnt_e[kWarps], cnt_a[kWarps];
+};
 
-__global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(RasterArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const ViewCounters* vc = a.vc;
     if (vc->overflow) return;
     const int tile = blockIdx.x;
-    const unsigned int begin = a.tile_start[tile], end = a.tile_start[tile + 1];
+    const unsigned int begin = a.sort.tile_start[tile], end = a.sort.tile_start[tile + 1];
     if (begin >= end) return;
-    const unsigned int* __restrict__ gids =
-        pass_parity(a.tile_or_and[0] ^ a.tile_or_and[1], a.tile_passes) ? a.inst_gid[1] : a.inst_gid[0];
 
-    __shared__ Rec32 s_r32[kBatch];
-    __shared__ Rec64 s_r64[kBatch];
-    __shared__ unsigned int s_gid[kBatch];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RasterSmem& S = *reinterpret_cast<RasterSmem*>(smem_raw);
+    // prologue: the tile's bucket of depth ranks -> gids in (depth, gid) order
+    // (reuses the walk's shared memory, fs_tilesort.cuh)
+    unsigned int* list = a.sort.inst + begin;
+    {
+        const unsigned int* sg =
+            sort_result_parity(a.sort.depth_state) ? a.sort.sorted_gid[1] : a.sort.sorted_gid[0];
+        sort_tile_list(list, a.sort.scratch + begin, end - begin, sg, a.sort.rank_bits,
+                       reinterpret_cast<unsigned int*>(smem_raw), a.sort.cap);
+    }
+    const unsigned int* __restrict__ gids = list - begin;  // indexed by instance position
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned int lt_mask = (1u << lane) - 1u;
     const int x0 = (tile % a.tiles_x) * kTile, y0 = (tile / a.tiles_x) * kTile;
     const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
     const bool inside = px < a.width && py < a.height;
     const unsigned int label = inside ? a.mask[(size_t)py * a.width + px] : 0u;
-    // pixel centre (k + 0.5, j + 0.5): exact in both precisions
-    const double pxc = (double)px + 0.5, pyc = (double)py + 0.5;
-    const float pxf = (float)pxc, pyf = (float)pyc;
-    // the warp's pixel-centre strip
+    const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
     const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
-    const float v_lo = (float)(y0 + 2 * warp) + 0.5f, v_hi = v_lo + 1.0f;
 
     const unsigned int inside_mask = __ballot_sync(0xffffffffu, inside);
     const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
@@ -66,6 +89,7 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(RasterArgs a)
     const double af = a.alpha_floor, tf = a.t_floor;
     const long long n_g = a.n_gaussians;
     double* __restrict__ acc = a.acc;
+    double* __restrict__ myval = S.val[warp];
 
     double T = 1.0;
     bool active = inside;
@@ -76,57 +100,123 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(RasterArgs a)
         // contributions.py:158-159 -- the whole tile terminated; also guards smem reuse
         if (__syncthreads_count(active) == 0) break;
         const unsigned int i = b + tid;
+        unsigned int wm = 0;
         if (i < end) {
             const unsigned int g = gids[i];
-            s_gid[tid] = g;
-            s_r32[tid] = a.r32[g];
-            s_r64[tid] = a.r64[g];
+            const Rec32 s = a.r32[g];
+            S.gid[tid] = g;
+            S.r32[tid] = s;
+            S.r64[tid] = a.r64[g];
+            // warps whose 2-row strip the alpha-floor ellipse box can reach
+            if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx)) {
+                const float r0 = ceilf(s.my - s.hy - 0.5f) - (float)y0;
+                const float r1 = floorf(s.my + s.hy - 0.5f) - (float)y0;
+                if (r1 >= 0.0f && r0 <= 15.0f) {
+                    const int w0 = max(0, (int)r0) >> 1, w1 = min(15, (int)r1) >> 1;
+                    wm = ((2u << w1) - 1u) & ~((1u << w0) - 1u);
+                }
+            }
         }
+        S.warp_mask[tid] = (unsigned char)wm;
         __syncthreads();
         const int nb = min((unsigned int)kBatch, end - b);
         steps += nb;
         if (!warp_live) continue;
-        for (int j = 0; j < nb; ++j) {
-            const Rec32 s = s_r32[j];
-            if (u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy || v_lo > s.my + s.hy)
-                continue;
-            const float du = pxf - s.mx, dv = pyf - s.my;
-            const float p = -0.5f * (s.a * du * du + s.c * dv * dv) - s.b * du * dv;
-            const bool cand = active && p >= s.cut;
-            const unsigned int cand_mask = __ballot_sync(0xffffffffu, cand);
-            if (!cand_mask) continue;
-            exact += __popc(cand_mask);
-            double w = 0.0;
-            if (cand) {
-                const Rec64 q = s_r64[j];
+        // per-warp compaction of the batch
+        int cnt = 0;
+#pragma unroll
+        for (int c = 0; c < kBatch / 32; ++c) {
+            const bool hit = (S.warp_mask[c * 32 + lane] >> warp) & 1u;
+            const unsigned int bal = __ballot_sync(0xffffffffu, hit);
+            if (hit) S.list[warp][cnt + __popc(bal & lt_mask)] = (unsigned char)(c * 32 + lane);
+            cnt += __popc(bal);
+        }
+        __syncwarp();
+        for (int m0 = 0; m0 < cnt; m0 += kMini) {
+            const int nm = min(kMini, cnt - m0);
+            // ---- A: float32 screen ----
+            unsigned int cm[kMini];
+            int base[kMini];
+            int total = 0;
+#pragma unroll
+            for (int k = 0; k < kMini; ++k) {
+                bool cand = false;
+                if (k < nm) {
+                    const Rec32 s = S.r32[S.list[warp][m0 + k]];
+                    const float du = pxf - s.mx, dv = pyf - s.my;
+                    const float p = -0.5f * (s.a * du * du + s.c * dv * dv) - s.b * du * dv;
+                    cand = active && p >= s.cut;
+                }
+                cm[k] = __ballot_sync(0xffffffffu, cand);
+                base[k] = total;
+                total += __popc(cm[k]);
+            }
+            if (total == 0) continue;
+            exact += total;
+            // ---- A2: exact float64 alpha on packed (splat, pixel) pairs ----
+#pragma unroll
+            for (int k = 0; k < kMini; ++k)
+                if ((cm[k] >> lane) & 1u)
+                    S.queue[warp][base[k] + __popc(cm[k] & lt_mask)] = (unsigned char)((k << 5) | lane);
+            __syncwarp();
+            for (int c = lane; c < total; c += 32) {
+                const unsigned int e = S.queue[warp][c];
+                const int k = e >> 5, src = e & 31;
+                const Rec64 q = S.r64[S.list[warp][m0 + k]];
+                // pixel centre (k + 0.5, j + 0.5) of the source lane, exact in float64
+                const double cx = (double)(x0 + (src & 15)) + 0.5;
+                const double cy = (double)(y0 + 2 * warp + (src >> 4)) + 0.5;
                 // power = -0.5 * (a*du*du + c*dv*dv) - b*du*dv   (contributions.py:142-145)
-                const double ddu = __dsub_rn(pxc, q.mx);
-                const double ddv = __dsub_rn(pyc, q.my);
+                const double ddu = __dsub_rn(cx, q.mx);
+                const double ddv = __dsub_rn(cy, q.my);
                 const double t1 = __dmul_rn(__dmul_rn(q.a, ddu), ddu);
                 const double t2 = __dmul_rn(__dmul_rn(q.c, ddv), ddv);
                 const double t3 = __dmul_rn(__dmul_rn(q.b, ddu), ddv);
                 const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), t3);
                 double alpha = __dmul_rn(q.o, exp(power));  // :146-147
-                alpha = alpha < kAlphaClamp ? alpha : kAlphaClamp;
-                const bool use = af > 0.0 ? (alpha >= af) : true;  // :148-149
-                if (use) {
-                    w = __dmul_rn(alpha, T);                    // :150
-                    T = __dmul_rn(T, __dsub_rn(1.0, alpha));    // :155
-                    if (tf > 0.0 && !(T >= tf)) active = false; // :156-157
+                myval[k * kRowStride + src] = alpha < kAlphaClamp ? alpha : kAlphaClamp;
+            }
+            __syncwarp();
+            // ---- B: per-pixel transmittance walk in list order ----
+            unsigned int cb[kMini];
+#pragma unroll
+            for (int k = 0; k < kMini; ++k) {
+                double w = 0.0;
+                if (((cm[k] >> lane) & 1u) && active) {
+                    const double alpha = myval[k * kRowStride + lane];
+                    if (af > 0.0 ? (alpha >= af) : true) {  // :148-149
+                        w = __dmul_rn(alpha, T);                     // :150
+                        T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
+                        if (tf > 0.0 && !(T >= tf)) active = false;  // :156-157
+                    }
+                }
+                myval[k * kRowStride + lane] = w;
+                cb[k] = __ballot_sync(0xffffffffu, w > 0.0);
+            }
+            __syncwarp();
+            // ---- C: aggregation + float64 atomics ----
+            if (uniform) {
+                const int k = lane & 7, seg = lane >> 3;
+                double v = 0.0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) v += myval[k * kRowStride + seg * 8 + t];
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                if (lane < kMini && k < nm && v > 0.0) {
+                    atomicAdd(acc + (size_t)lbl0 * n_g + S.gid[S.list[warp][m0 + k]], v);
+                }
+#pragma unroll
+                for (int t = 0; t < kMini; ++t) atom += cb[t] ? 1u : 0u;
+            } else {
+#pragma unroll
+                for (int k = 0; k < kMini; ++k) {
+                    if ((cb[k] >> lane) & 1u)
+                        atomicAdd(acc + (size_t)label * n_g + S.gid[S.list[warp][m0 + k]],
+                                  myval[k * kRowStride + lane]);
+                    atom += __popc(cb[k]);
                 }
             }
-            const unsigned int contrib = __ballot_sync(0xffffffffu, w > 0.0);
-            if (contrib) {
-                const unsigned int g = s_gid[j];
-                if (uniform) {
-                    const double sum = warp_sum(w);
-                    if (lane == 0) atomicAdd(acc + (size_t)lbl0 * n_g + g, sum);
-                    ++atom;
-                } else {
-                    if (w > 0.0) atomicAdd(acc + (size_t)label * n_g + g, w);
-                    atom += __popc(contrib);
-                }
-            }
+            __syncwarp();
             if (tf > 0.0) {
                 warp_live = __any_sync(0xffffffffu, active);
                 if (!warp_live) break;
@@ -134,17 +224,16 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(RasterArgs a)
         }
     }
     // per-CTA counters (one atomic each)
-    __shared__ unsigned long long s_e[8], s_a[8];
     if (lane == 0) {
-        s_e[warp] = exact;
-        s_a[warp] = atom;
+        S.cnt_e[warp] = exact;
+        S.cnt_a[warp] = atom;
     }
     __syncthreads();
     if (tid == 0) {
         unsigned long long e = 0, at = 0;
-        for (int w = 0; w < kRasterThreads / 32; ++w) {
-            e += s_e[w];
-            at += s_a[w];
+        for (int w = 0; w < kWarps; ++w) {
+            e += S.cnt_e[w];
+            at += S.cnt_a[w];
         }
         ViewCounters* v = a.vc;
         atomicAdd(&v->tile_steps, steps);
@@ -155,9 +244,21 @@ __global__ void __launch_bounds__(kRasterThreads, 4) raster_kernel(RasterArgs a)
 
 }  // namespace
 
+// Per device (called by fs_create after cudaSetDevice): opt in to >48 KB smem.
+static size_t raster_smem_bytes() {
+    return std::max(sizeof(RasterSmem), tile_sort_smem_bytes(kTileSortCap));
+}
+
+cudaError_t raster_configure() {
+    cudaError_t e = cudaFuncSetAttribute(raster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)raster_smem_bytes());
+    if (e != cudaSuccess) return e;
+    return tile_sort_configure(kTileSortCap);
+}
+
 void launch_raster(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
-    raster_kernel<<<a.ntiles, kRasterThreads, 0, st>>>(a);
+    raster_kernel<<<a.ntiles, kThreads, raster_smem_bytes(), st>>>(a);
 }
 
 }  // namespace fs

@@ -32,23 +32,48 @@ class LabelSolver:
         self.stats: dict = {}
 
     def accumulate(self, views: Sequence, num_objects: int,
-                   blend: BlendConfig = DEFAULT_BLEND, download: bool = True):
+                   blend: BlendConfig = DEFAULT_BLEND, download: bool = True,
+                   process_group=None):
+        """Accumulate A on the device (and keep it there); optionally view-sharded.
+
+        With ``process_group`` every rank validates all views (same errors on
+        every rank), accumulates its shard and one all-reduce joins them.
+        """
         views = list(views)
-        validate_views(views, int(num_objects))
-        n = len(self.scene)
         e = int(num_objects)
+        validate_views(views, e)
+        n = len(self.scene)
         ctx = self.ctx
+        acc_t = None
+        sel = views
+        if process_group is not None:
+            import torch
+            import torch.distributed as dist
+
+            from .distributed import shard_views
+            rank = dist.get_rank(process_group)
+            world = dist.get_world_size(process_group)
+            sel = [views[i] for i in shard_views(len(views), rank, world)]
+            acc_t = torch.zeros(e * max(n, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
+            acc_ptr = acc_t.data_ptr()
         with ctx.lock:
             ctx.set_scene(self.scene)
-            acc = ctx.alloc(8 * e * max(n, 1)).zero()
-            self.stats = ctx.accumulate([v for v, _ in views], [m.labels for _, m in views], e,
-                                        blend.alpha_floor, blend.transmittance_floor, acc.ptr)
+            if acc_t is None:
+                acc = ctx.alloc(8 * e * max(n, 1)).zero()
+                acc_ptr = acc.ptr
+            self.stats = ctx.accumulate([v for v, _ in sel], [m.labels for _, m in sel], e,
+                                        blend.alpha_floor, blend.transmittance_floor, acc_ptr)
+        if acc_t is not None:
+            import torch.distributed as dist
+            dist.all_reduce(acc_t, group=process_group)
+        with ctx.lock:
             if self._A is None or self._A.nbytes < 4 * e * max(n, 1):
                 self._A = ctx.alloc(4 * e * max(n, 1))
                 self._out = ctx.alloc(e * max(n, 1))
             if n:
-                ctx.finalize(acc.ptr, e * n, out_ptr=self._A.ptr)
-            acc.release()
+                ctx.finalize(acc_ptr, e * n, out_ptr=self._A.ptr)
+            if acc_t is None:
+                acc.release()
         self.num_objects = e
         if not download:
             return None
@@ -83,8 +108,12 @@ class LabelSolver:
 
 
 def solve(scene, views: Sequence, num_objects: int, gamma: float = 0.0, mode: str = "binary",
-          blend: BlendConfig = DEFAULT_BLEND, device: Optional[int] = None):
-    """(ContributionMatrix, Assignment) for one scene: the north-star entry point."""
+          blend: BlendConfig = DEFAULT_BLEND, device: Optional[int] = None, process_group=None):
+    """(ContributionMatrix, Assignment) for one scene: the north-star entry point.
+
+    Host numpy inputs in, host results out; with ``process_group`` the views
+    are sharded over the group's GPUs and every rank returns the full result.
+    """
     s = LabelSolver(scene, device)
-    matrix = s.accumulate(views, num_objects, blend)
+    matrix = s.accumulate(views, num_objects, blend, process_group=process_group)
     return matrix, s.assign(gamma, mode)

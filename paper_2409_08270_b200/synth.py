@@ -141,11 +141,17 @@ def analytic_masks(views, centers, radius, num_objects, rng=None, label_noise=0.
 
 def make_workload(seed: int, n_gaussians: int, n_views: int, width: int, height: int,
                   num_objects: int, label_noise: float = 0.0,
-                  scale_range=(0.002, 0.01), object_fraction: float = 0.5,
+                  scale_range=(0.002, 0.01), object_fraction=None,
                   iid_masks: bool = False, name: str = "") -> Workload:
-    """Box-geometry scene with E-1 ball objects and analytic (or iid) masks."""
+    """Box-geometry scene with E-1 ball objects and analytic (or iid) masks.
+
+    ``object_fraction`` (default: the balls' share of the box volume, i.e. a
+    uniform Gaussian density everywhere) of the Gaussians sit in the balls.
+    """
     rng = np.random.default_rng(seed)
     centers, radius = _ball_grid(num_objects - 1)
+    if object_fraction is None:
+        object_fraction = min(0.9, (num_objects - 1) * (4.0 / 3.0) * math.pi * radius ** 3 / 2.4 ** 3)
     n_obj_total = int(n_gaussians * object_fraction) if num_objects > 1 else 0
     per = n_obj_total // max(num_objects - 1, 1) if num_objects > 1 else 0
     parts, member = [], []

@@ -323,3 +323,31 @@ def test_label_solver_resident_matrix():
                               num_objects=2)
     M2, asn = fs.solve(wl2.scene, wl2.pairs(), 2, gamma=0.2)
     assert np.array_equal(asn.labels, oracle.assign_binary(M2.values, 0.2))
+
+
+def test_long_tile_buckets_merge_path():
+    # ~10k splats on a 64x48 image: every tile bucket exceeds the 4096-entry
+    # shared-memory sort, exercising the chunk sort + global merge path
+    from paper_2409_08270_b200 import CameraView
+    rng = np.random.default_rng(17)
+    n = 10000
+    means = np.stack([rng.uniform(-0.3, 0.3, n), rng.uniform(-0.2, 0.2, n),
+                      rng.choice(np.linspace(3.0, 4.0, 50), size=n)], axis=1)
+    scene = GaussianScene(means, rng.normal(size=(n, 4)), rng.uniform(0.05, 0.4, (n, 3)),
+                          rng.uniform(0.01, 0.05, n))
+    view = CameraView(0, 64, 48, 60.0, 60.0, 32.0, 24.0, np.eye(4))
+    ctx = _native.context(0)
+    with ctx.lock:
+        ctx.set_scene(scene)
+        offs, items = ctx.bin(view)
+    alive, mean2d, _, depth, radius, _ = oracle.project(scene.means, scene.rotations, scene.scales,
+                                                       oracle.camera_of(view))
+    o_offs, o_items = oracle.bin_tiles(alive, mean2d, depth, radius, view.width, view.height)
+    assert np.diff(o_offs).max() > 4096
+    assert np.array_equal(offs, o_offs)
+    assert np.array_equal(items, o_items)
+    m = LabelMask(0, rng.integers(0, 3, (48, 64), dtype=np.uint16))
+    A = accumulate_contributions(scene, [(view, m)], 3).values
+    ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities,
+                            [oracle.camera_of(view)], [m.labels], 3, threads=2)
+    np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
