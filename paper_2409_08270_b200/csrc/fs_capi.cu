@@ -73,10 +73,13 @@ struct Work {
     unsigned long long* status_depth = nullptr;
     unsigned long long* status_idx = nullptr;
     size_t status_depth_words = 0, status_idx_words = 0;
+    unsigned long long* k64 = nullptr;       // full depth key per gid (projection output)
+    unsigned int* pk[2] = {nullptr, nullptr};  // 32-bit primary depth keys (sort ping-pong)
+    unsigned long long* pk_oa = nullptr;     // OR/AND of the primary keys
     unsigned int* inst = nullptr;            // per-tile buckets: depth ranks, then gids
     unsigned int* scratch = nullptr;         // merge scratch for long buckets
-    unsigned int* tile_count = nullptr;      // ntiles
-    unsigned int* tile_cursor = nullptr;     // ntiles
+    unsigned int* count_bt = nullptr;        // ntiles x bin_blocks
+    unsigned int* partial = nullptr;         // bin_scan_blocks
     unsigned int* tile_start = nullptr;
     ViewCounters* vc = nullptr;
     unsigned long long* idx_oa = nullptr;  // OR/AND of the secondary (index) keys
@@ -139,7 +142,7 @@ void free_work(fs::Work& w) {
         if (p) cudaFree(p);
     };
     f(w.dkeys[0]); f(w.dkeys[1]); f(w.dvals[0]); f(w.dvals[1]); f(w.rect); f(w.r32); f(w.r64);
-    f(w.sdepth); f(w.sidx); f(w.status_depth); f(w.status_idx); f(w.inst); f(w.scratch); f(w.tile_count); f(w.tile_cursor);
+    f(w.k64); f(w.pk[0]); f(w.pk[1]); f(w.pk_oa); f(w.sdepth); f(w.sidx); f(w.status_depth); f(w.status_idx); f(w.inst); f(w.scratch); f(w.count_bt); f(w.partial);
     f(w.tile_start); f(w.vc); f(w.idx_oa); f(w.mask_dev);
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
@@ -158,6 +161,9 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
             if ((rc = dev_alloc(&w.dvals[k], n))) return rc;
         }
         if ((rc = dev_alloc(&w.rect, n))) return rc;
+        if ((rc = dev_alloc(&w.k64, n))) return rc;
+        if ((rc = dev_alloc(&w.pk[0], n))) return rc;
+        if ((rc = dev_alloc(&w.pk[1], n))) return rc;
         if ((rc = dev_alloc(&w.r32, n))) return rc;
         if ((rc = dev_alloc(&w.r64, n))) return rc;
         w.n_cap = n;
@@ -165,8 +171,10 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
     if (!w.vc) {
         if ((rc = dev_alloc(&w.vc, 1))) return rc;
         if ((rc = dev_alloc(&w.idx_oa, 2))) return rc;
+        if ((rc = dev_alloc(&w.pk_oa, 2))) return rc;
         if ((rc = dev_alloc(&w.sdepth, 1))) return rc;
         if ((rc = dev_alloc(&w.sidx, 1))) return rc;
+        if ((rc = dev_alloc(&w.partial, (size_t)fs::bin_scan_blocks(ctx->num_sms)))) return rc;
         CK(cudaMemset(w.sdepth, 0, sizeof(fs::SortState)));
         CK(cudaMemset(w.sidx, 0, sizeof(fs::SortState)));
     }
@@ -191,8 +199,7 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
     }
     if (ntiles > w.ntiles_cap) {
         if ((rc = dev_alloc(&w.tile_start, (size_t)ntiles + 1))) return rc;
-        if ((rc = dev_alloc(&w.tile_count, (size_t)ntiles))) return rc;
-        if ((rc = dev_alloc(&w.tile_cursor, (size_t)ntiles))) return rc;
+        if ((rc = dev_alloc(&w.count_bt, (size_t)ntiles * fs::bin_blocks(ctx->num_sms)))) return rc;
         w.ntiles_cap = ntiles;
     }
     if (mask_px > w.mask_cap) {
@@ -224,8 +231,8 @@ int check_cam(const fs_camera& c, int idx) {
                     c.height);
     long long tiles = (long long)fs::tiles_x_of(c.width) * fs::tiles_y_of(c.height);
     if (tiles > (1 << 24)) return fail(FS_EINVAL, "view %d: image too large (%lld tiles)", idx, tiles);
-    if (fs::tiles_x_of(c.width) > 65535 || fs::tiles_y_of(c.height) > 65535)
-        return fail(FS_EINVAL, "view %d: image too large", idx);
+    if (tiles > fs::kMaxTiles)
+        return fail(FS_EINVAL, "view %d: image too large (%lld tiles > %d)", idx, tiles, fs::kMaxTiles);
     return FS_OK;
 }
 
@@ -235,9 +242,9 @@ fs::BinBuffers bin_buffers(fs::Work& w) {
     b.sorted_gid[1] = w.dvals[1];
     b.depth_state = w.sdepth;
     b.rect = w.rect;
-    b.tile_count = w.tile_count;
+    b.count_bt = w.count_bt;
+    b.partial = w.partial;
     b.tile_start = w.tile_start;
-    b.tile_cursor = w.tile_cursor;
     b.inst = w.inst;
     b.capacity = w.inst_cap;
     return b;
@@ -250,6 +257,9 @@ fs::TileSortArgs tile_sort_args(fs::Work& w, long long n) {
     t.scratch = w.scratch;
     t.sorted_gid[0] = w.dvals[0];
     t.sorted_gid[1] = w.dvals[1];
+    t.sorted_pkey[0] = w.pk[0];
+    t.sorted_pkey[1] = w.pk[1];
+    t.k64 = w.k64;
     t.depth_state = w.sdepth;
     t.rank_bits = fs::bits_for((unsigned)(n > 0 ? n - 1 : 0));
     t.cap = fs::kTileSortCap;
@@ -263,22 +273,23 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
                  int cull_floor, fs::ProjectExport ex, cudaEvent_t after_sort = nullptr) {
     const int n = (int)ctx->n;
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
-    cudaMemsetAsync(w.tile_count, 0, sizeof(unsigned int) * (size_t)ntiles, w.stream);
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
-                       cull_floor, w.dkeys[0], w.dvals[0], w.rect, w.tile_count, w.r32, w.r64,
-                       w.vc, ex, ctx->num_sms, w.stream);
-    // invisible Gaussians carry the all-ones key; the sort substitutes the AND
-    // of the visible keys so they never add permuting digits
-    fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
-                                              nullptr, (unsigned)n, &w.vc->key_or,
-                                              &w.vc->key_and, 8, w.sdepth, w.status_depth,
-                                              ctx->num_sms, w.stream);
+                       cull_floor, w.k64, w.dvals[0], w.rect, nullptr, w.r32, w.r64, w.vc, ex,
+                       ctx->num_sms, w.stream);
+    // depth order: stable radix sort of the 32 highest varying key bits (gid
+    // order in, so exact ties stay in gid order); residual ties of the primary
+    // key are resolved against the full 64-bit key by the per-tile sort
+    fs::launch_primary_keys(n, w.k64, &w.vc->key_or, nullptr, nullptr, nullptr, w.pk[0], w.dvals[0],
+                            w.pk_oa, ctx->num_sms, w.stream);
+    fs::launch_radix_sort<unsigned int>(w.pk[0], w.dvals[0], w.pk[1], w.dvals[1], nullptr,
+                                        (unsigned)n, w.pk_oa, nullptr, 4, w.sdepth, w.status_depth,
+                                        ctx->num_sms, w.stream);
     if (after_sort) cudaEventRecord(after_sort, w.stream);
     fs::launch_bin(n, ntiles, tx, bin_buffers(w), w.vc, ctx->num_sms, w.stream);
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + (3 + 8) + 2 + 1 + 1; }
+int view_launches() { return 1 + 1 + 1 + (3 + 4) + 5 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
@@ -353,6 +364,7 @@ int fs_create(int device, int n_streams, fs_context** out) {
     }
     ctx->num_sms = prop.multiProcessorCount;
     e = fs::raster_configure();
+    if (e == cudaSuccess) e = fs::bin_configure();
     if (e != cudaSuccess) {
         delete ctx;
         return fs::set_cuda_error(e, "raster_configure", __FILE__, __LINE__);
@@ -589,15 +601,16 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
         if ((rc = ensure_work(ctx, w, std::max<long long>(k, 1), ntiles, cap, 1))) return rc;
         const unsigned long long init[2] = {0ull, ~0ull};
         CK(cudaMemcpyAsync(w.idx_oa, init, sizeof(init), cudaMemcpyHostToDevice, w.stream));
-        CK(cudaMemsetAsync(w.tile_count, 0, sizeof(unsigned int) * (size_t)ntiles, w.stream));
         fs::launch_view_begin(w.vc, w.stream);
         // LSD: stable sort by gaussian index, then stable sort by depth
         fs::launch_bin_splats_keys((int)k, d_idx, d_mean, d_rad, d_depth, width, height, w.dkeys[0],
-                                   w.dvals[0], w.dkeys[1], w.dvals[1], w.rect, w.tile_count,
-                                   w.idx_oa, w.sidx, w.status_idx, w.vc, ctx->num_sms, w.stream);
-        fs::launch_radix_sort<unsigned long long>(w.dkeys[0], w.dvals[0], w.dkeys[1], w.dvals[1],
-                                                  nullptr, (unsigned)k, &w.vc->key_or, nullptr, 8,
-                                                  w.sdepth, w.status_depth, ctx->num_sms, w.stream);
+                                   w.dvals[0], w.dkeys[1], w.dvals[1], w.rect, w.k64, w.idx_oa,
+                                   w.sidx, w.status_idx, w.vc, ctx->num_sms, w.stream);
+        fs::launch_primary_keys((int)k, w.k64, &w.vc->key_or, w.dvals[0], w.dvals[1], w.sidx,
+                                w.pk[0], w.dvals[0], w.pk_oa, ctx->num_sms, w.stream);
+        fs::launch_radix_sort<unsigned int>(w.pk[0], w.dvals[0], w.pk[1], w.dvals[1], nullptr,
+                                            (unsigned)k, w.pk_oa, nullptr, 4, w.sdepth,
+                                            w.status_depth, ctx->num_sms, w.stream);
         fs::launch_bin((int)k, ntiles, tx, bin_buffers(w), w.vc, ctx->num_sms, w.stream);
         fs::launch_tile_sort(ntiles, tile_sort_args(w, k), w.stream);
         CK(cudaGetLastError());

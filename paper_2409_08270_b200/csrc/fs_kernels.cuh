@@ -66,15 +66,19 @@ int launch_radix_sort(K* keys0, unsigned int* vals0, K* keys1, unsigned int* val
 
 // ---- fs_bin.cu ----
 struct BinBuffers {
-    const unsigned int* sorted_gid[2];  // depth sort result (ping-pong)
+    const unsigned int* sorted_gid[2];  // depth sort values (ping-pong)
     const SortState* depth_state;       // which of the two holds it
     const unsigned long long* rect;     // per gid
-    const unsigned int* tile_count;     // per tile (from the projection)
+    unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets
+    unsigned int* partial;              // bin_scan_blocks() partial sums
     unsigned int* tile_start;           // ntiles + 1
-    unsigned int* tile_cursor;          // ntiles
     unsigned int* inst;                 // capacity: ranks, gids after the per-tile sort
     unsigned int capacity;
 };
+constexpr int kMaxTiles = 49152;        // per-block tile histograms live in shared memory
+int bin_blocks(int num_sms);
+int bin_scan_blocks(int num_sms);
+cudaError_t bin_configure();
 void launch_bin(int n, int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc,
                 int num_sms, cudaStream_t st);
 
@@ -82,12 +86,35 @@ struct TileSortArgs {
     const unsigned int* tile_start;
     unsigned int* inst;
     unsigned int* scratch;
-    const unsigned int* sorted_gid[2];
+    const unsigned int* sorted_gid[2];   // depth sort values (ping-pong)
+    const unsigned int* sorted_pkey[2];  // depth sort 32-bit primary keys (ping-pong)
+    const unsigned long long* k64;       // full 64-bit depth key per gid
     const SortState* depth_state;
     int rank_bits;
     unsigned int cap;
     const ViewCounters* vc;
 };
+
+// Resolved (device-side) view of the depth order used by the per-tile sort.
+struct TileSortKeys {
+    const unsigned int* sorted_gid;
+    const unsigned int* pkey;
+    const unsigned long long* k64;
+    int rank_bits;
+};
+__device__ __forceinline__ TileSortKeys resolve_keys(const TileSortArgs& t) {
+    const int p = sort_result_parity(t.depth_state);
+    return TileSortKeys{t.sorted_gid[p], t.sorted_pkey[p], t.k64, t.rank_bits};
+}
+
+// 32-bit primary depth keys: the 32 highest varying bits of the 64-bit keys
+// (from their OR/AND), written in the order given by `order` (order0, or the
+// result buffer of order_state's sort; both null: gid order); pk_oa receives
+// the OR/AND of the primary keys.
+void launch_primary_keys(int n, const unsigned long long* k64, const unsigned long long* oa64,
+                         const unsigned int* order0, const unsigned int* order1,
+                         const SortState* order_state, unsigned int* pk, unsigned int* vals,
+                         unsigned long long* pk_oa, int num_sms, cudaStream_t st);
 size_t tile_sort_smem_bytes(unsigned int cap);
 cudaError_t tile_sort_configure(unsigned int cap);
 void launch_tile_sort(int ntiles, const TileSortArgs& t, cudaStream_t st);
@@ -97,7 +124,7 @@ void launch_tile_sort(int ntiles, const TileSortArgs& t, cudaStream_t st);
 void launch_bin_splats_keys(int k, const long long* index, const double* mean2d,
                             const long long* radius, const double* depth, int width, int height,
                             unsigned long long* dk0, unsigned int* dv0, unsigned long long* dk1,
-                            unsigned int* dv1, unsigned long long* rect, unsigned int* tile_count,
+                            unsigned int* dv1, unsigned long long* rect, unsigned long long* k64,
                             unsigned long long* idx_oa, SortState* idx_state,
                             unsigned long long* idx_status, ViewCounters* vc, int num_sms,
                             cudaStream_t st);

@@ -64,12 +64,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     // prologue: the tile's bucket of depth ranks -> gids in (depth, gid) order
     // (reuses the walk's shared memory, fs_tilesort.cuh)
     unsigned int* list = a.sort.inst + begin;
-    {
-        const unsigned int* sg =
-            sort_result_parity(a.sort.depth_state) ? a.sort.sorted_gid[1] : a.sort.sorted_gid[0];
-        sort_tile_list(list, a.sort.scratch + begin, end - begin, sg, a.sort.rank_bits,
-                       reinterpret_cast<unsigned int*>(smem_raw), a.sort.cap);
-    }
+    sort_tile_list(list, a.sort.scratch + begin, end - begin, resolve_keys(a.sort),
+                   reinterpret_cast<unsigned int*>(smem_raw), a.sort.cap);
     const unsigned int* __restrict__ gids = list - begin;  // indexed by instance position
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -140,9 +140,34 @@ static __device__ void block_merge(const unsigned int* src, unsigned int* dst, u
     }
 }
 
-static __device__ __noinline__ void sort_tile_list(unsigned int* list, unsigned int* scratch, unsigned int n,
-                               const unsigned int* __restrict__ sorted_gid, int rank_bits,
-                               unsigned int* smem, unsigned int cap) {
+// Entries whose 32-bit primary depth keys tie are re-ordered by the full
+// 64-bit key (stable, so gid order survives among exact ties).  `rk` holds
+// depth ranks (sorted), `pk` their primary keys; runs of equal pk are
+// contiguous because ranks are ordered by pk.  Runs are tiny in practice.
+static __device__ void fix_primary_ties(unsigned int* rk, const unsigned int* pk, unsigned int n,
+                                        const unsigned int* __restrict__ sorted_gid,
+                                        const unsigned long long* __restrict__ k64) {
+    for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads) {
+        if (pk[i + 1] != pk[i] || (i > 0 && pk[i - 1] == pk[i])) continue;  // not a run start
+        unsigned int j = i + 1;
+        while (j + 1 < n && pk[j + 1] == pk[i]) ++j;
+        // insertion sort rk[i..j] by k64[gid] (stable)
+        for (unsigned int x = i + 1; x <= j; ++x) {
+            const unsigned int r = rk[x];
+            const unsigned long long key = k64[sorted_gid[r]];
+            unsigned int y = x;
+            while (y > i && k64[sorted_gid[rk[y - 1]]] > key) {
+                rk[y] = rk[y - 1];
+                --y;
+            }
+            rk[y] = r;
+        }
+    }
+}
+
+static __device__ __noinline__ void sort_tile_list(unsigned int* list, unsigned int* scratch,
+                                                   unsigned int n, const TileSortKeys& K,
+                                                   unsigned int* smem, unsigned int cap) {
     unsigned int* a = smem;
     unsigned int* b = smem + cap;
     unsigned int* whist = smem + 2 * cap;
@@ -150,8 +175,13 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list, unsigned 
     if (n <= cap) {
         for (unsigned int i = threadIdx.x; i < n; i += kThreads) a[i] = list[i];
         __syncthreads();
-        const unsigned int* res = smem_radix_sort(a, b, n, rank_bits, whist, misc);
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = sorted_gid[res[i]];
+        unsigned int* res = smem_radix_sort(a, b, n, K.rank_bits, whist, misc);
+        unsigned int* pk = res == a ? b : a;
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) pk[i] = K.pkey[res[i]];
+        __syncthreads();
+        fix_primary_ties(res, pk, n, K.sorted_gid, K.k64);
+        __syncthreads();
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = K.sorted_gid[res[i]];
         __syncthreads();
         return;
     }
@@ -160,7 +190,7 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list, unsigned 
         const unsigned int m = min(cap, n - c0);
         for (unsigned int i = threadIdx.x; i < m; i += kThreads) a[i] = list[c0 + i];
         __syncthreads();
-        const unsigned int* res = smem_radix_sort(a, b, m, rank_bits, whist, misc);
+        const unsigned int* res = smem_radix_sort(a, b, m, K.rank_bits, whist, misc);
         for (unsigned int i = threadIdx.x; i < m; i += kThreads) list[c0 + i] = res[i];
         __syncthreads();
     }
@@ -177,7 +207,14 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list, unsigned 
         src = dst;
         dst = t;
     }
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = sorted_gid[src[i]];
+    // primary keys of the merged list go to the other global buffer
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) dst[i] = K.pkey[src[i]];
+    __threadfence_block();
+    __syncthreads();
+    fix_primary_ties(src, dst, n, K.sorted_gid, K.k64);
+    __threadfence_block();
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = K.sorted_gid[src[i]];
     __syncthreads();
 }
 

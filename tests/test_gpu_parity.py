@@ -351,3 +351,32 @@ def test_long_tile_buckets_merge_path():
     ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities,
                             [oracle.camera_of(view)], [m.labels], 3, threads=2)
     np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+
+
+def test_primary_key_ties_resolved_by_full_depth():
+    # depths spread over [2, 6] plus 1500 splats within 1e-11 of 3.0: the 32-bit
+    # primary depth keys tie for the latter, the full float64 order must win
+    from paper_2409_08270_b200 import CameraView
+    rng = np.random.default_rng(23)
+    n_near, n_far = 1500, 1500
+    z_near = 3.0 + rng.permutation(n_near) * 7e-15
+    z = np.concatenate([z_near, rng.uniform(2.0, 6.0, n_far)])
+    n = n_near + n_far
+    xy = rng.uniform(-0.15, 0.15, (n, 2)) * z[:, None]
+    scene = GaussianScene(np.c_[xy, z], np.tile([1.0, 0, 0, 0], (n, 1)),
+                          rng.uniform(0.01, 0.05, (n, 3)), rng.uniform(0.05, 0.3, n))
+    view = CameraView(0, 96, 64, 100.0, 100.0, 48.0, 32.0, np.eye(4))
+    ctx = _native.context(0)
+    with ctx.lock:
+        ctx.set_scene(scene)
+        offs, items = ctx.bin(view)
+    alive, mean2d, _, depth, radius, _ = oracle.project(scene.means, scene.rotations, scene.scales,
+                                                       oracle.camera_of(view))
+    o_offs, o_items = oracle.bin_tiles(alive, mean2d, depth, radius, view.width, view.height)
+    assert np.array_equal(offs, o_offs)
+    assert np.array_equal(items, o_items)
+    m = LabelMask(0, rng.integers(0, 2, (64, 96), dtype=np.uint16))
+    A = accumulate_contributions(scene, [(view, m)], 2).values
+    ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities,
+                            [oracle.camera_of(view)], [m.labels], 2, threads=2)
+    np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
