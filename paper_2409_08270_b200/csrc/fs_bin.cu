@@ -1,23 +1,20 @@
-// fs_bin.cu -- K2b-K2d: tile binning on the device (reference rasterizer.py:72-113).
+// fs_bin.cu -- K2: tile binning on the device (reference rasterizer.py:72-113).
 //
-// Input: all N Gaussians sorted by (depth, gid) by the depth radix sort
-// (fs_sort.cu) -- the position of a Gaussian in that order is its depth
-// rank -- plus each Gaussian's inclusive tile rectangle and the per-tile
-// instance counts, both produced by the projection kernel.
+// TileBinning appends every visible splat, in (depth, index) order, to every
+// tile its inclusive radius box covers.  Here the work splits in two:
 //
-//   tile_scan    one block: exclusive scan of the tile counts -> tile_start,
-//                per-tile write cursors, instance total, overflow flag;
-//   emit_ranks   one thread per depth rank: append the rank to the bucket of
-//                every tile its rectangle covers (atomic cursor, any order);
-//   sort_tile    one CTA per tile (inside the raster kernel, or standalone for
-//                the binning API): sort the bucket's ranks in shared memory
-//                (stable LSD radix, 8-bit digits, digits constant over the
-//                tile skipped), map rank -> gid.  Ranks are unique, so the
-//                result is exactly TileBinning.tile_lists' (depth, gid)
-//                order.  Buckets longer than the shared-memory capacity are
-//                sorted in chunks and merged through global memory.
-// Sorting each tile's short bucket in shared memory replaces a global radix
-// sort of all (tile, rank) instances.
+//   binning   (this file) -- per-tile buckets of gids in arbitrary order:
+//     bin_count   per-block tile histogram over a contiguous gid range (shared
+//                 memory atomics), written to a tile-major count matrix; also
+//                 the 16-bit primary depth key of every gid;
+//     scan        exclusive scan of the count matrix -> per-(tile, block)
+//                 write offsets, tile_start, instance total, overflow flag;
+//     bin_emit    every block re-walks its gid range and places instances
+//                 with shared-memory cursors (no global atomics);
+//   ordering  (fs_tilesort.cuh) -- each tile's bucket is sorted in shared
+//             memory by the primary key, ties resolved by (float64 key, id).
+//
+// No global sort of N depth keys or of the (tile, splat) instances is needed.
 #include <algorithm>
 
 #include "fs_common.cuh"
@@ -31,26 +28,42 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-__device__ __forceinline__ void rank_range(int n, int b, int g, int& lo, int& hi) {
+__device__ __forceinline__ void gid_range(int n, int b, int g, int& lo, int& hi) {
     const long long per = ((long long)n + g - 1) / g;
     lo = (int)min((long long)n, per * b);
     hi = (int)min((long long)n, per * (b + 1));
 }
 
-// per-block tile histogram of a contiguous range of depth ranks -> count[t * g + b]
-__global__ void __launch_bounds__(kThreads) bin_count_kernel(
-    int n, int ntiles, int tiles_x, const unsigned int* __restrict__ v0,
-    const unsigned int* __restrict__ v1, const SortState* __restrict__ dst,
-    const unsigned long long* __restrict__ rect, unsigned int* __restrict__ count_bt) {
+// Primary key: the 16 highest bits in which the view's depth keys differ.
+__device__ __forceinline__ int primary_shift(const unsigned long long* oa) {
+    const unsigned long long vary = oa[0] ^ oa[1];
+    const int hb = vary ? 63 - __clzll((long long)vary) : 0;
+    return hb > 15 ? hb - 15 : 0;
+}
+
+// per-block tile histogram of a contiguous gid range -> count[t * g + b];
+// primary depth keys of the range
+__global__ void __launch_bounds__(kThreads) bin_count_kernel(BinBuffers b, int ntiles,
+                                                             int tiles_x) {
     extern __shared__ unsigned int s_hist[];
     for (int t = threadIdx.x; t < ntiles; t += kThreads) s_hist[t] = 0;
     __syncthreads();
-    const unsigned int* gids = sort_result_parity(dst) ? v1 : v0;
+    const int shift = primary_shift(b.key_oa);
+    const unsigned long long z = b.key_oa[1];
     int lo, hi;
-    rank_range(n, blockIdx.x, gridDim.x, lo, hi);
-    for (int r = lo + threadIdx.x; r < hi; r += kThreads) count_rect_tiles(rect[gids[r]], tiles_x, s_hist);
+    gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
+    for (int g = lo + threadIdx.x; g < hi; g += kThreads) {
+        const unsigned long long rc = b.rect[g];
+        count_rect_tiles(rc, tiles_x, s_hist);
+        if (rc != ~0ull) {
+            unsigned long long key = b.k64[g];
+            if (key == ~0ull) key = z;
+            b.pk[g] = (unsigned short)((key >> shift) & 0xFFFFull);
+        }
+    }
     __syncthreads();
-    for (int t = threadIdx.x; t < ntiles; t += kThreads) count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
+    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+        b.count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
 }
 
 // exclusive scan of v over the block (blockDim == kThreads); *total = block sum
@@ -139,28 +152,24 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(unsigned int* __re
 }
 
 // per-block: cursors from the scanned matrix, then shared-memory atomics place
-// every instance of the block's rank range (buckets: block segments in rank
-// order; order inside a segment is restored by the per-tile sort)
-__global__ void __launch_bounds__(kThreads) bin_emit_kernel(
-    int n, int ntiles, int tiles_x, const unsigned int* __restrict__ v0,
-    const unsigned int* __restrict__ v1, const SortState* __restrict__ dst,
-    const unsigned long long* __restrict__ rect, const unsigned int* __restrict__ off_bt,
-    unsigned int* __restrict__ inst, const ViewCounters* __restrict__ vc) {
+// every instance of the block's gid range
+__global__ void __launch_bounds__(kThreads) bin_emit_kernel(BinBuffers b, int ntiles, int tiles_x,
+                                                            const ViewCounters* __restrict__ vc) {
     if (vc->overflow) return;
     extern __shared__ unsigned int s_cur[];
-    for (int t = threadIdx.x; t < ntiles; t += kThreads) s_cur[t] = off_bt[(size_t)t * gridDim.x + blockIdx.x];
+    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+        s_cur[t] = b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
     __syncthreads();
-    const unsigned int* gids = sort_result_parity(dst) ? v1 : v0;
     int lo, hi;
-    rank_range(n, blockIdx.x, gridDim.x, lo, hi);
-    for (int r = lo + threadIdx.x; r < hi; r += kThreads) {
-        const unsigned long long rc = rect[gids[r]];
+    gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
+    for (int g = lo + threadIdx.x; g < hi; g += kThreads) {
+        const unsigned long long rc = b.rect[g];
         if (rc == ~0ull) continue;
         const unsigned int tx0 = rc & 0xFFFF, tx1 = (rc >> 16) & 0xFFFF;
         const unsigned int ty0 = (rc >> 32) & 0xFFFF, ty1 = (rc >> 48) & 0xFFFF;
         for (unsigned int ty = ty0; ty <= ty1; ++ty)
             for (unsigned int tx = tx0; tx <= tx1; ++tx)
-                inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = (unsigned int)r;
+                b.inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = (unsigned int)g;
     }
 }
 
@@ -170,11 +179,8 @@ __global__ void __launch_bounds__(kThreads) tile_sort_kernel(TileSortArgs t) {
     if (t.vc->overflow) return;
     const unsigned int begin = t.tile_start[tile], end = t.tile_start[tile + 1];
     if (begin >= end) return;
-    sort_tile_list(t.inst + begin, t.scratch + begin, end - begin, resolve_keys(t),
-                   reinterpret_cast<unsigned int*>(smem_raw), t.cap);
+    sort_tile_list(t.inst + begin, t.scratch64 + 2ull * begin, end - begin, t.keys, smem_raw, t.cap);
 }
-
-// ---- binning of an explicit splat list (TileBinning over ProjectedGaussian) ----
 
 __device__ __forceinline__ void block_or_and(unsigned long long o, unsigned long long a,
                                              unsigned long long* dst) {
@@ -188,47 +194,21 @@ __device__ __forceinline__ void block_or_and(unsigned long long o, unsigned long
     }
 }
 
-// keys = gaussian index (secondary sort key), vals = list position, rect +
-// tile counts per position
-__global__ void splat_index_kernel(int k, const long long* __restrict__ index,
-                                   const double* __restrict__ mean2d,
-                                   const long long* __restrict__ radius, int width, int height,
-                                   unsigned long long* __restrict__ keys,
-                                   unsigned int* __restrict__ vals,
-                                   unsigned long long* __restrict__ rect,
-                                   unsigned int* __restrict__ tile_count,
-                                   unsigned long long* __restrict__ oa) {
+// explicit splat list: rect + depth key per list position, key OR/AND
+__global__ void splat_keys_kernel(int k, const double* __restrict__ mean2d,
+                                  const long long* __restrict__ radius,
+                                  const double* __restrict__ depth, int width, int height,
+                                  unsigned long long* __restrict__ rect,
+                                  unsigned long long* __restrict__ k64,
+                                  ViewCounters* __restrict__ vc) {
     const int tx_n = tiles_x_of(width), ty_n = tiles_y_of(height);
     const int stride = gridDim.x * blockDim.x;
     const int iters = (k + stride - 1) / stride;
     unsigned long long o = 0, a = ~0ull;
     for (int it = 0; it < iters; ++it) {
-        int i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+        const int i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
         if (i < k) {
-            unsigned long long key = (unsigned long long)index[i] ^ 0x8000000000000000ull;
-            keys[i] = key;
-            vals[i] = (unsigned)i;
-            o |= key;
-            a &= key;
-            const unsigned long long rc =
-                tile_rect(mean2d[2 * i], mean2d[2 * i + 1], (double)radius[i], tx_n, ty_n);
-            rect[i] = rc;
-        }
-    }
-    block_or_and(o, a, oa);
-}
-
-// 64-bit depth key per list position (the index sort's result gives the
-// stable input order of the depth sort)
-__global__ void splat_depth_kernel(int k, const double* __restrict__ depth,
-                                   unsigned long long* __restrict__ k64,
-                                   ViewCounters* __restrict__ vc) {
-    const int stride = gridDim.x * blockDim.x;
-    const int iters = (k + stride - 1) / stride;
-    unsigned long long o = 0, a = ~0ull;
-    for (int it = 0; it < iters; ++it) {
-        int i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
-        if (i < k) {
+            rect[i] = tile_rect(mean2d[2 * i], mean2d[2 * i + 1], (double)radius[i], tx_n, ty_n);
             const unsigned long long key = f64_sort_key(depth[i]);
             k64[i] = key;
             o |= key;
@@ -236,31 +216,6 @@ __global__ void splat_depth_kernel(int k, const double* __restrict__ depth,
         }
     }
     block_or_and(o, a, &vc->key_or);
-}
-
-__global__ void primary_keys_kernel(int n, const unsigned long long* __restrict__ k64,
-                                    const unsigned long long* __restrict__ oa64,
-                                    const unsigned int* order0, const unsigned int* order1,
-                                    const SortState* __restrict__ order_state,
-                                    unsigned int* __restrict__ pk, unsigned int* vals,
-                                    unsigned long long* __restrict__ pk_oa) {
-    const unsigned int* order = order_state ? (sort_result_parity(order_state) ? order1 : order0)
-                                            : order0;
-    const unsigned long long o = oa64[0], z = oa64[1];
-    const unsigned long long vary = o ^ z;
-    const int hb = vary ? 63 - __clzll((long long)vary) : 0;
-    const int shift = hb > 31 ? hb - 31 : 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        pk_oa[0] = (unsigned int)(o >> shift);
-        pk_oa[1] = (unsigned int)(z >> shift);
-    }
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const unsigned int g = order ? order[i] : (unsigned int)i;
-        unsigned long long key = k64[g];
-        if (key == ~0ull) key = z;  // invisible: never widens the varying digits
-        pk[i] = (unsigned int)(key >> shift);
-        vals[i] = g;
-    }
 }
 
 }  // namespace
@@ -276,22 +231,21 @@ cudaError_t bin_configure() {
                                 (int)(kMaxTiles * sizeof(unsigned int)));
 }
 
-void launch_bin(int n, int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc,
-                int num_sms, cudaStream_t st) {
+void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
+                cudaStream_t st) {
     const int g = bin_blocks(num_sms), g2 = bin_scan_blocks(num_sms);
     const size_t smem = sizeof(unsigned int) * (size_t)ntiles;
     const long long m = (long long)ntiles * g;
-    bin_count_kernel<<<g, kThreads, smem, st>>>(n, ntiles, tiles_x, b.sorted_gid[0], b.sorted_gid[1],
-                                                b.depth_state, b.rect, b.count_bt);
+    bin_count_kernel<<<g, kThreads, smem, st>>>(b, ntiles, tiles_x);
     scan_reduce_kernel<<<g2, kThreads, 0, st>>>(b.count_bt, m, b.partial);
     scan_partials_kernel<<<1, 1024, 0, st>>>(b.partial, g2, b.capacity, vc);
     scan_apply_kernel<<<g2, kThreads, 0, st>>>(b.count_bt, m, g, b.partial, ntiles, b.tile_start, vc);
-    bin_emit_kernel<<<g, kThreads, smem, st>>>(n, ntiles, tiles_x, b.sorted_gid[0], b.sorted_gid[1],
-                                               b.depth_state, b.rect, b.count_bt, b.inst, vc);
+    bin_emit_kernel<<<g, kThreads, smem, st>>>(b, ntiles, tiles_x, vc);
 }
 
 size_t tile_sort_smem_bytes(unsigned int cap) {
-    return sizeof(unsigned int) * (2 * (size_t)cap + kWarps * 256 + 64);
+    // two packed (key, gid) buffers, per-warp digit counters, misc, run flags
+    return 16 * (size_t)cap + sizeof(unsigned int) * (kWarps * 256 + 64) + cap;
 }
 
 cudaError_t tile_sort_configure(unsigned int cap) {
@@ -304,29 +258,12 @@ void launch_tile_sort(int ntiles, const TileSortArgs& t, cudaStream_t st) {
     tile_sort_kernel<<<ntiles, kThreads, tile_sort_smem_bytes(t.cap), st>>>(t);
 }
 
-void launch_bin_splats_keys(int k, const long long* index, const double* mean2d,
-                            const long long* radius, const double* depth, int width, int height,
-                            unsigned long long* dk0, unsigned int* dv0, unsigned long long* dk1,
-                            unsigned int* dv1, unsigned long long* rect, unsigned long long* k64,
-                            unsigned long long* idx_oa, SortState* idx_state,
-                            unsigned long long* idx_status, ViewCounters* vc, int num_sms,
-                            cudaStream_t st) {
+void launch_splat_keys(int k, const double* mean2d, const long long* radius, const double* depth,
+                       int width, int height, unsigned long long* rect, unsigned long long* k64,
+                       ViewCounters* vc, int num_sms, cudaStream_t st) {
     if (k <= 0) return;
-    int grid = std::min((k + 255) / 256, num_sms * 8);
-    splat_index_kernel<<<grid, 256, 0, st>>>(k, index, mean2d, radius, width, height, dk0, dv0, rect,
-                                             nullptr, idx_oa);
-    launch_radix_sort<unsigned long long>(dk0, dv0, dk1, dv1, nullptr, (unsigned)k, idx_oa, nullptr,
-                                          8, idx_state, idx_status, num_sms, st);
-    splat_depth_kernel<<<grid, 256, 0, st>>>(k, depth, k64, vc);
-}
-
-void launch_primary_keys(int n, const unsigned long long* k64, const unsigned long long* oa64,
-                         const unsigned int* order0, const unsigned int* order1,
-                         const SortState* order_state, unsigned int* pk, unsigned int* vals,
-                         unsigned long long* pk_oa, int num_sms, cudaStream_t st) {
-    const int grid = std::max(1, std::min((n + 255) / 256, num_sms * 8));
-    primary_keys_kernel<<<grid, 256, 0, st>>>(n, k64, oa64, order0, order1, order_state, pk, vals,
-                                              pk_oa);
+    const int grid = std::min((k + 255) / 256, num_sms * 8);
+    splat_keys_kernel<<<grid, 256, 0, st>>>(k, mean2d, radius, depth, width, height, rect, k64, vc);
 }
 
 }  // namespace fs

@@ -63,26 +63,18 @@ struct Work {
     unsigned int inst_cap = 0;
     int ntiles_cap = 0;
     size_t mask_cap = 0;
-    unsigned long long* dkeys[2] = {nullptr, nullptr};
-    unsigned int* dvals[2] = {nullptr, nullptr};
-    unsigned long long* rect = nullptr;
+    unsigned long long* rect = nullptr;      // per gid tile rectangle
     Rec32* r32 = nullptr;
     Rec64* r64 = nullptr;
-    SortState* sdepth = nullptr;             // depth sort state
-    SortState* sidx = nullptr;               // splat-list index sort state (fs_bin_splats)
-    unsigned long long* status_depth = nullptr;
-    unsigned long long* status_idx = nullptr;
-    size_t status_depth_words = 0, status_idx_words = 0;
-    unsigned long long* k64 = nullptr;       // full depth key per gid (projection output)
-    unsigned int* pk[2] = {nullptr, nullptr};  // 32-bit primary depth keys (sort ping-pong)
-    unsigned long long* pk_oa = nullptr;     // OR/AND of the primary keys
-    unsigned int* inst = nullptr;            // per-tile buckets: depth ranks, then gids
-    unsigned int* scratch = nullptr;         // merge scratch for long buckets
+    unsigned long long* k64 = nullptr;       // per gid order-preserving float64 depth key
+    unsigned short* pk = nullptr;            // per gid 16-bit primary depth key
+    unsigned int* tie = nullptr;             // per splat tie id (fs_bin_splats only)
+    unsigned int* inst = nullptr;            // per-tile buckets of gids
+    unsigned long long* scratch64 = nullptr; // 2 x capacity: long-bucket merge scratch
     unsigned int* count_bt = nullptr;        // ntiles x bin_blocks
     unsigned int* partial = nullptr;         // bin_scan_blocks
     unsigned int* tile_start = nullptr;
     ViewCounters* vc = nullptr;
-    unsigned long long* idx_oa = nullptr;  // OR/AND of the secondary (index) keys
     uint16_t* mask_dev = nullptr;
     uint16_t* pinned = nullptr;
     cudaEvent_t h2d_done = nullptr;
@@ -141,9 +133,8 @@ void free_work(fs::Work& w) {
     auto f = [](void* p) {
         if (p) cudaFree(p);
     };
-    f(w.dkeys[0]); f(w.dkeys[1]); f(w.dvals[0]); f(w.dvals[1]); f(w.rect); f(w.r32); f(w.r64);
-    f(w.k64); f(w.pk[0]); f(w.pk[1]); f(w.pk_oa); f(w.sdepth); f(w.sidx); f(w.status_depth); f(w.status_idx); f(w.inst); f(w.scratch); f(w.count_bt); f(w.partial);
-    f(w.tile_start); f(w.vc); f(w.idx_oa); f(w.mask_dev);
+    f(w.rect); f(w.r32); f(w.r64); f(w.k64); f(w.pk); f(w.tie); f(w.inst); f(w.scratch64);
+    f(w.count_bt); f(w.partial); f(w.tile_start); f(w.vc); f(w.mask_dev);
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
     if (w.done) cudaEventDestroy(w.done);
@@ -156,45 +147,21 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
                 size_t mask_px) {
     int rc;
     if (n > w.n_cap) {
-        for (int k = 0; k < 2; ++k) {
-            if ((rc = dev_alloc(&w.dkeys[k], n))) return rc;
-            if ((rc = dev_alloc(&w.dvals[k], n))) return rc;
-        }
         if ((rc = dev_alloc(&w.rect, n))) return rc;
-        if ((rc = dev_alloc(&w.k64, n))) return rc;
-        if ((rc = dev_alloc(&w.pk[0], n))) return rc;
-        if ((rc = dev_alloc(&w.pk[1], n))) return rc;
         if ((rc = dev_alloc(&w.r32, n))) return rc;
         if ((rc = dev_alloc(&w.r64, n))) return rc;
+        if ((rc = dev_alloc(&w.k64, n))) return rc;
+        if ((rc = dev_alloc(&w.pk, n))) return rc;
+        if ((rc = dev_alloc(&w.tie, n))) return rc;
         w.n_cap = n;
     }
     if (!w.vc) {
         if ((rc = dev_alloc(&w.vc, 1))) return rc;
-        if ((rc = dev_alloc(&w.idx_oa, 2))) return rc;
-        if ((rc = dev_alloc(&w.pk_oa, 2))) return rc;
-        if ((rc = dev_alloc(&w.sdepth, 1))) return rc;
-        if ((rc = dev_alloc(&w.sidx, 1))) return rc;
         if ((rc = dev_alloc(&w.partial, (size_t)fs::bin_scan_blocks(ctx->num_sms)))) return rc;
-        CK(cudaMemset(w.sdepth, 0, sizeof(fs::SortState)));
-        CK(cudaMemset(w.sidx, 0, sizeof(fs::SortState)));
-    }
-    {
-        // look-back status words must start zeroed (epoch 0 = never ready)
-        const size_t need = fs::sort_status_words((unsigned)std::min<long long>(std::max(n, w.n_cap), 0xffffffffLL));
-        if (need > w.status_depth_words) {
-            if ((rc = dev_alloc(&w.status_depth, need))) return rc;
-            CK(cudaMemset(w.status_depth, 0, need * 8));
-            w.status_depth_words = need;
-        }
-        if (need > w.status_idx_words) {
-            if ((rc = dev_alloc(&w.status_idx, need))) return rc;
-            CK(cudaMemset(w.status_idx, 0, need * 8));
-            w.status_idx_words = need;
-        }
     }
     if (inst > w.inst_cap) {
         if ((rc = dev_alloc(&w.inst, inst))) return rc;
-        if ((rc = dev_alloc(&w.scratch, inst))) return rc;
+        if ((rc = dev_alloc(&w.scratch64, 2 * (size_t)inst))) return rc;
         w.inst_cap = inst;
     }
     if (ntiles > w.ntiles_cap) {
@@ -236,12 +203,13 @@ int check_cam(const fs_camera& c, int idx) {
     return FS_OK;
 }
 
-fs::BinBuffers bin_buffers(fs::Work& w) {
+fs::BinBuffers bin_buffers(fs::Work& w, int n) {
     fs::BinBuffers b;
-    b.sorted_gid[0] = w.dvals[0];
-    b.sorted_gid[1] = w.dvals[1];
-    b.depth_state = w.sdepth;
+    b.n = n;
     b.rect = w.rect;
+    b.k64 = w.k64;
+    b.key_oa = &w.vc->key_or;  // key_or, key_and are adjacent
+    b.pk = w.pk;
     b.count_bt = w.count_bt;
     b.partial = w.partial;
     b.tile_start = w.tile_start;
@@ -250,46 +218,34 @@ fs::BinBuffers bin_buffers(fs::Work& w) {
     return b;
 }
 
-fs::TileSortArgs tile_sort_args(fs::Work& w, long long n) {
+fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr) {
     fs::TileSortArgs t;
     t.tile_start = w.tile_start;
     t.inst = w.inst;
-    t.scratch = w.scratch;
-    t.sorted_gid[0] = w.dvals[0];
-    t.sorted_gid[1] = w.dvals[1];
-    t.sorted_pkey[0] = w.pk[0];
-    t.sorted_pkey[1] = w.pk[1];
-    t.k64 = w.k64;
-    t.depth_state = w.sdepth;
-    t.rank_bits = fs::bits_for((unsigned)(n > 0 ? n - 1 : 0));
+    t.scratch64 = w.scratch64;
+    t.keys.pk = w.pk;
+    t.keys.k64 = w.k64;
+    t.keys.tie = tie;
     t.cap = fs::kTileSortCap;
     t.vc = w.vc;
     return t;
 }
 
-// Projection + depth sort + per-tile buckets of one view on workspace w
-// (the buckets are sorted by the raster prologue or launch_tile_sort).
+// Projection + per-tile buckets of one view on workspace w (the buckets are
+// depth-ordered by the raster prologue or launch_tile_sort).
 void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
-                 int cull_floor, fs::ProjectExport ex, cudaEvent_t after_sort = nullptr) {
+                 int cull_floor, fs::ProjectExport ex, cudaEvent_t after_project = nullptr) {
     const int n = (int)ctx->n;
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
-                       cull_floor, w.k64, w.dvals[0], w.rect, nullptr, w.r32, w.r64, w.vc, ex,
+                       cull_floor, w.k64, nullptr, w.rect, nullptr, w.r32, w.r64, w.vc, ex,
                        ctx->num_sms, w.stream);
-    // depth order: stable radix sort of the 32 highest varying key bits (gid
-    // order in, so exact ties stay in gid order); residual ties of the primary
-    // key are resolved against the full 64-bit key by the per-tile sort
-    fs::launch_primary_keys(n, w.k64, &w.vc->key_or, nullptr, nullptr, nullptr, w.pk[0], w.dvals[0],
-                            w.pk_oa, ctx->num_sms, w.stream);
-    fs::launch_radix_sort<unsigned int>(w.pk[0], w.dvals[0], w.pk[1], w.dvals[1], nullptr,
-                                        (unsigned)n, w.pk_oa, nullptr, 4, w.sdepth, w.status_depth,
-                                        ctx->num_sms, w.stream);
-    if (after_sort) cudaEventRecord(after_sort, w.stream);
-    fs::launch_bin(n, ntiles, tx, bin_buffers(w), w.vc, ctx->num_sms, w.stream);
+    if (after_project) cudaEventRecord(after_project, w.stream);
+    fs::launch_bin(ntiles, tx, bin_buffers(w, n), w.vc, ctx->num_sms, w.stream);
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + 1 + (3 + 4) + 5 + 1 + 1; }
+int view_launches() { return 1 + 1 + 5 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
@@ -308,7 +264,7 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.alpha_floor = alpha_floor;
     ra.t_floor = t_floor;
     ra.mask = mask;
-    ra.sort = tile_sort_args(w, ctx->n);
+    ra.sort = tile_sort_args(w);
     ra.r32 = w.r32;
     ra.r64 = w.r64;
     ra.acc = acc;
@@ -502,7 +458,7 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
         (rc = dev_alloc(&ex.radius, n1)))
         return rc;
     fs::launch_project((int)n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, to_cam(*cam), 0.0,
-                       0, w.dkeys[0], w.dvals[0], w.rect, nullptr, w.r32, w.r64, w.vc, ex,
+                       0, w.k64, nullptr, w.rect, nullptr, w.r32, w.r64, w.vc, ex,
                        ctx->num_sms, w.stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(w.stream));
@@ -558,7 +514,7 @@ int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t
     for (int attempt = 0; attempt < 2; ++attempt) {
         if ((rc = ensure_work(ctx, w, ctx->n, ntiles, cap, 1))) return rc;
         enqueue_bin(ctx, w, k, 0.0, 0, fs::ProjectExport{});
-        fs::launch_tile_sort(ntiles, tile_sort_args(w, ctx->n), w.stream);
+        fs::launch_tile_sort(ntiles, tile_sort_args(w), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
         CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
@@ -584,35 +540,34 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
     fs::Work& w = ctx->work[0];
     const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
     unsigned int cap = std::max(w.inst_cap, initial_inst_cap(k));
+    std::vector<unsigned int> tie((size_t)std::max<int64_t>(k, 0));
+    for (int64_t i = 0; i < k; ++i) {
+        if (index[i] < 0 || index[i] > 0xffffffffLL)
+            return fail(FS_EINVAL, "fs_bin_splats: gaussian_index %lld out of range", (long long)index[i]);
+        tie[i] = (unsigned int)index[i];
+    }
     double *d_mean = nullptr, *d_depth = nullptr;
-    long long *d_rad = nullptr, *d_idx = nullptr;
+    long long* d_rad = nullptr;
     const size_t k1 = (size_t)std::max<int64_t>(k, 1);
     if ((rc = dev_alloc(&d_mean, 2 * k1)) || (rc = dev_alloc(&d_depth, k1)) ||
-        (rc = dev_alloc(&d_rad, k1)) || (rc = dev_alloc(&d_idx, k1)))
+        (rc = dev_alloc(&d_rad, k1)))
         return rc;
     if (k > 0) {
         CK(cudaMemcpy(d_mean, mean2d, 16 * (size_t)k, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(d_depth, depth, 8 * (size_t)k, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(d_rad, radius, 8 * (size_t)k, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_idx, index, 8 * (size_t)k, cudaMemcpyHostToDevice));
     }
     fs::ViewCounters vc{};
     for (int attempt = 0; attempt < 2; ++attempt) {
         if ((rc = ensure_work(ctx, w, std::max<long long>(k, 1), ntiles, cap, 1))) return rc;
-        const unsigned long long init[2] = {0ull, ~0ull};
-        CK(cudaMemcpyAsync(w.idx_oa, init, sizeof(init), cudaMemcpyHostToDevice, w.stream));
         fs::launch_view_begin(w.vc, w.stream);
-        // LSD: stable sort by gaussian index, then stable sort by depth
-        fs::launch_bin_splats_keys((int)k, d_idx, d_mean, d_rad, d_depth, width, height, w.dkeys[0],
-                                   w.dvals[0], w.dkeys[1], w.dvals[1], w.rect, w.k64, w.idx_oa,
-                                   w.sidx, w.status_idx, w.vc, ctx->num_sms, w.stream);
-        fs::launch_primary_keys((int)k, w.k64, &w.vc->key_or, w.dvals[0], w.dvals[1], w.sidx,
-                                w.pk[0], w.dvals[0], w.pk_oa, ctx->num_sms, w.stream);
-        fs::launch_radix_sort<unsigned int>(w.pk[0], w.dvals[0], w.pk[1], w.dvals[1], nullptr,
-                                            (unsigned)k, w.pk_oa, nullptr, 4, w.sdepth,
-                                            w.status_depth, ctx->num_sms, w.stream);
-        fs::launch_bin((int)k, ntiles, tx, bin_buffers(w), w.vc, ctx->num_sms, w.stream);
-        fs::launch_tile_sort(ntiles, tile_sort_args(w, k), w.stream);
+        if (k > 0)
+            CK(cudaMemcpyAsync(w.tie, tie.data(), sizeof(unsigned int) * (size_t)k,
+                               cudaMemcpyHostToDevice, w.stream));
+        fs::launch_splat_keys((int)k, d_mean, d_rad, d_depth, width, height, w.rect, w.k64, w.vc,
+                              ctx->num_sms, w.stream);
+        fs::launch_bin(ntiles, tx, bin_buffers(w, (int)k), w.vc, ctx->num_sms, w.stream);
+        fs::launch_tile_sort(ntiles, tile_sort_args(w, w.tie), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
         CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
@@ -622,7 +577,6 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
     cudaFree(d_mean);
     cudaFree(d_depth);
     cudaFree(d_rad);
-    cudaFree(d_idx);
     if (vc.overflow) return fail(FS_ENOMEM, "fs_bin_splats: instance buffer overflow");
     return copy_tile_lists(w, ntiles, vc.n_valid, tile_offsets, items, items_capacity, n_items);
 }

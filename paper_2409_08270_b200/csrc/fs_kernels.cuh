@@ -6,19 +6,6 @@
 
 namespace fs {
 
-// ---- radix sort state (one per sort call site, device memory) ----
-struct SortState {
-    unsigned int offsets[8][256];  // per digit position: histogram, then exclusive offsets
-    unsigned int tile_counter[8];  // tile ids claimed by each pass
-    unsigned int active;           // bit p: pass p permutes (not the identity)
-    unsigned int epoch;            // look-back status generation
-};
-
-// Which ping-pong buffer holds the sorted result (0 or 1).
-__device__ __forceinline__ int sort_result_parity(const SortState* st) {
-    return __popc(st->active) & 1;
-}
-
 // Inclusive tile rectangle of a splat's radius box (rasterizer.py:106-113),
 // packed tx0 | tx1 << 16 | ty0 << 32 | ty1 << 48; ~0 when empty.
 __device__ __forceinline__ unsigned long long tile_rect(double mx, double my, double r, int tx_n,
@@ -54,83 +41,54 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
                     ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st);
 void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 
-// ---- fs_sort.cu ----
-size_t sort_status_words(unsigned int n_cap);
-// d_or_and: {OR, AND} of the valid keys (digits constant over all keys are
-// skipped); sub: if non-null, keys equal to all-ones are replaced by *sub.
-template <typename K>
-int launch_radix_sort(K* keys0, unsigned int* vals0, K* keys1, unsigned int* vals1,
-                      const unsigned int* d_n, unsigned int n_cap,
-                      const unsigned long long* d_or_and, const unsigned long long* sub, int passes,
-                      SortState* st, unsigned long long* status, int num_sms, cudaStream_t s);
-
 // ---- fs_bin.cu ----
+// Per-tile buckets of gids (any order) from per-block tile histograms, plus
+// the 16-bit primary depth key of every gid.
 struct BinBuffers {
-    const unsigned int* sorted_gid[2];  // depth sort values (ping-pong)
-    const SortState* depth_state;       // which of the two holds it
+    int n;                              // Gaussians (or splats)
     const unsigned long long* rect;     // per gid
+    const unsigned long long* k64;      // per gid: order-preserving float64 depth key
+    const unsigned long long* key_oa;   // {OR, AND} of the visible depth keys
+    unsigned short* pk;                 // out: per gid primary key
     unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets
     unsigned int* partial;              // bin_scan_blocks() partial sums
     unsigned int* tile_start;           // ntiles + 1
-    unsigned int* inst;                 // capacity: ranks, gids after the per-tile sort
+    unsigned int* inst;                 // capacity: gids, depth-ordered by the tile sort
     unsigned int capacity;
 };
 constexpr int kMaxTiles = 49152;        // per-block tile histograms live in shared memory
 int bin_blocks(int num_sms);
 int bin_scan_blocks(int num_sms);
 cudaError_t bin_configure();
-void launch_bin(int n, int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc,
-                int num_sms, cudaStream_t st);
+void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
+                cudaStream_t st);
 
+// Inputs of the per-tile depth ordering (fs_tilesort.cuh).
+struct TileSortKeys {
+    const unsigned short* pk;        // primary key per gid
+    const unsigned long long* k64;   // full depth key per gid
+    const unsigned int* tie;         // tie id per gid (nullptr: the gid itself)
+};
 struct TileSortArgs {
     const unsigned int* tile_start;
     unsigned int* inst;
-    unsigned int* scratch;
-    const unsigned int* sorted_gid[2];   // depth sort values (ping-pong)
-    const unsigned int* sorted_pkey[2];  // depth sort 32-bit primary keys (ping-pong)
-    const unsigned long long* k64;       // full 64-bit depth key per gid
-    const SortState* depth_state;
-    int rank_bits;
+    unsigned long long* scratch64;   // 2 x capacity entries (long buckets only)
+    TileSortKeys keys;
     unsigned int cap;
     const ViewCounters* vc;
 };
-
-// Resolved (device-side) view of the depth order used by the per-tile sort.
-struct TileSortKeys {
-    const unsigned int* sorted_gid;
-    const unsigned int* pkey;
-    const unsigned long long* k64;
-    int rank_bits;
-};
-__device__ __forceinline__ TileSortKeys resolve_keys(const TileSortArgs& t) {
-    const int p = sort_result_parity(t.depth_state);
-    return TileSortKeys{t.sorted_gid[p], t.sorted_pkey[p], t.k64, t.rank_bits};
-}
-
-// 32-bit primary depth keys: the 32 highest varying bits of the 64-bit keys
-// (from their OR/AND), written in the order given by `order` (order0, or the
-// result buffer of order_state's sort; both null: gid order); pk_oa receives
-// the OR/AND of the primary keys.
-void launch_primary_keys(int n, const unsigned long long* k64, const unsigned long long* oa64,
-                         const unsigned int* order0, const unsigned int* order1,
-                         const SortState* order_state, unsigned int* pk, unsigned int* vals,
-                         unsigned long long* pk_oa, int num_sms, cudaStream_t st);
 size_t tile_sort_smem_bytes(unsigned int cap);
 cudaError_t tile_sort_configure(unsigned int cap);
 void launch_tile_sort(int ntiles, const TileSortArgs& t, cudaStream_t st);
 
-// Binning of an explicit splat list: secondary sort by gaussian index, then
-// depth keys (written to dk0/dv0 for the depth sort that follows).
-void launch_bin_splats_keys(int k, const long long* index, const double* mean2d,
-                            const long long* radius, const double* depth, int width, int height,
-                            unsigned long long* dk0, unsigned int* dv0, unsigned long long* dk1,
-                            unsigned int* dv1, unsigned long long* rect, unsigned long long* k64,
-                            unsigned long long* idx_oa, SortState* idx_state,
-                            unsigned long long* idx_status, ViewCounters* vc, int num_sms,
-                            cudaStream_t st);
+// Explicit splat list (TileBinning over ProjectedGaussian): rect, depth key
+// and key OR/AND per list position.
+void launch_splat_keys(int k, const double* mean2d, const long long* radius, const double* depth,
+                       int width, int height, unsigned long long* rect, unsigned long long* k64,
+                       ViewCounters* vc, int num_sms, cudaStream_t st);
 
 // ---- fs_raster.cu ----
-constexpr unsigned int kTileSortCap = 4096;  // bucket entries sorted in shared memory
+constexpr unsigned int kTileSortCap = 2048;  // bucket entries sorted in shared memory
 struct RasterArgs {
     int width, height, tiles_x, ntiles;
     int num_objects;

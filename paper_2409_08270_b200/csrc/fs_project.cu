@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) project_kernel(
                 count_rect_tiles(rc, tx_n, tile_count);
             }
             keys[i] = key;
-            vals[i] = (unsigned int)i;
+            if (vals) vals[i] = (unsigned int)i;
             rect[i] = rc;
             // walk records (float64 exact, float32 screen)
             Rec64 q;

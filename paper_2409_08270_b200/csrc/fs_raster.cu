@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     // prologue: the tile's bucket of depth ranks -> gids in (depth, gid) order
     // (reuses the walk's shared memory, fs_tilesort.cuh)
     unsigned int* list = a.sort.inst + begin;
-    sort_tile_list(list, a.sort.scratch + begin, end - begin, resolve_keys(a.sort),
-                   reinterpret_cast<unsigned int*>(smem_raw), a.sort.cap);
+    sort_tile_list(list, a.sort.scratch64 + 2ull * begin, end - begin, a.sort.keys, smem_raw,
+                   a.sort.cap);
     const unsigned int* __restrict__ gids = list - begin;  // indexed by instance position
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

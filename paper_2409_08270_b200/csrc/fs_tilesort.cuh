@@ -1,6 +1,19 @@
-// fs_tilesort.cuh -- per-tile sort of a bucket of depth ranks (shared by the
+// fs_tilesort.cuh -- per-tile depth ordering of a tile's bucket (shared by the
 // raster kernel prologue, fs_raster.cu, and the standalone tile_sort_kernel
-// of the binning API, fs_bin.cu).  See fs_bin.cu for the pipeline.
+// of the binning API, fs_bin.cu).
+//
+// A bucket holds the gids whose tile rectangle covers the tile, in arbitrary
+// order.  The reference order is np.lexsort((index, depth)) with float64 depth
+// (rasterizer.py:91).  Per tile:
+//   1. stable LSD radix sort (shared memory, 2 x 8-bit digits) of
+//      (primary << 32 | gid) by the 16-bit primary key = the 16 highest bits
+//      in which the view's float64 depth keys differ (order-preserving);
+//   2. runs of equal primary key are re-ordered by (full 64-bit depth key,
+//      tie id) -- tie id = gid for scenes, the splat's gaussian_index for
+//      explicit splat lists.  A parallel inversion check skips sorted runs;
+//      only runs that need it get a (short) insertion sort.
+// Buckets longer than `cap` are sorted in chunks and merged through global
+// memory before step 2.  The result is exactly the reference's tile list.
 #pragma once
 
 #include "fs_common.cuh"
@@ -12,12 +25,9 @@ namespace tilesort {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-// ---------------------------------------------------------------------------
-// Per-tile sort of a bucket of depth ranks (device function shared by the
-// raster kernel's prologue and tile_sort_kernel).  256 threads.  `smem` holds
-// at least 2*cap + kWarps*256 + 64 words.  On return list[0..n) holds gids in
-// (depth, gid) order.
-// ---------------------------------------------------------------------------
+static __device__ __forceinline__ unsigned int pk_of(unsigned long long e) {
+    return (unsigned int)(e >> 32);
+}
 
 // exclusive scan over 256 values held one per thread (blockDim == 256)
 static __device__ __forceinline__ unsigned int block_excl_scan256(unsigned int v, unsigned int* s_w) {
@@ -37,17 +47,19 @@ static __device__ __forceinline__ unsigned int block_excl_scan256(unsigned int v
     return base + x - v;
 }
 
-// stable LSD radix sort of n <= cap keys in shared memory; returns the buffer
-// holding the result (a or b)
-static __device__ unsigned int* smem_radix_sort(unsigned int* a, unsigned int* b, unsigned int n,
-                                         int bits, unsigned int* whist, unsigned int* s_misc) {
+// Stable LSD radix sort of n packed entries by their 16-bit primary key
+// (bits 32..47); returns the buffer holding the result (a or b).
+static __device__ unsigned long long* smem_sort_pk(unsigned long long* a, unsigned long long* b,
+                                                   unsigned int n, unsigned int* whist,
+                                                   unsigned int* s_misc) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned int lt_mask = (1u << lane) - 1u;
-    // digits that vary over this tile
-    unsigned int o = 0, z = 0xFFFFFFFFu;
+    // digits that vary over this bucket
+    unsigned int o = 0, z = 0xFFFFu;
     for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
-        o |= a[i];
-        z &= a[i];
+        const unsigned int k = pk_of(a[i]);
+        o |= k;
+        z &= k;
     }
     o = __reduce_or_sync(0xffffffffu, o);
     z = __reduce_and_sync(0xffffffffu, z);
@@ -56,7 +68,7 @@ static __device__ unsigned int* smem_radix_sort(unsigned int* a, unsigned int* b
         s_misc[kWarps + warp] = z;
     }
     __syncthreads();
-    unsigned int vary = 0, allz = 0xFFFFFFFFu;
+    unsigned int vary = 0, allz = 0xFFFFu;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
         vary |= s_misc[w];
@@ -67,21 +79,21 @@ static __device__ unsigned int* smem_radix_sort(unsigned int* a, unsigned int* b
     // each warp owns a contiguous slice (keeps the scatter stable)
     const unsigned int per = ((n + kWarps - 1) / kWarps + 31u) & ~31u;
     const unsigned int lo = min(n, per * warp), hi = min(n, lo + per);
-    for (int shift = 0; shift < bits; shift += 8) {
+    for (int shift = 0; shift < 16; shift += 8) {
         if (!((vary >> shift) & 0xFFu)) continue;
         for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) whist[i] = 0;
         __syncthreads();
         for (unsigned int base = lo; base < hi; base += 32) {
             const unsigned int idx = base + lane;
             const bool valid = idx < hi;
-            const unsigned int d = valid ? (a[idx] >> shift) & 0xFFu : 0u;
+            const unsigned int d = valid ? (pk_of(a[idx]) >> shift) & 0xFFu : 0u;
             const unsigned int peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
             if (valid && lane == 31 - __clz(peers)) whist[warp * 256 + d] += __popc(peers);
             __syncwarp();
         }
         __syncthreads();
-        // digit-major, warp-minor exclusive offsets
         {
+            // digit-major, warp-minor exclusive offsets
             const int d = threadIdx.x;
             unsigned int run = 0;
 #pragma unroll
@@ -98,123 +110,140 @@ static __device__ unsigned int* smem_radix_sort(unsigned int* a, unsigned int* b
         for (unsigned int base = lo; base < hi; base += 32) {
             const unsigned int idx = base + lane;
             const bool valid = idx < hi;
-            const unsigned int key = valid ? a[idx] : 0u;
-            const unsigned int d = (key >> shift) & 0xFFu;
+            const unsigned long long e = valid ? a[idx] : 0ull;
+            const unsigned int d = (pk_of(e) >> shift) & 0xFFu;
             const unsigned int peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
             const unsigned int off = valid ? whist[warp * 256 + d] : 0u;
             __syncwarp();
             if (valid) {
-                b[off + __popc(peers & lt_mask)] = key;
+                b[off + __popc(peers & lt_mask)] = e;
                 if (lane == 31 - __clz(peers)) whist[warp * 256 + d] = off + __popc(peers);
             }
             __syncwarp();
         }
         __syncthreads();
-        unsigned int* t = a;
+        unsigned long long* t = a;
         a = b;
         b = t;
     }
     return a;
 }
 
-// merge sorted src[lo, mid) and src[mid, hi) into dst[lo, hi) with the whole block
-static __device__ void block_merge(const unsigned int* src, unsigned int* dst, unsigned int lo,
-                            unsigned int mid, unsigned int hi) {
+// merge sorted src[lo, mid) and src[mid, hi) into dst[lo, hi) by primary key
+static __device__ void block_merge(const unsigned long long* src, unsigned long long* dst,
+                                   unsigned int lo, unsigned int mid, unsigned int hi) {
     const unsigned int na = mid - lo, nb = hi - mid, total = na + nb;
     const unsigned int per = (total + kThreads - 1) / kThreads;
     const unsigned int d0 = min(total, per * threadIdx.x), d1 = min(total, d0 + per);
     if (d0 >= d1) return;
-    const unsigned int* A = src + lo;
-    const unsigned int* B = src + mid;
-    // merge path: i elements of A and d0 - i of B precede output position d0
+    const unsigned long long* A = src + lo;
+    const unsigned long long* B = src + mid;
     unsigned int l = d0 > nb ? d0 - nb : 0u, r = min(d0, na);
-    while (l < r) {
+    while (l < r) {  // merge path
         const unsigned int m = (l + r) >> 1;
-        if (A[m] <= B[d0 - m - 1]) l = m + 1;
+        if (pk_of(A[m]) <= pk_of(B[d0 - m - 1])) l = m + 1;
         else r = m;
     }
     unsigned int i = l, j = d0 - l;
     for (unsigned int k = d0; k < d1; ++k) {
-        const bool take_a = j >= nb || (i < na && A[i] <= B[j]);
+        const bool take_a = j >= nb || (i < na && pk_of(A[i]) <= pk_of(B[j]));
         dst[lo + k] = take_a ? A[i++] : B[j++];
     }
 }
 
-// Entries whose 32-bit primary depth keys tie are re-ordered by the full
-// 64-bit key (stable, so gid order survives among exact ties).  `rk` holds
-// depth ranks (sorted), `pk` their primary keys; runs of equal pk are
-// contiguous because ranks are ordered by pk.  Runs are tiny in practice.
-static __device__ void fix_primary_ties(unsigned int* rk, const unsigned int* pk, unsigned int n,
-                                        const unsigned int* __restrict__ sorted_gid,
-                                        const unsigned long long* __restrict__ k64) {
+// full order of an entry: (64-bit depth key, tie id)
+static __device__ __forceinline__ bool entry_less(unsigned long long x, unsigned long long y,
+                                                  const TileSortKeys K) {
+    const unsigned int gx = (unsigned int)x, gy = (unsigned int)y;
+    const unsigned long long kx = K.k64[gx], ky = K.k64[gy];
+    if (kx != ky) return kx < ky;
+    const unsigned int tx = K.tie ? K.tie[gx] : gx, ty = K.tie ? K.tie[gy] : gy;
+    return tx < ty;
+}
+
+// Re-order runs of equal primary key by (k64, tie).  `e` is sorted by
+// primary key; `flag` (n bytes) is scratch.
+static __device__ void fix_primary_ties(unsigned long long* e, unsigned int n,
+                                        const TileSortKeys K, unsigned char* flag) {
+    // inversion check of each adjacent equal-key pair, in parallel
+    for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads)
+        flag[i] = (pk_of(e[i]) == pk_of(e[i + 1]) && entry_less(e[i + 1], e[i], K)) ? 1 : 0;
+    __syncthreads();
     for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads) {
-        if (pk[i + 1] != pk[i] || (i > 0 && pk[i - 1] == pk[i])) continue;  // not a run start
+        if (pk_of(e[i + 1]) != pk_of(e[i]) || (i > 0 && pk_of(e[i - 1]) == pk_of(e[i]))) continue;
         unsigned int j = i + 1;
-        while (j + 1 < n && pk[j + 1] == pk[i]) ++j;
-        // insertion sort rk[i..j] by k64[gid] (stable)
-        for (unsigned int x = i + 1; x <= j; ++x) {
-            const unsigned int r = rk[x];
-            const unsigned long long key = k64[sorted_gid[r]];
+        bool inverted = flag[i] != 0;
+        while (j + 1 < n && pk_of(e[j + 1]) == pk_of(e[i])) {
+            inverted |= flag[j] != 0;
+            ++j;
+        }
+        if (!inverted) continue;
+        for (unsigned int x = i + 1; x <= j; ++x) {  // insertion sort of the run (stable)
+            const unsigned long long v = e[x];
             unsigned int y = x;
-            while (y > i && k64[sorted_gid[rk[y - 1]]] > key) {
-                rk[y] = rk[y - 1];
+            while (y > i && entry_less(v, e[y - 1], K)) {
+                e[y] = e[y - 1];
                 --y;
             }
-            rk[y] = r;
+            e[y] = v;
         }
     }
 }
 
-static __device__ __noinline__ void sort_tile_list(unsigned int* list, unsigned int* scratch,
-                                                   unsigned int n, const TileSortKeys& K,
-                                                   unsigned int* smem, unsigned int cap) {
-    unsigned int* a = smem;
-    unsigned int* b = smem + cap;
-    unsigned int* whist = smem + 2 * cap;
+// Sorts list[0, n) (gids) into the reference order.  smem: at least
+// tile_sort_smem_bytes(cap) bytes; scratch64: 2n entries of global scratch.
+static __device__ __noinline__ void sort_tile_list(unsigned int* list,
+                                                   unsigned long long* scratch64, unsigned int n,
+                                                   const TileSortKeys K, unsigned char* smem,
+                                                   unsigned int cap) {
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(smem);
+    unsigned long long* b = a + cap;
+    unsigned int* whist = reinterpret_cast<unsigned int*>(b + cap);
     unsigned int* misc = whist + kWarps * 256;
+    unsigned char* flag = reinterpret_cast<unsigned char*>(misc + 64);
     if (n <= cap) {
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) a[i] = list[i];
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
+            const unsigned int g = list[i];
+            a[i] = ((unsigned long long)K.pk[g] << 32) | g;
+        }
         __syncthreads();
-        unsigned int* res = smem_radix_sort(a, b, n, K.rank_bits, whist, misc);
-        unsigned int* pk = res == a ? b : a;
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) pk[i] = K.pkey[res[i]];
+        unsigned long long* res = smem_sort_pk(a, b, n, whist, misc);
+        fix_primary_ties(res, n, K, flag);
         __syncthreads();
-        fix_primary_ties(res, pk, n, K.sorted_gid, K.k64);
-        __syncthreads();
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = K.sorted_gid[res[i]];
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = (unsigned int)res[i];
         __syncthreads();
         return;
     }
-    // long bucket: sort chunks of cap in shared memory, then merge through global memory
+    // long bucket: sort chunks in shared memory, merge through global memory
+    unsigned long long* g0 = scratch64;
+    unsigned long long* g1 = scratch64 + n;
     for (unsigned int c0 = 0; c0 < n; c0 += cap) {
         const unsigned int m = min(cap, n - c0);
-        for (unsigned int i = threadIdx.x; i < m; i += kThreads) a[i] = list[c0 + i];
+        for (unsigned int i = threadIdx.x; i < m; i += kThreads) {
+            const unsigned int g = list[c0 + i];
+            a[i] = ((unsigned long long)K.pk[g] << 32) | g;
+        }
         __syncthreads();
-        const unsigned int* res = smem_radix_sort(a, b, m, K.rank_bits, whist, misc);
-        for (unsigned int i = threadIdx.x; i < m; i += kThreads) list[c0 + i] = res[i];
+        const unsigned long long* res = smem_sort_pk(a, b, m, whist, misc);
+        for (unsigned int i = threadIdx.x; i < m; i += kThreads) g0[c0 + i] = res[i];
         __syncthreads();
     }
-    unsigned int* src = list;
-    unsigned int* dst = scratch;
+    unsigned long long* src = g0;
+    unsigned long long* dst = g1;
     for (unsigned int width = cap; width < n; width *= 2) {
         for (unsigned int lo = 0; lo < n; lo += 2 * width) {
             const unsigned int mid = min(n, lo + width), hi = min(n, lo + 2 * width);
             block_merge(src, dst, lo, mid, hi);
         }
-        __threadfence_block();
         __syncthreads();
-        unsigned int* t = src;
+        unsigned long long* t = src;
         src = dst;
         dst = t;
     }
-    // primary keys of the merged list go to the other global buffer
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) dst[i] = K.pkey[src[i]];
-    __threadfence_block();
+    // tie fix-up flags for the long list live in the other global buffer
+    fix_primary_ties(src, n, K, reinterpret_cast<unsigned char*>(dst));
     __syncthreads();
-    fix_primary_ties(src, dst, n, K.sorted_gid, K.k64);
-    __threadfence_block();
-    __syncthreads();
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = K.sorted_gid[src[i]];
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = (unsigned int)src[i];
     __syncthreads();
 }
 
