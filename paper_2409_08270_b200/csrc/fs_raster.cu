@@ -52,6 +52,38 @@ struct RasterSmem {
     unsigned long long cnt_e[kWarps], cnt_a[kWarps];
 };
 
+// tile-sort scratch (fs_tilesort.cuh) and the walk share the same bytes
+constexpr size_t kSortBytes = 16 * (size_t)kTileSortCap + 4 * (kWarps * 256 + 64) + kTileSortCap;
+union RasterShared {
+    RasterSmem walk;
+    unsigned char sort[kSortBytes];
+};
+static_assert(sizeof(RasterShared) <= 48 * 1024, "raster shared memory must stay static (<= 48 KB)");
+
+// Candidate columns of one pixel row for one splat: the pixels whose float32
+// power clears the conservative cut, from the roots of the quadratic
+//   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
+// (widened by float32 rounding margins).  Returns a 16-bit column mask.
+__device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0) {
+    if (!(s.cut > -INFINITY)) return 0xFFFFu;  // exact blend: no alpha floor
+    const float dv = v_centre - s.my;
+    const float Q = -2.0f * s.cut;
+    const float detc = s.a * s.c - s.b * s.b;
+    const float t1 = s.a * Q, t2 = detc * dv * dv;
+    const float D = t1 - t2 + 1e-5f * (fabsf(t1) + fabsf(t2)) + 1e-20f;
+    if (!(D >= 0.0f)) return 0u;
+    const float inv_a = 1.0f / s.a;
+    const float ctr = s.mx - 0.5f - s.b * dv * inv_a;
+    const float half = sqrtf(D) * inv_a;
+    const float eps = 0.03f + 1e-5f * fabsf(ctr);
+    const float lo = ceilf(ctr - half - eps) - (float)x0;
+    const float hi = floorf(ctr + half + eps) - (float)x0;
+    if (hi < 0.0f || lo > 15.0f || lo > hi) return 0u;
+    const int c0 = lo < 0.0f ? 0 : (int)lo;
+    const int c1 = hi > 15.0f ? 15 : (int)hi;
+    return (2u << c1) - (1u << c0);
+}
+
 __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const ViewCounters* vc = a.vc;
     if (vc->overflow) return;
@@ -59,12 +91,11 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const unsigned int begin = a.sort.tile_start[tile], end = a.sort.tile_start[tile + 1];
     if (begin >= end) return;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    RasterSmem& S = *reinterpret_cast<RasterSmem*>(smem_raw);
-    // prologue: the tile's bucket of depth ranks -> gids in (depth, gid) order
-    // (reuses the walk's shared memory, fs_tilesort.cuh)
+    __shared__ __align__(16) RasterShared SH;
+    RasterSmem& S = SH.walk;
+    // prologue: the tile's bucket -> gids in the reference (depth, id) order
     unsigned int* list = a.sort.inst + begin;
-    sort_tile_list(list, a.sort.scratch64 + 2ull * begin, end - begin, a.sort.keys, smem_raw,
+    sort_tile_list(list, a.sort.scratch64 + 2ull * begin, end - begin, a.sort.keys, SH.sort,
                    a.sort.cap);
     const unsigned int* __restrict__ gids = list - begin;  // indexed by instance position
 
@@ -74,15 +105,20 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
     const bool inside = px < a.width && py < a.height;
     const unsigned int label = inside ? a.mask[(size_t)py * a.width + px] : 0u;
-    const float pxf = (float)px + 0.5f, pyf = (float)py + 0.5f;
     const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
+    // screen lanes: k = lane & 7 (splat of the mini-batch), row = (lane >> 3) & 1
+    const int scr_k = lane & 7;
+    const float scr_v = (float)(y0 + 2 * warp + ((lane >> 3) & 1)) + 0.5f;
 
     const unsigned int inside_mask = __ballot_sync(0xffffffffu, inside);
     const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
     const unsigned int lbl0 = __shfl_sync(0xffffffffu, label, first);
     const bool uniform = __all_sync(0xffffffffu, !inside || label == lbl0);
 
-    const double af = a.alpha_floor, tf = a.t_floor;
+    // alpha >= af_eff and T < tf_eff reproduce the reference's floors (and
+    // their absence when a floor is 0: alpha >= 0 > -1, T >= 0 > -1)
+    const double af_eff = a.alpha_floor > 0.0 ? a.alpha_floor : -1.0;
+    const double tf_eff = a.t_floor > 0.0 ? a.t_floor : -1.0;
     const long long n_g = a.n_gaussians;
     double* __restrict__ acc = a.acc;
     double* __restrict__ myval = S.val[warp];
@@ -130,20 +166,19 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         __syncwarp();
         for (int m0 = 0; m0 < cnt; m0 += kMini) {
             const int nm = min(kMini, cnt - m0);
-            // ---- A: float32 screen ----
+            // ---- A: float32 screen, transposed: lane (k, row) solves for the
+            //      candidate columns of splat k on its pixel row ----
+            unsigned int rowmask = 0;
+            if (scr_k < nm) rowmask = row_candidates(S.r32[S.list[warp][m0 + scr_k]], scr_v, x0);
+            const unsigned int act = __ballot_sync(0xffffffffu, active);
             unsigned int cm[kMini];
             int base[kMini];
             int total = 0;
 #pragma unroll
             for (int k = 0; k < kMini; ++k) {
-                bool cand = false;
-                if (k < nm) {
-                    const Rec32 s = S.r32[S.list[warp][m0 + k]];
-                    const float du = pxf - s.mx, dv = pyf - s.my;
-                    const float p = -0.5f * (s.a * du * du + s.c * dv * dv) - s.b * du * dv;
-                    cand = active && p >= s.cut;
-                }
-                cm[k] = __ballot_sync(0xffffffffu, cand);
+                const unsigned int r0 = __shfl_sync(0xffffffffu, rowmask, k);
+                const unsigned int r1 = __shfl_sync(0xffffffffu, rowmask, k + 8);
+                cm[k] = (r0 | (r1 << 16)) & act;
                 base[k] = total;
                 total += __popc(cm[k]);
             }
@@ -177,25 +212,33 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             unsigned int cb[kMini];
 #pragma unroll
             for (int k = 0; k < kMini; ++k) {
-                double w = 0.0;
+                cb[k] = 0;
+                if (!cm[k]) continue;  // warp-uniform
+                bool contributes = false;
                 if (((cm[k] >> lane) & 1u) && active) {
                     const double alpha = myval[k * kRowStride + lane];
-                    if (af > 0.0 ? (alpha >= af) : true) {  // :148-149
-                        w = __dmul_rn(alpha, T);                     // :150
-                        T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
-                        if (tf > 0.0 && !(T >= tf)) active = false;  // :156-157
+                    if (alpha >= af_eff) {  // :148-149
+                        const double w = __dmul_rn(alpha, T);       // :150
+                        T = __dmul_rn(T, __dsub_rn(1.0, alpha));    // :155
+                        active = !(T < tf_eff);                     // :156-157
+                        myval[k * kRowStride + lane] = w;
+                        contributes = w > 0.0;
                     }
                 }
-                myval[k * kRowStride + lane] = w;
-                cb[k] = __ballot_sync(0xffffffffu, w > 0.0);
+                cb[k] = __ballot_sync(0xffffffffu, contributes);
             }
             __syncwarp();
             // ---- C: aggregation + float64 atomics ----
             if (uniform) {
                 const int k = lane & 7, seg = lane >> 3;
+                unsigned int bits = 0;
+#pragma unroll
+                for (int t = 0; t < kMini; ++t) bits = t == k ? cb[t] : bits;
+                bits = (bits >> (seg * 8)) & 0xFFu;
                 double v = 0.0;
 #pragma unroll
-                for (int t = 0; t < 8; ++t) v += myval[k * kRowStride + seg * 8 + t];
+                for (int t = 0; t < 8; ++t)
+                    if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * 8 + t];
                 v += __shfl_xor_sync(0xffffffffu, v, 8);
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
                 if (lane < kMini && k < nm && v > 0.0) {
@@ -213,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 }
             }
             __syncwarp();
-            if (tf > 0.0) {
+            if (a.t_floor > 0.0) {
                 warp_live = __any_sync(0xffffffffu, active);
                 if (!warp_live) break;
             }
@@ -241,20 +284,13 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
 }  // namespace
 
 // Per device (called by fs_create after cudaSetDevice): opt in to >48 KB smem.
-static size_t raster_smem_bytes() {
-    return std::max(sizeof(RasterSmem), tile_sort_smem_bytes(kTileSortCap));
-}
-
 cudaError_t raster_configure() {
-    cudaError_t e = cudaFuncSetAttribute(raster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)raster_smem_bytes());
-    if (e != cudaSuccess) return e;
     return tile_sort_configure(kTileSortCap);
 }
 
 void launch_raster(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
-    raster_kernel<<<a.ntiles, kThreads, raster_smem_bytes(), st>>>(a);
+    raster_kernel<<<a.ntiles, kThreads, 0, st>>>(a);
 }
 
 }  // namespace fs
