@@ -29,6 +29,7 @@ extern "C" {
 #define FS_EINVAL 1   /* invalid argument (ValueError on the Python side) */
 #define FS_ECUDA 2    /* CUDA runtime failure (RuntimeError) */
 #define FS_ENOMEM 3   /* device or pinned allocation failed */
+#define FS_ELABEL 4   /* a mask label >= num_objects (see stats->label_error_view) */
 
 #define FS_MODE_BINARY 0
 #define FS_MODE_SCENE 1
@@ -59,6 +60,7 @@ typedef struct {
     int64_t atomics;          /* float64 accumulator atomics */
     int64_t retried_views;    /* views re-run after growing the instance buffers */
     int64_t launches;         /* kernels this call launched */
+    int64_t label_error_view; /* first view with a label >= num_objects, or -1 */
     double gpu_ms;            /* CUDA-event time of the view loop on the device */
     /* per-stage CUDA-event times summed over views; only with fs_set_timing(ctx, 1) */
     double prep_ms;           /* projection + depth radix sort */

@@ -17,7 +17,7 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libflashsplat_b200.so"
 
-FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM = 0, 1, 2, 3
+FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ELABEL = 0, 1, 2, 3, 4
 MODE_BINARY, MODE_SCENE = 0, 1
 
 # Every symbol include/flashsplat_b200.h declares (checked by tests/test_capi.py).
@@ -31,6 +31,14 @@ EXPORTS = (
 
 class NativeUnavailable(RuntimeError):
     """The CUDA library is not built or no sm_100 device is usable."""
+
+
+class LabelRangeError(ValueError):
+    """A mask label >= num_objects; `view` is the first offending view's position."""
+
+    def __init__(self, msg: str, view: int):
+        super().__init__(msg)
+        self.view = view
 
 
 class FsCamera(ctypes.Structure):
@@ -50,7 +58,7 @@ class FsProjectionStats(ctypes.Structure):
 class FsAccumulateStats(ctypes.Structure):
     _fields_ = [(k, ctypes.c_int64) for k in
                 ("views", "view_pixels", "emitted", "instances", "tile_steps", "exact_evals",
-                 "atomics", "retried_views", "launches")] + [
+                 "atomics", "retried_views", "launches", "label_error_view")] + [
                     (k, ctypes.c_double) for k in ("gpu_ms", "prep_ms", "bin_ms", "raster_ms")]
 
     def as_dict(self) -> dict:
@@ -183,11 +191,15 @@ class Context:
         self._scene_key = None
         self.n = 0
         self.lock = threading.RLock()
+        self._buffers: dict = {}
 
     def set_timing(self, enable: bool) -> None:
         _check(load().fs_set_timing(self.handle, 1 if enable else 0))
 
     def close(self) -> None:
+        for buf in getattr(self, "_buffers", {}).values():
+            buf.release()
+        self._buffers = {}
         if self.handle:
             load().fs_destroy(self.handle)
             self.handle = None
@@ -261,11 +273,25 @@ class Context:
             keep = [np.ascontiguousarray(m, dtype=np.uint16) for m in masks]
             ptrs = (ctypes.c_void_p * max(nv, 1))(*[k.ctypes.data for k in keep])
         st = FsAccumulateStats()
-        _check(load().fs_accumulate(self.handle, nv, ctypes.byref(cams), ctypes.byref(ptrs),
-                                    1 if masks_on_device else 0, int(num_objects),
-                                    float(alpha_floor), float(t_floor), acc_ptr,
-                                    ctypes.byref(st)))
+        L = load()
+        rc = L.fs_accumulate(self.handle, nv, ctypes.byref(cams), ctypes.byref(ptrs),
+                             1 if masks_on_device else 0, int(num_objects), float(alpha_floor),
+                             float(t_floor), acc_ptr, ctypes.byref(st))
+        if rc == FS_ELABEL:
+            raise LabelRangeError(L.fs_last_error().decode(errors="replace"),
+                                  int(st.label_error_view))
+        _check(rc)
         return st.as_dict()
+
+    def buffer(self, role: str, nbytes: int) -> "DeviceBuffer":
+        """Grow-only device scratch owned by the context, keyed by role."""
+        buf = self._buffers.get(role)
+        if buf is None or buf.nbytes < nbytes:
+            if buf is not None:
+                buf.release()
+            buf = DeviceBuffer(self, max(int(nbytes), 1))
+            self._buffers[role] = buf
+        return buf
 
     def finalize(self, acc_ptr: int, count: int, out_ptr: int = None, out: np.ndarray = None):
         if out is not None:
@@ -280,18 +306,25 @@ class Context:
 
 def assign(values: np.ndarray, gamma: float, mode: int, ctx: Context = None,
            on_device_ptr: int = None, n: int = None, e: int = None, out_ptr: int = None):
-    """fs_assign on host arrays (returns uint8) or on device pointers (in place)."""
+    """fs_assign on host arrays (returns uint8) or on device pointers (in place).
+
+    Host arrays go through the (default) context's cached device buffers,
+    under the context lock.
+    """
     L = load()
-    h = ctx.handle if ctx is not None else None
-    if on_device_ptr is not None:
-        _check(L.fs_assign(h, on_device_ptr, int(n), int(e), float(gamma), int(mode),
-                           out_ptr, 1))
-        return None
-    values = np.ascontiguousarray(values, dtype=np.float32)
-    e, n = values.shape
-    out = np.zeros(n if mode == MODE_BINARY else (e, n), np.uint8)
-    _check(L.fs_assign(h, _p(values), int(n), int(e), float(gamma), int(mode), _p(out), 0))
-    return out
+    if ctx is None:
+        ctx = context()
+    with ctx.lock:
+        if on_device_ptr is not None:
+            _check(L.fs_assign(ctx.handle, on_device_ptr, int(n), int(e), float(gamma), int(mode),
+                               out_ptr, 1))
+            return None
+        values = np.ascontiguousarray(values, dtype=np.float32)
+        e, n = values.shape
+        out = np.zeros(n if mode == MODE_BINARY else (e, n), np.uint8)
+        _check(L.fs_assign(ctx.handle, _p(values), int(n), int(e), float(gamma), int(mode),
+                           _p(out), 0))
+        return out
 
 
 _contexts: dict = {}

@@ -90,7 +90,7 @@ class ContributionMatrix:
 
 
 def validate_views(views: Sequence, num_objects: int) -> None:
-    """Reference checks in view order (``contributions.py:104-114``)."""
+    """Reference checks in view order (``contributions.py:104-114``), on the host."""
     for view, mask in views:
         labels = mask.labels
         if labels.shape != (view.height, view.width):
@@ -103,6 +103,30 @@ def validate_views(views: Sequence, num_objects: int) -> None:
             raise ValueError(
                 f"view {view.view_id}: label {top} at pixel ({j}, {k}) "
                 f"exceeds object count {num_objects}")
+
+
+def check_shapes(views: Sequence, num_objects: int) -> None:
+    """Shape checks on the host; label ranges are checked on the device.
+
+    If a view has the wrong shape, the reference would still have raised for
+    an out-of-range label in an earlier view first, so those views get the
+    full host check (``contributions.py:103-114`` order).
+    """
+    for i, (view, mask) in enumerate(views):
+        if mask.labels.shape != (view.height, view.width):
+            validate_views(views[: i + 1], num_objects)
+
+
+def run_device_accumulate(ctx, views: Sequence, num_objects: int, blend, acc_ptr) -> dict:
+    """ctx.accumulate with the reference's label error reproduced on failure."""
+    from . import _native
+
+    try:
+        return ctx.accumulate([v for v, _ in views], [m.labels for _, m in views], num_objects,
+                              blend.alpha_floor, blend.transmittance_floor, acc_ptr)
+    except _native.LabelRangeError as err:
+        validate_views([views[err.view]], num_objects)  # raises the reference message
+        raise
 
 
 def accumulate_contributions(
@@ -124,8 +148,13 @@ def accumulate_contributions(
     """
     views = list(views)
     num_objects = int(num_objects)
-    validate_views(views, num_objects)
+    check_shapes(views, num_objects)
+    if len(scene) == 0:
+        validate_views(views, num_objects)
+        return ContributionMatrix(values=np.zeros((num_objects, 0), dtype=np.float32))
     if process_group is not None:
+        # every rank checks every view so all ranks raise the same error
+        validate_views(views, num_objects)
         from .distributed import accumulate_sharded
         values = accumulate_sharded(scene, views, num_objects, blend, process_group,
                                     device=device, stats=stats)
@@ -136,13 +165,10 @@ def accumulate_contributions(
     n = len(scene)
     with ctx.lock:
         ctx.set_scene(scene)
-        acc = ctx.alloc(8 * num_objects * max(n, 1)).zero()
-        st = ctx.accumulate([v for v, _ in views], [m.labels for _, m in views], num_objects,
-                            blend.alpha_floor, blend.transmittance_floor, acc.ptr)
+        acc = ctx.buffer("acc64", 8 * num_objects * n).zero()
+        st = run_device_accumulate(ctx, views, num_objects, blend, acc.ptr)
         out = np.empty((num_objects, n), dtype=np.float32)
-        if out.size:
-            ctx.finalize(acc.ptr, out.size, out=out)
-        acc.release()
+        ctx.finalize(acc.ptr, out.size, out=out)
     if stats is not None:
         stats.update(st)
     return ContributionMatrix(values=out)

@@ -100,7 +100,21 @@ struct fs_context {
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     bool timing = false;
     std::vector<cudaEvent_t> stage_events;  // 4 per view when timing
+    // grow-only scratch reused across calls (no cudaMalloc/cudaFree per call)
+    long long scene_cap = 0;
+    double* up_means = nullptr;   // AoS staging of the scene upload
+    double* up_quats = nullptr;
+    double* up_scales = nullptr;
+    unsigned char* pinned_up[2] = {nullptr, nullptr};  // host->device staging ring
+    cudaEvent_t pinned_free[2] = {nullptr, nullptr};
+    float* tmp_f32 = nullptr;     // fs_finalize to host
+    size_t tmp_f32_cap = 0;
+    float* asg_in = nullptr;      // fs_assign with host buffers
+    uint8_t* asg_out = nullptr;
+    size_t asg_in_cap = 0, asg_out_cap = 0;
 };
+
+
 
 using fs::fail;
 
@@ -126,6 +140,47 @@ int dev_alloc(T** p, size_t count) {
         return fail(FS_ENOMEM, "cudaMalloc of %zu bytes failed: %s", count * sizeof(T),
                     cudaGetErrorString(e));
     }
+    return FS_OK;
+}
+
+constexpr size_t kUploadChunk = 8u << 20;  // pinned staging chunk (bytes)
+
+// Pageable host -> device copy through the context's two pinned chunks, so the
+// host memcpy of chunk i overlaps the DMA of chunk i-1.
+int upload(fs_context* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!ctx->pinned_up[0]) {
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->pinned_up[k]), kUploadChunk));
+            CK(cudaEventCreateWithFlags(&ctx->pinned_free[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->pinned_free[k], st));
+        }
+    }
+    const unsigned char* s = static_cast<const unsigned char*>(src);
+    unsigned char* d = static_cast<unsigned char*>(dst);
+    int slot = 0;
+    for (size_t off = 0; off < bytes; off += kUploadChunk) {
+        const size_t m = std::min(kUploadChunk, bytes - off);
+        CK(cudaEventSynchronize(ctx->pinned_free[slot]));
+        memcpy(ctx->pinned_up[slot], s + off, m);
+        CK(cudaMemcpyAsync(d + off, ctx->pinned_up[slot], m, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(ctx->pinned_free[slot], st));
+        slot ^= 1;
+    }
+    return FS_OK;
+}
+
+template <typename T>
+int grow(T** p, size_t* cap, size_t count) {
+    if (count <= *cap && *p) return FS_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *cap = 0;
+        return fail(FS_ENOMEM, "cudaMalloc of %zu bytes failed", count * sizeof(T));
+    }
+    *cap = count;
     return FS_OK;
 }
 
@@ -245,7 +300,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + 5 + 1 + 1; }
+int view_launches() { return 1 + 1 + 5 + 1 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
@@ -269,6 +324,7 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.r64 = w.r64;
     ra.acc = acc;
     ra.vc = w.vc;
+    fs::launch_mask_check(mask, (long long)cam.width * cam.height, w.vc, ctx->num_sms, w.stream);
     fs::launch_raster(ra, w.stream);
     if (ev) cudaEventRecord(ev[3], w.stream);
     if (log) fs::view_end_kernel<<<1, 32, 0, w.stream>>>(w.vc, log);
@@ -354,8 +410,14 @@ void fs_destroy(fs_context* ctx) {
     cudaDeviceSynchronize();
     for (auto& w : ctx->work) free_work(w);
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
-                    (void*)ctx->opac, (void*)ctx->tile_oa_table, (void*)ctx->view_log})
+                    (void*)ctx->opac, (void*)ctx->tile_oa_table, (void*)ctx->view_log,
+                    (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
+                    (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out})
         if (p) cudaFree(p);
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->pinned_up[k]) cudaFreeHost(ctx->pinned_up[k]);
+        if (ctx->pinned_free[k]) cudaEventDestroy(ctx->pinned_free[k]);
+    }
     for (cudaEvent_t e : ctx->stage_events) cudaEventDestroy(e);
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
     if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
@@ -419,26 +481,27 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
     int rc;
-    if ((rc = dev_alloc(&ctx->mx, n)) || (rc = dev_alloc(&ctx->my, n)) ||
-        (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
-        (rc = dev_alloc(&ctx->opac, n)))
-        return rc;
+    if (n > ctx->scene_cap) {
+        if ((rc = dev_alloc(&ctx->mx, n)) || (rc = dev_alloc(&ctx->my, n)) ||
+            (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->opac, n)) || (rc = dev_alloc(&ctx->up_means, 3 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->up_quats, 4 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->up_scales, 3 * (size_t)n)))
+            return rc;
+        ctx->scene_cap = n;
+    }
     ctx->n = n;
     if (n == 0) return FS_OK;
-    double *d_means = nullptr, *d_quats = nullptr, *d_scales = nullptr;
-    if ((rc = dev_alloc(&d_means, 3 * (size_t)n)) || (rc = dev_alloc(&d_quats, 4 * (size_t)n)) ||
-        (rc = dev_alloc(&d_scales, 3 * (size_t)n)))
+    cudaStream_t st = ctx->work[0].stream;
+    if ((rc = upload(ctx, ctx->up_means, means, 24 * (size_t)n, st)) ||
+        (rc = upload(ctx, ctx->up_quats, quats, 32 * (size_t)n, st)) ||
+        (rc = upload(ctx, ctx->up_scales, scales, 24 * (size_t)n, st)) ||
+        (rc = upload(ctx, ctx->opac, opacities, 8 * (size_t)n, st)))
         return rc;
-    CK(cudaMemcpy(d_means, means, 24 * (size_t)n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(d_quats, quats, 32 * (size_t)n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(d_scales, scales, 24 * (size_t)n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->opac, opacities, 8 * (size_t)n, cudaMemcpyHostToDevice));
-    fs::launch_scene_setup((int)n, d_means, d_quats, d_scales, ctx->mx, ctx->my, ctx->mz, ctx->sig, 0);
+    fs::launch_scene_setup((int)n, ctx->up_means, ctx->up_quats, ctx->up_scales, ctx->mx, ctx->my,
+                           ctx->mz, ctx->sig, st);
     CK(cudaGetLastError());
-    CK(cudaDeviceSynchronize());
-    cudaFree(d_means);
-    cudaFree(d_quats);
-    cudaFree(d_scales);
+    CK(cudaStreamSynchronize(st));
     return FS_OK;
 }
 
@@ -590,7 +653,10 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
     if (num_objects < 1 || num_objects > 65536)
         return fail(FS_EINVAL, "fs_accumulate: num_objects must be in [1, 65536], got %d", num_objects);
     if (!acc && ctx->n > 0) return fail(FS_EINVAL, "fs_accumulate: NULL accumulator");
-    if (stats) memset(stats, 0, sizeof(*stats));
+    if (stats) {
+        memset(stats, 0, sizeof(*stats));
+        stats->label_error_view = -1;
+    }
     if (n_views == 0 || ctx->n == 0) return FS_OK;
     int rc;
     int max_tiles = 1;
@@ -693,7 +759,14 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         if (log[v].overflow) return fail(FS_ENOMEM, "view %d: instance buffer overflow after retry", v);
         ++retried;
     }
+    long long bad_view = -1;
+    for (int v = 0; v < n_views; ++v)
+        if (log[v].max_label >= (unsigned)num_objects) {
+            bad_view = v;
+            break;
+        }
     if (stats) {
+        stats->label_error_view = bad_view;
         stats->views = n_views;
         stats->view_pixels = view_px;
         for (const auto& l : log) {
@@ -710,6 +783,9 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         stats->bin_ms = bin_ms;
         stats->raster_ms = raster_ms;
     }
+    if (bad_view >= 0)
+        return fail(FS_ELABEL, "view %lld: label %u exceeds object count %d", bad_view,
+                    log[bad_view].max_label, num_objects);
     return FS_OK;
 }
 
@@ -719,17 +795,17 @@ int fs_finalize(fs_context* ctx, const double* acc, int64_t count, float* out, i
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());  // acc may come from another stream (e.g. an NCCL all-reduce)
     cudaStream_t st = ctx->work[0].stream;
-    float* dst = out_on_device ? out : nullptr;
+    float* dst = out;
     if (!out_on_device) {
-        int rc = dev_alloc(&dst, (size_t)count);
+        int rc = grow(&ctx->tmp_f32, &ctx->tmp_f32_cap, (size_t)count);
         if (rc) return rc;
+        dst = ctx->tmp_f32;
     }
     fs::launch_finalize(acc, dst, count, st);
     CK(cudaGetLastError());
     if (!out_on_device) {
         CK(cudaMemcpyAsync(out, dst, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        cudaFree(dst);
     } else {
         CK(cudaStreamSynchronize(st));
     }
@@ -754,18 +830,28 @@ int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float
     uint8_t* dout = out;
     void *tmpA = nullptr, *tmpO = nullptr;
     if (!on_device) {
-        CK(cudaMallocAsync(&tmpA, in_bytes, st));
-        CK(cudaMallocAsync(&tmpO, out_bytes, st));
-        CK(cudaMemcpyAsync(tmpA, A, in_bytes, cudaMemcpyHostToDevice, st));
-        dA = static_cast<const float*>(tmpA);
-        dout = static_cast<uint8_t*>(tmpO);
+        if (ctx) {  // context-owned scratch (the context is single-threaded by contract)
+            int rc;
+            if ((rc = grow(&ctx->asg_in, &ctx->asg_in_cap, in_bytes / sizeof(float))) ||
+                (rc = grow(&ctx->asg_out, &ctx->asg_out_cap, out_bytes)))
+                return rc;
+            dA = ctx->asg_in;
+            dout = ctx->asg_out;
+            CK(cudaMemcpyAsync(ctx->asg_in, A, in_bytes, cudaMemcpyHostToDevice, st));
+        } else {
+            CK(cudaMallocAsync(&tmpA, in_bytes, st));
+            CK(cudaMallocAsync(&tmpO, out_bytes, st));
+            CK(cudaMemcpyAsync(tmpA, A, in_bytes, cudaMemcpyHostToDevice, st));
+            dA = static_cast<const float*>(tmpA);
+            dout = static_cast<uint8_t*>(tmpO);
+        }
     }
     fs::launch_assign(dA, n, num_objects, gamma, mode, dout, st);
     CK(cudaGetLastError());
     if (!on_device) {
         CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
-        CK(cudaFreeAsync(tmpA, st));
-        CK(cudaFreeAsync(tmpO, st));
+        if (tmpA) CK(cudaFreeAsync(tmpA, st));
+        if (tmpO) CK(cudaFreeAsync(tmpO, st));
     }
     CK(cudaStreamSynchronize(st));
     return FS_OK;

@@ -102,6 +102,8 @@ struct RasterArgs {
     ViewCounters* vc;
 };
 cudaError_t raster_configure();
+void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, int num_sms,
+                       cudaStream_t st);
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 
 // ---- fs_assign.cu ----

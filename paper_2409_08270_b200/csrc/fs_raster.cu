@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
     const unsigned int lbl0 = __shfl_sync(0xffffffffu, label, first);
     const bool uniform = __all_sync(0xffffffffu, !inside || label == lbl0);
+    // out-of-range labels (reported by mask_check_kernel) never address the accumulator
+    const bool lbl_ok = label < (unsigned)a.num_objects;
+    const bool lbl0_ok = lbl0 < (unsigned)a.num_objects;
 
     // alpha >= af_eff and T < tf_eff reproduce the reference's floors (and
     // their absence when a floor is 0: alpha >= 0 > -1, T >= 0 > -1)
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                     if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * 8 + t];
                 v += __shfl_xor_sync(0xffffffffu, v, 8);
                 v += __shfl_xor_sync(0xffffffffu, v, 16);
-                if (lane < kMini && k < nm && v > 0.0) {
+                if (lane < kMini && k < nm && v > 0.0 && lbl0_ok) {
                     atomicAdd(acc + (size_t)lbl0 * n_g + S.gid[S.list[warp][m0 + k]], v);
                 }
 #pragma unroll
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             } else {
 #pragma unroll
                 for (int k = 0; k < kMini; ++k) {
-                    if ((cb[k] >> lane) & 1u)
+                    if (((cb[k] >> lane) & 1u) && lbl_ok)
                         atomicAdd(acc + (size_t)label * n_g + S.gid[S.list[warp][m0 + k]],
                                   myval[k * kRowStride + lane]);
                     atom += __popc(cb[k]);
@@ -281,7 +284,27 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     }
 }
 
+// Largest label of a view's mask (contributions.py:108-114 is checked by the
+// host from this value; empty tiles are not visited by the raster kernel).
+__global__ void mask_check_kernel(const uint16_t* __restrict__ mask, long long count,
+                                  ViewCounters* __restrict__ vc) {
+    unsigned int m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x)
+        m = max(m, (unsigned int)mask[i]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(&vc->max_label, m);
+}
+
 }  // namespace
+
+void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, int num_sms,
+                       cudaStream_t st) {
+    if (count <= 0) return;
+    long long blocks = (count + 255) / 256;
+    if (blocks > num_sms * 4) blocks = num_sms * 4;
+    mask_check_kernel<<<(int)blocks, 256, 0, st>>>(mask, count, vc);
+}
 
 // Per device (called by fs_create after cudaSetDevice): opt in to >48 KB smem.
 cudaError_t raster_configure() {

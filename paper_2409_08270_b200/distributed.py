@@ -64,13 +64,12 @@ def _gpu_partial_host(scene, views, num_objects, blend) -> np.ndarray:
     n = len(scene)
     with ctx.lock:
         ctx.set_scene(scene)
-        acc = ctx.alloc(8 * num_objects * max(n, 1)).zero()
+        acc = ctx.buffer("acc64", 8 * num_objects * max(n, 1)).zero()
         ctx.accumulate([v for v, _ in views], [m.labels for _, m in views], num_objects,
                        blend.alpha_floor, blend.transmittance_floor, acc.ptr)
         out = np.zeros((num_objects, n), dtype=np.float64)
         if out.size:
             acc.to_host(out)
-        acc.release()
     return out
 
 

@@ -14,22 +14,39 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .contributions import ContributionMatrix, validate_views
+from .contributions import ContributionMatrix, check_shapes, run_device_accumulate, validate_views
 from .rasterizer import DEFAULT_BLEND, BlendConfig
 from .solver import Assignment, _check_gamma
 
 
 class LabelSolver:
-    def __init__(self, scene, device: Optional[int] = None):
+    """Accumulate once, then re-run the argmax for any gamma on the device.
+
+    ``own_buffers=False`` borrows the context's scratch buffers (one-shot
+    solves); the default keeps a private device copy of the matrix alive for
+    the solver's lifetime (the interactive-gamma service case).
+    """
+
+    def __init__(self, scene, device: Optional[int] = None, own_buffers: bool = True):
         from . import _native
 
         self._native = _native
         self.scene = scene
         self.ctx = _native.context(device)
+        self.own = own_buffers
         self.num_objects = 0
         self._A = None  # device float32 E x N
         self._out = None
         self.stats: dict = {}
+
+    def _buffers(self, e: int, n: int):
+        need_a, need_o = 4 * e * max(n, 1), e * max(n, 1)
+        if not self.own:
+            return self.ctx.buffer("A32", need_a), self.ctx.buffer("labels", need_o)
+        if self._A is None or self._A.nbytes < need_a:
+            self._A = self.ctx.alloc(need_a)
+            self._out = self.ctx.alloc(need_o)
+        return self._A, self._out
 
     def accumulate(self, views: Sequence, num_objects: int,
                    blend: BlendConfig = DEFAULT_BLEND, download: bool = True,
@@ -41,8 +58,11 @@ class LabelSolver:
         """
         views = list(views)
         e = int(num_objects)
-        validate_views(views, e)
         n = len(self.scene)
+        if process_group is not None or n == 0:
+            validate_views(views, e)
+        else:
+            check_shapes(views, e)
         ctx = self.ctx
         acc_t = None
         sel = views
@@ -55,35 +75,31 @@ class LabelSolver:
             world = dist.get_world_size(process_group)
             sel = [views[i] for i in shard_views(len(views), rank, world)]
             acc_t = torch.zeros(e * max(n, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
-            acc_ptr = acc_t.data_ptr()
         with ctx.lock:
             ctx.set_scene(self.scene)
             if acc_t is None:
-                acc = ctx.alloc(8 * e * max(n, 1)).zero()
-                acc_ptr = acc.ptr
-            self.stats = ctx.accumulate([v for v, _ in sel], [m.labels for _, m in sel], e,
-                                        blend.alpha_floor, blend.transmittance_floor, acc_ptr)
+                acc_ptr = ctx.buffer("acc64", 8 * e * max(n, 1)).zero().ptr
+            else:
+                acc_ptr = acc_t.data_ptr()
+            self.stats = run_device_accumulate(ctx, sel, e, blend, acc_ptr) if n else {}
         if acc_t is not None:
             import torch.distributed as dist
             dist.all_reduce(acc_t, group=process_group)
         with ctx.lock:
-            if self._A is None or self._A.nbytes < 4 * e * max(n, 1):
-                self._A = ctx.alloc(4 * e * max(n, 1))
-                self._out = ctx.alloc(e * max(n, 1))
+            A, out = self._buffers(e, n)
+            self._A_cur, self._out_cur = A, out
             if n:
-                ctx.finalize(acc_ptr, e * n, out_ptr=self._A.ptr)
-            if acc_t is None:
-                acc.release()
+                ctx.finalize(acc_ptr, e * n, out_ptr=A.ptr)
         self.num_objects = e
         if not download:
             return None
         values = np.empty((e, n), dtype=np.float32)
         if values.size:
-            self._A.to_host(values)
+            A.to_host(values)
         return ContributionMatrix(values=values)
 
     def assign(self, gamma: float, mode: str = "binary") -> Assignment:
-        if self._A is None:
+        if getattr(self, "_A_cur", None) is None:
             raise ValueError("accumulate() must run before assign()")
         gamma = _check_gamma(gamma)
         e, n = self.num_objects, len(self.scene)
@@ -91,18 +107,18 @@ class LabelSolver:
         if mode == "binary":
             if e != 2:
                 raise ValueError(f"binary assignment requires E=2, got E={e}")
-            nat.assign(None, gamma, nat.MODE_BINARY, ctx=self.ctx, on_device_ptr=self._A.ptr,
-                       n=n, e=e, out_ptr=self._out.ptr)
+            nat.assign(None, gamma, nat.MODE_BINARY, ctx=self.ctx, on_device_ptr=self._A_cur.ptr,
+                       n=n, e=e, out_ptr=self._out_cur.ptr)
             labels = np.empty(n, np.uint8)
-            self._out.to_host(labels)
+            self._out_cur.to_host(labels)
             return Assignment(mode="binary", gamma=gamma, labels=labels)
         if mode == "scene":
             if e < 2:
                 raise ValueError(f"scene assignment requires E>=2, got E={e}")
-            nat.assign(None, gamma, nat.MODE_SCENE, ctx=self.ctx, on_device_ptr=self._A.ptr,
-                       n=n, e=e, out_ptr=self._out.ptr)
+            nat.assign(None, gamma, nat.MODE_SCENE, ctx=self.ctx, on_device_ptr=self._A_cur.ptr,
+                       n=n, e=e, out_ptr=self._out_cur.ptr)
             member = np.empty((e, n), np.uint8)
-            self._out.to_host(member)
+            self._out_cur.to_host(member)
             return Assignment(mode="scene", gamma=gamma, membership=member)
         raise ValueError(f"unknown assignment mode {mode!r}")
 
@@ -114,6 +130,6 @@ def solve(scene, views: Sequence, num_objects: int, gamma: float = 0.0, mode: st
     Host numpy inputs in, host results out; with ``process_group`` the views
     are sharded over the group's GPUs and every rank returns the full result.
     """
-    s = LabelSolver(scene, device)
+    s = LabelSolver(scene, device, own_buffers=False)
     matrix = s.accumulate(views, num_objects, blend, process_group=process_group)
     return matrix, s.assign(gamma, mode)

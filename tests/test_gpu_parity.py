@@ -380,3 +380,24 @@ def test_primary_key_ties_resolved_by_full_depth():
     ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities,
                             [oracle.camera_of(view)], [m.labels], 2, threads=2)
     np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+
+
+def test_label_errors_detected_on_device_in_reference_order():
+    from paper_2409_08270_b200 import CameraView
+    g = GaussianScene([[0, 0, 2.0]], [[1, 0, 0, 0]], [[0.05] * 3], [0.9])
+    v = CameraView(0, 64, 64, 40.0, 40.0, 32.0, 32.0, np.eye(4))
+    ok = LabelMask(0, np.zeros((64, 64), np.uint16))
+    far = np.zeros((64, 64), np.uint16)
+    far[60, 2] = 7  # a tile no splat reaches
+    with pytest.raises(ValueError, match=r"view 0: label 7 at pixel \(60, 2\) exceeds object count 2"):
+        accumulate_contributions(g, [(v, ok), (v, LabelMask(0, far))], 2)
+    v3 = CameraView(3, 64, 64, 40.0, 40.0, 32.0, 32.0, np.eye(4))
+    bad_shape = LabelMask(3, np.zeros((8, 8), np.uint16))
+    v1 = CameraView(1, 64, 64, 40.0, 40.0, 32.0, 32.0, np.eye(4))
+    with pytest.raises(ValueError, match=r"view 1: label 7"):
+        accumulate_contributions(g, [(v, ok), (v1, LabelMask(1, far)), (v3, bad_shape)], 2)
+    with pytest.raises(ValueError, match="does not match"):
+        accumulate_contributions(g, [(v, ok), (v3, bad_shape), (v1, LabelMask(1, far))], 2)
+    # the context stays usable after a label error
+    A = accumulate_contributions(g, [(v, ok)], 2).values
+    assert A[0, 0] > 0
