@@ -312,21 +312,40 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (raster-accumulate), live events ----
+    # ---- roofline of the dominant kernel (raster-accumulate) ----
+    # The timed steps overlap views on 4 streams, so per-kernel event times
+    # there include other streams' work.  The kernel's own duration is taken
+    # from one more (untimed for `value`) pass on a 1-stream context with CUDA
+    # events around every raster launch on its stream.
+    ctx1 = _native.Context(local, streams=1)
+    ctx1.set_scene(wl.scene)
+    ctx1.set_timing(True)
+    iso = None
+    for _ in range(2):
+        acc.zero_()
+        iso = ctx1.accumulate(views, mask_ptrs, E, floors[0], floors[1], acc.data_ptr(),
+                              masks_on_device=True)
+    ctx1.close()
     st = stats[-1]
-    views_n = max(st["views"], 1)
-    raster_avg_s = st["raster_ms"] / views_n / 1e3
-    alg_bytes = (BYTES_PER_PIXEL * st["view_pixels"] + BYTES_PER_TILE_STEP * st["tile_steps"]
-                 + BYTES_PER_ATOMIC * st["atomics"]) / views_n
+    views_n = max(iso["views"], 1)
+    raster_avg_s = iso["raster_ms"] / views_n / 1e3
+    alg_bytes = (BYTES_PER_PIXEL * iso["view_pixels"] + BYTES_PER_TILE_STEP * iso["tile_steps"]
+                 + BYTES_PER_ATOMIC * iso["atomics"]) / views_n
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / raster_avg_s / 1e9 if raster_avg_s > 0 else None
     traffic = None
+    instr = None
     tp = ROOT / "profiles" / "raster_traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+            rec = json.loads(tp.read_text()).get(args.config, {})
+            traffic = rec.get("dram_bytes_per_launch")
+            instr = rec.get("warp_instructions_per_launch")
         except Exception:
             traffic = None
+    clk_summary = clk.summary()
+    sm_hz = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
+    issue_peak = 148 * 4 * sm_hz  # warp-instructions / s (one issue slot per scheduler per clock)
     stage_sum = st["prep_ms"] + st["bin_ms"] + st["raster_ms"]
     line = {
         "metric": "view-pixels/sec of contribution accumulation",
@@ -344,15 +363,22 @@ def main():
         "gpu_launches": int(sum(s["launches"] for s in stats) + 2 * args.steps),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "peak_source": peak_kind,
-                     "kernel": "raster_kernel (K3)",
+                     "peak_source": peak_kind, "kernel": "raster_kernel (K3)",
                      "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": raster_avg_s * 1e3,
-                     "note": "event-timed on the launching stream with 4 concurrent view streams"},
+                     "share_of_serial_step": iso["raster_ms"] / iso["gpu_ms"] if iso["gpu_ms"] else None,
+                     "timing": "CUDA events around each raster launch on its stream, 1-stream pass",
+                     "binding": {
+                         "resource": "SM warp-instruction issue (not HBM: see DESIGN.md)",
+                         "warp_instructions_per_launch": instr,
+                         "achieved_winst_per_s": (instr / raster_avg_s) if instr else None,
+                         "peak_winst_per_s": issue_peak,
+                         "frac": (instr / raster_avg_s / issue_peak) if instr else None,
+                         "instructions_source": "profiles/raster_traffic.json (ncu --set full)"}},
         "stages_ms_per_step": {"prep": st["prep_ms"], "bin": st["bin_ms"],
                                "raster": st["raster_ms"], "sum": stage_sum},
         "counters_per_step": {k: st[k] for k in ("emitted", "instances", "tile_steps",
                                                  "exact_evals", "atomics", "retried_views")},
-        "clocks": clk.summary(),
+        "clocks": clk_summary,
     }
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = {k: v for k, v in cpu_baseline(wl, args.cpu_views).items()

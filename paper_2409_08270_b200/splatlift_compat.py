@@ -1,0 +1,75 @@
+"""Drop-in switch for code written against the reference package ``splatlift``.
+
+``install()`` rebinds the hot-path entry points everywhere the reference
+imports them, so its CLI (``splatlift accumulate`` / ``splatlift assign``),
+its FastAPI service and user code run on the B200 kernels unchanged:
+
+    splatlift.accumulate_contributions / splatlift.contributions.accumulate_contributions
+    splatlift.cli.accumulate_contributions                (reference cli.py:17)
+    splatlift.assign_binary / assign_scene, splatlift.solver.*,
+    splatlift.cli.*  (cli.py:25), splatlift.service.*     (service.py:28)
+
+The replacement functions accept the reference's own ``GaussianScene``,
+``CameraView``, ``LabelMask`` and ``ContributionMatrix`` objects (they only
+read the documented attributes) and return objects with the reference's
+attributes and file formats (``values`` / ``save`` / ``load``;
+``labels`` / ``membership`` / ``save``).  ``uninstall()`` restores the
+originals.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import contributions as _contrib
+from . import solver as _solver
+
+_TARGETS = {
+    "accumulate_contributions": ["splatlift", "splatlift.contributions", "splatlift.cli"],
+    "assign_binary": ["splatlift", "splatlift.solver", "splatlift.cli", "splatlift.service"],
+    "assign_scene": ["splatlift", "splatlift.solver", "splatlift.cli", "splatlift.service"],
+}
+_saved: dict = {}
+
+
+def _replacement(name):
+    if name == "accumulate_contributions":
+        ref_matrix = importlib.import_module("splatlift.contributions").ContributionMatrix
+
+        def accumulate_contributions(scene, views, num_objects, blend=None, **kw):
+            from .rasterizer import DEFAULT_BLEND
+            m = _contrib.accumulate_contributions(scene, views, num_objects,
+                                                  blend if blend is not None else DEFAULT_BLEND,
+                                                  **kw)
+            return ref_matrix(values=m.values)  # the caller's own type
+
+        return accumulate_contributions
+    ref_assignment = importlib.import_module("splatlift.solver").Assignment
+    impl = getattr(_solver, name)
+
+    def assign(matrix, gamma):
+        a = impl(matrix, gamma)
+        return ref_assignment(mode=a.mode, gamma=a.gamma, labels=a.labels,
+                              membership=a.membership)
+
+    assign.__name__ = name
+    return assign
+
+
+def install() -> None:
+    for name, modules in _TARGETS.items():
+        fn = _replacement(name)
+        for modname in modules:
+            try:
+                mod = importlib.import_module(modname)
+            except ImportError:
+                continue
+            if hasattr(mod, name):
+                _saved.setdefault((modname, name), getattr(mod, name))
+                setattr(mod, name, fn)
+
+
+def uninstall() -> None:
+    for (modname, name), fn in _saved.items():
+        setattr(importlib.import_module(modname), name, fn)
+    _saved.clear()

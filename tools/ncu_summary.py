@@ -1,0 +1,38 @@
+"""Condense an ncu report (--set full) into the metrics DESIGN.md cites."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__grid_size", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+]
+
+
+def summarise(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    head, units = rows[0], rows[1]
+    out = []
+    for vals in rows[2:]:
+        rec = {"kernel": vals[head.index("Kernel Name")][:80]}
+        for k in KEYS:
+            if k in head:
+                i = head.index(k)
+                rec[k] = f"{vals[i]} {units[i]}".strip()
+        out.append(rec)
+    return out
+
+
+if __name__ == "__main__":
+    print(json.dumps(summarise(sys.argv[1]), indent=1))
