@@ -216,7 +216,7 @@ def main():
 
     torch.cuda.set_device(local)
     group = None
-    if world > 1:
+    if world > 1 or "RANK" in os.environ:  # torchrun: NCCL path even for one rank
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
 

@@ -6,7 +6,7 @@
 //   binning   (this file) -- per-tile buckets of gids in arbitrary order:
 //     bin_count   per-block tile histogram over a contiguous gid range (shared
 //                 memory atomics), written to a tile-major count matrix; also
-//                 the 16-bit primary depth key of every gid;
+//                 the 32-bit primary depth key of every gid;
 //     scan        exclusive scan of the count matrix -> per-(tile, block)
 //                 write offsets, tile_start, instance total, overflow flag;
 //     bin_emit    every block re-walks its gid range and places instances
@@ -34,11 +34,11 @@ __device__ __forceinline__ void gid_range(int n, int b, int g, int& lo, int& hi)
     hi = (int)min((long long)n, per * (b + 1));
 }
 
-// Primary key: the 16 highest bits in which the view's depth keys differ.
+// Primary key: the 32 highest bits in which the view's depth keys differ.
 __device__ __forceinline__ int primary_shift(const unsigned long long* oa) {
     const unsigned long long vary = oa[0] ^ oa[1];
     const int hb = vary ? 63 - __clzll((long long)vary) : 0;
-    return hb > 15 ? hb - 15 : 0;
+    return hb > 31 ? hb - 31 : 0;
 }
 
 // per-block tile histogram of a contiguous gid range -> count[t * g + b];
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinBuffers b, int n
         if (rc != ~0ull) {
             unsigned long long key = b.k64[g];
             if (key == ~0ull) key = z;
-            b.pk[g] = (unsigned short)((key >> shift) & 0xFFFFull);
+            b.pk[g] = (unsigned int)(key >> shift);
         }
     }
     __syncthreads();

@@ -67,7 +67,7 @@ struct Work {
     Rec32* r32 = nullptr;
     Rec64* r64 = nullptr;
     unsigned long long* k64 = nullptr;       // per gid order-preserving float64 depth key
-    unsigned short* pk = nullptr;            // per gid 16-bit primary depth key
+    unsigned int* pk = nullptr;              // per gid 32-bit primary depth key
     unsigned int* tie = nullptr;             // per splat tie id (fs_bin_splats only)
     unsigned int* inst = nullptr;            // per-tile buckets of gids
     unsigned long long* scratch64 = nullptr; // 2 x capacity: long-bucket merge scratch

@@ -43,13 +43,13 @@ void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 
 // ---- fs_bin.cu ----
 // Per-tile buckets of gids (any order) from per-block tile histograms, plus
-// the 16-bit primary depth key of every gid.
+// the 32-bit primary depth key of every gid.
 struct BinBuffers {
     int n;                              // Gaussians (or splats)
     const unsigned long long* rect;     // per gid
     const unsigned long long* k64;      // per gid: order-preserving float64 depth key
     const unsigned long long* key_oa;   // {OR, AND} of the visible depth keys
-    unsigned short* pk;                 // out: per gid primary key
+    unsigned int* pk;                   // out: per gid primary key
     unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets
     unsigned int* partial;              // bin_scan_blocks() partial sums
     unsigned int* tile_start;           // ntiles + 1
@@ -65,7 +65,7 @@ void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, 
 
 // Inputs of the per-tile depth ordering (fs_tilesort.cuh).
 struct TileSortKeys {
-    const unsigned short* pk;        // primary key per gid
+    const unsigned int* pk;          // primary key per gid
     const unsigned long long* k64;   // full depth key per gid
     const unsigned int* tie;         // tie id per gid (nullptr: the gid itself)
 };

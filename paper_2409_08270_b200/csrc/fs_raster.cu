@@ -2,29 +2,31 @@
 // into the E x N float64 contribution accumulator (reference
 // contributions.py:119-160, the `_accumulate_view` walk).
 //
-// One CTA per 16x16 tile, one thread per pixel; warp w owns tile rows 2w and
-// 2w+1.  The tile's depth-ordered list streams through shared memory in
-// batches of 256 records (one coalesced gather per thread).  While loading,
-// each thread also computes which warps' 2-row strips the record's
-// alpha-floor ellipse box can reach; every warp then compacts the batch to
-// its own list (ballot + popc), so a warp never iterates over splats that
-// cannot touch its pixels.
+// One CTA per 16x16 tile (its bucket already depth-ordered by the tile sort,
+// fs_tilesort.cuh), one thread per pixel; warp w owns tile rows 2w and 2w+1.
+// The eight warps walk the tile's list independently -- no block barriers:
 //
-// Each warp walks its list in mini-batches of 8 splats:
-//   A  float32 screen per (splat, pixel): a conservative power cut rejects
-//      samples whose alpha is certainly below alpha_floor (the reference
+//   gather   32 list entries per step: each lane loads one gid and its float32
+//            screen record, tests the record's alpha-floor ellipse box
+//            against the warp's 2x16 pixel strip, and the hits are appended
+//            (in list order) to a per-warp shared-memory ring;
+//   per mini-batch of 8 ring entries:
+//   A  transposed float32 screen: lane (splat k, row r) solves the quadratic
+//      for the columns of its row whose float32 power clears a conservative
+//      cut -- samples certainly below alpha_floor are dropped (the reference
 //      gives them no weight and no transmittance update, contributions.py:148);
-//   A2 the surviving (splat, pixel) pairs of the mini-batch are packed into a
-//      per-warp queue and the exact float64 alpha -- the reference's
-//      expression order, no FMA contraction, float64 exp, 0.99 clamp -- is
-//      computed for 32 pairs per round (alpha does not depend on T, so the
-//      expensive part runs on full warps);
-//   B  per pixel, in list order: alpha floor, w = alpha*T, T *= (1-alpha),
-//      T floor after the update (contributions.py:148-157);
-//   C  label-uniform warps reduce the 8 rows of w with a padded transpose in
-//      shared memory + 2 shuffles and issue one float64 atomic per splat;
-//      mixed-label warps issue one atomic per contributing lane.
-// The CTA stops when no pixel of the tile is active (contributions.py:158-159).
+//   A2 the surviving (splat, pixel) pairs are packed and the exact float64
+//      alpha -- reference expression order, no FMA contraction, float64 exp,
+//      0.99 clamp -- is computed 32 pairs per round (alpha does not depend on
+//      T, so the expensive part runs on full warps);
+//   B  every lane walks its own candidates in list order: alpha floor,
+//      w = alpha*T, T *= (1-alpha), T floor after the update (:148-157);
+//   C  label-uniform warps reduce w with a padded transpose in shared memory
+//      + 2 shuffles and issue one float64 atomic per splat; mixed-label warps
+//      issue one atomic per contributing pixel.
+// A warp stops when none of its pixels is active (contributions.py:158-159:
+// pixels are independent, the reference's tile-level break is an
+// optimisation of the same rule).
 #include <algorithm>
 
 #include "fs_common.cuh"
@@ -37,22 +39,24 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBatch = 256;
 constexpr int kMini = 8;
+constexpr int kRing = 64;       // per-warp ring of strip hits (>= kMini - 1 + 32)
 constexpr int kRowStride = 33;  // doubles per padded w/alpha row (bank-conflict-free transpose)
 
-struct RasterSmem {
-    Rec32 r32[kBatch];
-    Rec64 r64[kBatch];
-    unsigned int gid[kBatch];
-    unsigned char warp_mask[kBatch];
-    unsigned char list[kWarps][kBatch];
-    unsigned char queue[kWarps][kMini * 32];
-    double val[kWarps][kMini * kRowStride];  // alpha, then w
-    unsigned long long cnt_e[kWarps], cnt_a[kWarps];
+struct WarpSmem {
+    Rec32 rec[kRing];
+    unsigned int gid[kRing];
+    unsigned char queue[kMini * 32];
+    double val[kMini * kRowStride];  // alpha, then w
 };
 
-// tile-sort scratch (fs_tilesort.cuh) and the walk share the same bytes
+struct RasterSmem {
+    WarpSmem w[kWarps];
+    unsigned long long cnt_e[kWarps], cnt_a[kWarps], cnt_s[kWarps];
+};
+
+// The prologue's tile sort (fs_tilesort.cuh) and the walk share the same bytes;
+// sorting inside the raster kernel overlaps its latency with other CTAs' walks.
 constexpr size_t kSortBytes = 16 * (size_t)kTileSortCap + 4 * (kWarps * 256 + 64) + kTileSortCap;
 union RasterShared {
     RasterSmem walk;
@@ -90,25 +94,27 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const int tile = blockIdx.x;
     const unsigned int begin = a.sort.tile_start[tile], end = a.sort.tile_start[tile + 1];
     if (begin >= end) return;
+    const unsigned int n_list = end - begin;
 
     __shared__ __align__(16) RasterShared SH;
     RasterSmem& S = SH.walk;
     // prologue: the tile's bucket -> gids in the reference (depth, id) order
-    unsigned int* list = a.sort.inst + begin;
-    sort_tile_list(list, a.sort.scratch64 + 2ull * begin, end - begin, a.sort.keys, SH.sort,
-                   a.sort.cap);
-    const unsigned int* __restrict__ gids = list - begin;  // indexed by instance position
-
+    unsigned int* sorted = a.sort.inst + begin;
+    sort_tile_list(sorted, a.sort.scratch64 + 2ull * begin, n_list, a.sort.keys, SH.sort, a.sort.cap);
+    const unsigned int* __restrict__ list = sorted;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    WarpSmem& W = S.w[warp];
     const unsigned int lt_mask = (1u << lane) - 1u;
     const int x0 = (tile % a.tiles_x) * kTile, y0 = (tile / a.tiles_x) * kTile;
     const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
     const bool inside = px < a.width && py < a.height;
     const unsigned int label = inside ? a.mask[(size_t)py * a.width + px] : 0u;
+    // the warp's pixel-centre strip
     const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
+    const float v_lo = (float)(y0 + 2 * warp) + 0.5f, v_hi = v_lo + 1.0f;
     // screen lanes: k = lane & 7 (splat of the mini-batch), row = (lane >> 3) & 1
     const int scr_k = lane & 7;
-    const float scr_v = (float)(y0 + 2 * warp + ((lane >> 3) & 1)) + 0.5f;
+    const float scr_v = v_lo + (float)((lane >> 3) & 1);
 
     const unsigned int inside_mask = __ballot_sync(0xffffffffu, inside);
     const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
@@ -124,55 +130,40 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const double tf_eff = a.t_floor > 0.0 ? a.t_floor : -1.0;
     const long long n_g = a.n_gaussians;
     double* __restrict__ acc = a.acc;
-    double* __restrict__ myval = S.val[warp];
+    double* __restrict__ myval = W.val;
 
     double T = 1.0;
     bool active = inside;
-    bool warp_live = inside_mask != 0u;
     unsigned long long steps = 0, exact = 0, atom = 0;
+    int head = 0, cnt = 0;  // ring of strip hits
 
-    for (unsigned int b = begin; b < end; b += kBatch) {
-        // contributions.py:158-159 -- the whole tile terminated; also guards smem reuse
-        if (__syncthreads_count(active) == 0) break;
-        const unsigned int i = b + tid;
-        unsigned int wm = 0;
-        if (i < end) {
-            const unsigned int g = gids[i];
-            const Rec32 s = a.r32[g];
-            S.gid[tid] = g;
-            S.r32[tid] = s;
-            S.r64[tid] = a.r64[g];
-            // warps whose 2-row strip the alpha-floor ellipse box can reach
-            if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx)) {
-                const float r0 = ceilf(s.my - s.hy - 0.5f) - (float)y0;
-                const float r1 = floorf(s.my + s.hy - 0.5f) - (float)y0;
-                if (r1 >= 0.0f && r0 <= 15.0f) {
-                    const int w0 = max(0, (int)r0) >> 1, w1 = min(15, (int)r1) >> 1;
-                    wm = ((2u << w1) - 1u) & ~((1u << w0) - 1u);
-                }
-            }
+    for (unsigned int c = 0; c < n_list && __any_sync(0xffffffffu, active); c += 32) {
+        // ---- gather: 32 entries, keep the ones whose ellipse box meets the strip ----
+        const unsigned int idx = c + lane;
+        bool hit = false;
+        Rec32 s;
+        unsigned int g = 0;
+        if (idx < n_list) {
+            g = list[idx];
+            s = a.r32[g];
+            hit = !(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
+                    v_lo > s.my + s.hy);
         }
-        S.warp_mask[tid] = (unsigned char)wm;
-        __syncthreads();
-        const int nb = min((unsigned int)kBatch, end - b);
-        steps += nb;
-        if (!warp_live) continue;
-        // per-warp compaction of the batch
-        int cnt = 0;
-#pragma unroll
-        for (int c = 0; c < kBatch / 32; ++c) {
-            const bool hit = (S.warp_mask[c * 32 + lane] >> warp) & 1u;
-            const unsigned int bal = __ballot_sync(0xffffffffu, hit);
-            if (hit) S.list[warp][cnt + __popc(bal & lt_mask)] = (unsigned char)(c * 32 + lane);
-            cnt += __popc(bal);
+        steps += min(32u, n_list - c);
+        const unsigned int bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
+            W.rec[slot] = s;
+            W.gid[slot] = g;
         }
+        cnt += __popc(bal);
         __syncwarp();
-        for (int m0 = 0; m0 < cnt; m0 += kMini) {
-            const int nm = min(kMini, cnt - m0);
-            // ---- A: float32 screen, transposed: lane (k, row) solves for the
-            //      candidate columns of splat k on its pixel row ----
+        const bool last = c + 32 >= n_list;
+        while (cnt >= kMini || (last && cnt > 0)) {
+            const int nm = min(kMini, cnt);
+            // ---- A: float32 screen, transposed ----
             unsigned int rowmask = 0;
-            if (scr_k < nm) rowmask = row_candidates(S.r32[S.list[warp][m0 + scr_k]], scr_v, x0);
+            if (scr_k < nm) rowmask = row_candidates(W.rec[(head + scr_k) & (kRing - 1)], scr_v, x0);
             const unsigned int act = __ballot_sync(0xffffffffu, active);
             unsigned int cm[kMini];
             int base[kMini];
@@ -185,100 +176,103 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 base[k] = total;
                 total += __popc(cm[k]);
             }
-            if (total == 0) continue;
-            exact += total;
-            // ---- A2: exact float64 alpha on packed (splat, pixel) pairs ----
+            if (total > 0) {
+                exact += total;
+                // ---- A2: exact float64 alpha on packed (splat, pixel) pairs ----
 #pragma unroll
-            for (int k = 0; k < kMini; ++k)
-                if ((cm[k] >> lane) & 1u)
-                    S.queue[warp][base[k] + __popc(cm[k] & lt_mask)] = (unsigned char)((k << 5) | lane);
-            __syncwarp();
-            for (int c = lane; c < total; c += 32) {
-                const unsigned int e = S.queue[warp][c];
-                const int k = e >> 5, src = e & 31;
-                const Rec64 q = S.r64[S.list[warp][m0 + k]];
-                // pixel centre (k + 0.5, j + 0.5) of the source lane, exact in float64
-                const double cx = (double)(x0 + (src & 15)) + 0.5;
-                const double cy = (double)(y0 + 2 * warp + (src >> 4)) + 0.5;
-                // power = -0.5 * (a*du*du + c*dv*dv) - b*du*dv   (contributions.py:142-145)
-                const double ddu = __dsub_rn(cx, q.mx);
-                const double ddv = __dsub_rn(cy, q.my);
-                const double t1 = __dmul_rn(__dmul_rn(q.a, ddu), ddu);
-                const double t2 = __dmul_rn(__dmul_rn(q.c, ddv), ddv);
-                const double t3 = __dmul_rn(__dmul_rn(q.b, ddu), ddv);
-                const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), t3);
-                double alpha = __dmul_rn(q.o, exp(power));  // :146-147
-                myval[k * kRowStride + src] = alpha < kAlphaClamp ? alpha : kAlphaClamp;
-            }
-            __syncwarp();
-            // ---- B: per-pixel transmittance walk in list order ----
-            unsigned int cb[kMini];
+                for (int k = 0; k < kMini; ++k)
+                    if ((cm[k] >> lane) & 1u)
+                        W.queue[base[k] + __popc(cm[k] & lt_mask)] = (unsigned char)((k << 5) | lane);
+                __syncwarp();
+                for (int q0 = lane; q0 < total; q0 += 32) {
+                    const unsigned int e = W.queue[q0];
+                    const int k = e >> 5, src = e & 31;
+                    const Rec64 q = a.r64[W.gid[(head + k) & (kRing - 1)]];
+                    // pixel centre (k + 0.5, j + 0.5) of the source lane, exact in float64
+                    const double cx = (double)(x0 + (src & 15)) + 0.5;
+                    const double cy = (double)(y0 + 2 * warp + (src >> 4)) + 0.5;
+                    // power = -0.5 * (a*du*du + c*dv*dv) - b*du*dv   (contributions.py:142-145)
+                    const double ddu = __dsub_rn(cx, q.mx);
+                    const double ddv = __dsub_rn(cy, q.my);
+                    const double t1 = __dmul_rn(__dmul_rn(q.a, ddu), ddu);
+                    const double t2 = __dmul_rn(__dmul_rn(q.c, ddv), ddv);
+                    const double t3 = __dmul_rn(__dmul_rn(q.b, ddu), ddv);
+                    const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), t3);
+                    const double alpha = __dmul_rn(q.o, exp(power));  // :146-147
+                    myval[k * kRowStride + src] = alpha < kAlphaClamp ? alpha : kAlphaClamp;
+                }
+                __syncwarp();
+                // ---- B: every lane walks its own candidates in list order ----
+                unsigned int mine = 0;
 #pragma unroll
-            for (int k = 0; k < kMini; ++k) {
-                cb[k] = 0;
-                if (!cm[k]) continue;  // warp-uniform
-                bool contributes = false;
-                if (((cm[k] >> lane) & 1u) && active) {
-                    const double alpha = myval[k * kRowStride + lane];
-                    if (alpha >= af_eff) {  // :148-149
-                        const double w = __dmul_rn(alpha, T);       // :150
-                        T = __dmul_rn(T, __dsub_rn(1.0, alpha));    // :155
-                        active = !(T < tf_eff);                     // :156-157
-                        myval[k * kRowStride + lane] = w;
-                        contributes = w > 0.0;
+                for (int k = 0; k < kMini; ++k) mine |= ((cm[k] >> lane) & 1u) << k;
+                while (mine) {
+                    const int k = __ffs(mine) - 1;
+                    mine &= mine - 1u;
+                    double w = 0.0;
+                    if (active) {
+                        const double alpha = myval[k * kRowStride + lane];
+                        if (alpha >= af_eff) {                          // :148-149
+                            w = __dmul_rn(alpha, T);                     // :150
+                            T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
+                            active = !(T < tf_eff);                      // :156-157
+                        }
+                    }
+                    myval[k * kRowStride + lane] = w;
+                }
+                __syncwarp();
+                // ---- C: aggregation + float64 atomics ----
+                if (uniform) {
+                    const int k = lane & 7, seg = lane >> 3;
+                    unsigned int bits = 0;
+#pragma unroll
+                    for (int t = 0; t < kMini; ++t) bits = t == k ? cm[t] : bits;
+                    bits = (bits >> (seg * 8)) & 0xFFu;
+                    double v = 0.0;
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * 8 + t];
+                    v += __shfl_xor_sync(0xffffffffu, v, 8);
+                    v += __shfl_xor_sync(0xffffffffu, v, 16);
+                    const bool fire = lane < kMini && k < nm && v > 0.0 && lbl0_ok;
+                    if (fire)
+                        atomicAdd(acc + (size_t)lbl0 * n_g + W.gid[(head + k) & (kRing - 1)], v);
+                    atom += __popc(__ballot_sync(0xffffffffu, fire));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kMini; ++k) {
+                        bool fire = false;
+                        if ((cm[k] >> lane) & 1u) {
+                            const double w = myval[k * kRowStride + lane];
+                            fire = w > 0.0 && lbl_ok;
+                            if (fire)
+                                atomicAdd(acc + (size_t)label * n_g + W.gid[(head + k) & (kRing - 1)], w);
+                        }
+                        atom += __popc(__ballot_sync(0xffffffffu, fire));
                     }
                 }
-                cb[k] = __ballot_sync(0xffffffffu, contributes);
+                __syncwarp();
             }
-            __syncwarp();
-            // ---- C: aggregation + float64 atomics ----
-            if (uniform) {
-                const int k = lane & 7, seg = lane >> 3;
-                unsigned int bits = 0;
-#pragma unroll
-                for (int t = 0; t < kMini; ++t) bits = t == k ? cb[t] : bits;
-                bits = (bits >> (seg * 8)) & 0xFFu;
-                double v = 0.0;
-#pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * 8 + t];
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                if (lane < kMini && k < nm && v > 0.0 && lbl0_ok) {
-                    atomicAdd(acc + (size_t)lbl0 * n_g + S.gid[S.list[warp][m0 + k]], v);
-                }
-#pragma unroll
-                for (int t = 0; t < kMini; ++t) atom += cb[t] ? 1u : 0u;
-            } else {
-#pragma unroll
-                for (int k = 0; k < kMini; ++k) {
-                    if (((cb[k] >> lane) & 1u) && lbl_ok)
-                        atomicAdd(acc + (size_t)label * n_g + S.gid[S.list[warp][m0 + k]],
-                                  myval[k * kRowStride + lane]);
-                    atom += __popc(cb[k]);
-                }
-            }
-            __syncwarp();
-            if (a.t_floor > 0.0) {
-                warp_live = __any_sync(0xffffffffu, active);
-                if (!warp_live) break;
-            }
+            head = (head + nm) & (kRing - 1);
+            cnt -= nm;
         }
     }
     // per-CTA counters (one atomic each)
     if (lane == 0) {
         S.cnt_e[warp] = exact;
         S.cnt_a[warp] = atom;
+        S.cnt_s[warp] = steps;
     }
     __syncthreads();
     if (tid == 0) {
-        unsigned long long e = 0, at = 0;
+        unsigned long long e = 0, at = 0, st = 0;
         for (int w = 0; w < kWarps; ++w) {
             e += S.cnt_e[w];
             at += S.cnt_a[w];
+            st = max(st, S.cnt_s[w]);
         }
         ViewCounters* v = a.vc;
-        atomicAdd(&v->tile_steps, steps);
+        atomicAdd(&v->tile_steps, st);
         atomicAdd(&v->exact_evals, e);
         atomicAdd(&v->atomics, at);
     }
@@ -306,7 +300,7 @@ void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, 
     mask_check_kernel<<<(int)blocks, 256, 0, st>>>(mask, count, vc);
 }
 
-// Per device (called by fs_create after cudaSetDevice): opt in to >48 KB smem.
+// Per device (called by fs_create after cudaSetDevice).
 cudaError_t raster_configure() {
     return tile_sort_configure(kTileSortCap);
 }

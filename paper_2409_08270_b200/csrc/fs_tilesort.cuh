@@ -5,13 +5,14 @@
 // A bucket holds the gids whose tile rectangle covers the tile, in arbitrary
 // order.  The reference order is np.lexsort((index, depth)) with float64 depth
 // (rasterizer.py:91).  Per tile:
-//   1. stable LSD radix sort (shared memory, 2 x 8-bit digits) of
-//      (primary << 32 | gid) by the 16-bit primary key = the 16 highest bits
-//      in which the view's float64 depth keys differ (order-preserving);
-//   2. runs of equal primary key are re-ordered by (full 64-bit depth key,
-//      tie id) -- tie id = gid for scenes, the splat's gaussian_index for
-//      explicit splat lists.  A parallel inversion check skips sorted runs;
-//      only runs that need it get a (short) insertion sort.
+//   1. single-pass counting sort (shared memory, 2048 buckets) of
+//      (primary << 32 | gid) by an 11-bit digit that is monotone in the 32-bit
+//      primary key (= the 32 highest bits in which the view's float64 depth
+//      keys differ) over the bucket's own key range;
+//   2. runs of equal digit are ordered by the full order (primary key, full
+//      64-bit depth key, tie id) -- tie id = gid for scenes, the splat's
+//      gaussian_index for explicit splat lists.  A parallel inversion check
+//      skips sorted runs; only runs that need it get a (short) insertion sort.
 // Buckets longer than `cap` are sorted in chunks and merged through global
 // memory before step 2.  The result is exactly the reference's tile list.
 #pragma once
@@ -45,88 +46,6 @@ static __device__ __forceinline__ unsigned int block_excl_scan256(unsigned int v
     for (int w = 0; w < kWarps; ++w) base += w < warp ? s_w[w] : 0u;
     __syncthreads();
     return base + x - v;
-}
-
-// Stable LSD radix sort of n packed entries by their 16-bit primary key
-// (bits 32..47); returns the buffer holding the result (a or b).
-static __device__ unsigned long long* smem_sort_pk(unsigned long long* a, unsigned long long* b,
-                                                   unsigned int n, unsigned int* whist,
-                                                   unsigned int* s_misc) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned int lt_mask = (1u << lane) - 1u;
-    // digits that vary over this bucket
-    unsigned int o = 0, z = 0xFFFFu;
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
-        const unsigned int k = pk_of(a[i]);
-        o |= k;
-        z &= k;
-    }
-    o = __reduce_or_sync(0xffffffffu, o);
-    z = __reduce_and_sync(0xffffffffu, z);
-    if (lane == 0) {
-        s_misc[warp] = o;
-        s_misc[kWarps + warp] = z;
-    }
-    __syncthreads();
-    unsigned int vary = 0, allz = 0xFFFFu;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        vary |= s_misc[w];
-        allz &= s_misc[kWarps + w];
-    }
-    vary ^= allz;
-    __syncthreads();
-    // each warp owns a contiguous slice (keeps the scatter stable)
-    const unsigned int per = ((n + kWarps - 1) / kWarps + 31u) & ~31u;
-    const unsigned int lo = min(n, per * warp), hi = min(n, lo + per);
-    for (int shift = 0; shift < 16; shift += 8) {
-        if (!((vary >> shift) & 0xFFu)) continue;
-        for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) whist[i] = 0;
-        __syncthreads();
-        for (unsigned int base = lo; base < hi; base += 32) {
-            const unsigned int idx = base + lane;
-            const bool valid = idx < hi;
-            const unsigned int d = valid ? (pk_of(a[idx]) >> shift) & 0xFFu : 0u;
-            const unsigned int peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
-            if (valid && lane == 31 - __clz(peers)) whist[warp * 256 + d] += __popc(peers);
-            __syncwarp();
-        }
-        __syncthreads();
-        {
-            // digit-major, warp-minor exclusive offsets
-            const int d = threadIdx.x;
-            unsigned int run = 0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const unsigned int c = whist[w * 256 + d];
-                whist[w * 256 + d] = run;
-                run += c;
-            }
-            const unsigned int base = block_excl_scan256(run, s_misc);
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) whist[w * 256 + d] += base;
-        }
-        __syncthreads();
-        for (unsigned int base = lo; base < hi; base += 32) {
-            const unsigned int idx = base + lane;
-            const bool valid = idx < hi;
-            const unsigned long long e = valid ? a[idx] : 0ull;
-            const unsigned int d = (pk_of(e) >> shift) & 0xFFu;
-            const unsigned int peers = __match_any_sync(0xffffffffu, valid ? d : 256u + lane);
-            const unsigned int off = valid ? whist[warp * 256 + d] : 0u;
-            __syncwarp();
-            if (valid) {
-                b[off + __popc(peers & lt_mask)] = e;
-                if (lane == 31 - __clz(peers)) whist[warp * 256 + d] = off + __popc(peers);
-            }
-            __syncwarp();
-        }
-        __syncthreads();
-        unsigned long long* t = a;
-        a = b;
-        b = t;
-    }
-    return a;
 }
 
 // merge sorted src[lo, mid) and src[mid, hi) into dst[lo, hi) by primary key
@@ -190,6 +109,106 @@ static __device__ void fix_primary_ties(unsigned long long* e, unsigned int n,
     }
 }
 
+// ---- single-pass counting sort (the n <= cap path) ----
+// Entries are bucketed by an 11-bit digit that is monotone in the primary key
+// over this bucket's own key range; digit ties are then ordered by the full
+// (primary, 64-bit depth, id) order.  Not stable -- it does not need to be,
+// every tie is resolved by the full order afterwards.
+struct DigitMap {
+    unsigned int lo, shift;
+};
+
+static __device__ __forceinline__ unsigned int digit_of(unsigned int pk, DigitMap m) {
+    return (pk - m.lo) >> m.shift;
+}
+
+static __device__ __forceinline__ bool full_less(unsigned long long x, unsigned long long y,
+                                                 const TileSortKeys K) {
+    const unsigned int px = pk_of(x), py = pk_of(y);
+    if (px != py) return px < py;
+    return entry_less(x, y, K);
+}
+
+static __device__ unsigned long long* smem_count_sort(unsigned long long* a, unsigned long long* b,
+                                                      unsigned int n, unsigned int* hist,
+                                                      unsigned int* s_misc, DigitMap* map) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned int lo = 0xFFFFFFFFu, hi = 0;
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
+        const unsigned int k = pk_of(a[i]);
+        lo = min(lo, k);
+        hi = max(hi, k);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) {
+        s_misc[warp] = lo;
+        s_misc[kWarps + warp] = hi;
+    }
+    for (int i = threadIdx.x; i < 2048; i += kThreads) hist[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        lo = min(lo, s_misc[w]);
+        hi = max(hi, s_misc[kWarps + w]);
+    }
+    const unsigned int range = hi - lo;
+    const int bits = range ? 32 - __clz(range) : 0;
+    const DigitMap m{lo, bits > 11 ? (unsigned int)(bits - 11) : 0u};
+    *map = m;
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&hist[digit_of(pk_of(a[i]), m)], 1u);
+    __syncthreads();
+    unsigned int c[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        c[j] = hist[threadIdx.x * 8 + j];
+        sum += c[j];
+    }
+    unsigned int run = block_excl_scan256(sum, s_misc);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        hist[threadIdx.x * 8 + j] = run;
+        run += c[j];
+    }
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
+        const unsigned long long e = a[i];
+        b[atomicAdd(&hist[digit_of(pk_of(e), m)], 1u)] = e;
+    }
+    __syncthreads();
+    return b;
+}
+
+// Orders every run of equal digit by the full order (parallel inversion check,
+// insertion sort only for runs that need it).
+static __device__ void fix_digit_runs(unsigned long long* e, unsigned int n, const TileSortKeys K,
+                                      unsigned char* flag, DigitMap m) {
+    for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads)
+        flag[i] = (digit_of(pk_of(e[i]), m) == digit_of(pk_of(e[i + 1]), m) &&
+                   full_less(e[i + 1], e[i], K)) ? 1 : 0;
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads) {
+        const unsigned int d = digit_of(pk_of(e[i]), m);
+        if (digit_of(pk_of(e[i + 1]), m) != d || (i > 0 && digit_of(pk_of(e[i - 1]), m) == d)) continue;
+        unsigned int j = i + 1;
+        bool inverted = flag[i] != 0;
+        while (j + 1 < n && digit_of(pk_of(e[j + 1]), m) == d) {
+            inverted |= flag[j] != 0;
+            ++j;
+        }
+        if (!inverted) continue;
+        for (unsigned int x = i + 1; x <= j; ++x) {
+            const unsigned long long v = e[x];
+            unsigned int y = x;
+            while (y > i && full_less(v, e[y - 1], K)) {
+                e[y] = e[y - 1];
+                --y;
+            }
+            e[y] = v;
+        }
+    }
+}
+
 // Sorts list[0, n) (gids) into the reference order.  smem: at least
 // tile_sort_smem_bytes(cap) bytes; scratch64: 2n entries of global scratch.
 static __device__ __noinline__ void sort_tile_list(unsigned int* list,
@@ -207,8 +226,9 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list,
             a[i] = ((unsigned long long)K.pk[g] << 32) | g;
         }
         __syncthreads();
-        unsigned long long* res = smem_sort_pk(a, b, n, whist, misc);
-        fix_primary_ties(res, n, K, flag);
+        DigitMap m;
+        unsigned long long* res = smem_count_sort(a, b, n, whist, misc, &m);
+        fix_digit_runs(res, n, K, flag, m);
         __syncthreads();
         for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = (unsigned int)res[i];
         __syncthreads();
@@ -224,7 +244,10 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list,
             a[i] = ((unsigned long long)K.pk[g] << 32) | g;
         }
         __syncthreads();
-        const unsigned long long* res = smem_sort_pk(a, b, m, whist, misc);
+        DigitMap dm;
+        unsigned long long* res = smem_count_sort(a, b, m, whist, misc, &dm);
+        fix_digit_runs(res, m, K, flag, dm);  // chunk fully ordered
+        __syncthreads();
         for (unsigned int i = threadIdx.x; i < m; i += kThreads) g0[c0 + i] = res[i];
         __syncthreads();
     }
