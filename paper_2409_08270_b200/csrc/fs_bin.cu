@@ -41,26 +41,15 @@ __device__ __forceinline__ int primary_shift(const unsigned long long* oa) {
     return hb > 31 ? hb - 31 : 0;
 }
 
-// per-block tile histogram of a contiguous gid range -> count[t * g + b];
-// primary depth keys of the range
+// per-block tile histogram of a contiguous gid range -> count[t * g + b]
 __global__ void __launch_bounds__(kThreads) bin_count_kernel(BinBuffers b, int ntiles,
                                                              int tiles_x) {
     extern __shared__ unsigned int s_hist[];
     for (int t = threadIdx.x; t < ntiles; t += kThreads) s_hist[t] = 0;
     __syncthreads();
-    const int shift = primary_shift(b.key_oa);
-    const unsigned long long z = b.key_oa[1];
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
-    for (int g = lo + threadIdx.x; g < hi; g += kThreads) {
-        const unsigned long long rc = b.rect[g];
-        count_rect_tiles(rc, tiles_x, s_hist);
-        if (rc != ~0ull) {
-            unsigned long long key = b.k64[g];
-            if (key == ~0ull) key = z;
-            b.pk[g] = (unsigned int)(key >> shift);
-        }
-    }
+    for (int g = lo + threadIdx.x; g < hi; g += kThreads) count_rect_tiles(b.rect[g], tiles_x, s_hist);
     __syncthreads();
     for (int t = threadIdx.x; t < ntiles; t += kThreads)
         b.count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
@@ -160,16 +149,22 @@ __global__ void __launch_bounds__(kThreads) bin_emit_kernel(BinBuffers b, int nt
     for (int t = threadIdx.x; t < ntiles; t += kThreads)
         s_cur[t] = b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
     __syncthreads();
+    const int shift = primary_shift(b.key_oa);
+    const unsigned long long z = b.key_oa[1];
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
     for (int g = lo + threadIdx.x; g < hi; g += kThreads) {
         const unsigned long long rc = b.rect[g];
         if (rc == ~0ull) continue;
+        unsigned long long key = b.k64[g];
+        if (key == ~0ull) key = z;
+        // instance = (32-bit primary depth key, gid)
+        const unsigned long long e = ((key >> shift) << 32) | (unsigned int)g;
         const unsigned int tx0 = rc & 0xFFFF, tx1 = (rc >> 16) & 0xFFFF;
         const unsigned int ty0 = (rc >> 32) & 0xFFFF, ty1 = (rc >> 48) & 0xFFFF;
         for (unsigned int ty = ty0; ty <= ty1; ++ty)
             for (unsigned int tx = tx0; tx <= tx1; ++tx)
-                b.inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = (unsigned int)g;
+                b.inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = e;
     }
 }
 
@@ -179,7 +174,8 @@ __global__ void __launch_bounds__(kThreads) tile_sort_kernel(TileSortArgs t) {
     if (t.vc->overflow) return;
     const unsigned int begin = t.tile_start[tile], end = t.tile_start[tile + 1];
     if (begin >= end) return;
-    sort_tile_list(t.inst + begin, t.scratch64 + 2ull * begin, end - begin, t.keys, smem_raw, t.cap);
+    sort_tile_list(t.inst + begin, sorted_view(t.inst, begin), t.scratch64 + 2ull * begin, end - begin,
+                   t.keys, smem_raw, t.cap);
 }
 
 __device__ __forceinline__ void block_or_and(unsigned long long o, unsigned long long a,

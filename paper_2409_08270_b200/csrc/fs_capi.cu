@@ -67,9 +67,8 @@ struct Work {
     Rec32* r32 = nullptr;
     Rec64* r64 = nullptr;
     unsigned long long* k64 = nullptr;       // per gid order-preserving float64 depth key
-    unsigned int* pk = nullptr;              // per gid 32-bit primary depth key
     unsigned int* tie = nullptr;             // per splat tie id (fs_bin_splats only)
-    unsigned int* inst = nullptr;            // per-tile buckets of gids
+    unsigned long long* inst = nullptr;      // per-tile buckets of instances -> sorted gids
     unsigned long long* scratch64 = nullptr; // 2 x capacity: long-bucket merge scratch
     unsigned int* count_bt = nullptr;        // ntiles x bin_blocks
     unsigned int* partial = nullptr;         // bin_scan_blocks
@@ -188,7 +187,7 @@ void free_work(fs::Work& w) {
     auto f = [](void* p) {
         if (p) cudaFree(p);
     };
-    f(w.rect); f(w.r32); f(w.r64); f(w.k64); f(w.pk); f(w.tie); f(w.inst); f(w.scratch64);
+    f(w.rect); f(w.r32); f(w.r64); f(w.k64); f(w.tie); f(w.inst); f(w.scratch64);
     f(w.count_bt); f(w.partial); f(w.tile_start); f(w.vc); f(w.mask_dev);
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
@@ -206,7 +205,6 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
         if ((rc = dev_alloc(&w.r32, n))) return rc;
         if ((rc = dev_alloc(&w.r64, n))) return rc;
         if ((rc = dev_alloc(&w.k64, n))) return rc;
-        if ((rc = dev_alloc(&w.pk, n))) return rc;
         if ((rc = dev_alloc(&w.tie, n))) return rc;
         w.n_cap = n;
     }
@@ -264,7 +262,6 @@ fs::BinBuffers bin_buffers(fs::Work& w, int n) {
     b.rect = w.rect;
     b.k64 = w.k64;
     b.key_oa = &w.vc->key_or;  // key_or, key_and are adjacent
-    b.pk = w.pk;
     b.count_bt = w.count_bt;
     b.partial = w.partial;
     b.tile_start = w.tile_start;
@@ -278,7 +275,6 @@ fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr) 
     t.tile_start = w.tile_start;
     t.inst = w.inst;
     t.scratch64 = w.scratch64;
-    t.keys.pk = w.pk;
     t.keys.k64 = w.k64;
     t.keys.tie = tie;
     t.cap = fs::kTileSortCap;
@@ -556,9 +552,13 @@ static int copy_tile_lists(fs::Work& w, int ntiles, unsigned int n_valid, int64_
     *n_items = n_valid;
     if (items) {
         if (items_capacity < (int64_t)n_valid) return fail(FS_EINVAL, "fs_bin: items buffer too small");
-        std::vector<unsigned int> g(n_valid);
-        if (n_valid) CK(cudaMemcpy(g.data(), w.inst, sizeof(unsigned int) * n_valid, cudaMemcpyDeviceToHost));
-        for (unsigned int i = 0; i < n_valid; ++i) items[i] = g[i];
+        // bucket t's gids sit in the first half of its instance bytes (sorted_view)
+        std::vector<unsigned long long> g(n_valid);
+        if (n_valid) CK(cudaMemcpy(g.data(), w.inst, sizeof(unsigned long long) * n_valid, cudaMemcpyDeviceToHost));
+        for (int t = 0; t < ntiles; ++t) {
+            const unsigned int* v = fs::sorted_view(g.data(), starts[t]);
+            for (unsigned int i = starts[t]; i < starts[t + 1]; ++i) items[i] = v[i - starts[t]];
+        }
     }
     return FS_OK;
 }

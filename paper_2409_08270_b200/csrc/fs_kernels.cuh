@@ -42,18 +42,19 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
 void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 
 // ---- fs_bin.cu ----
-// Per-tile buckets of gids (any order) from per-block tile histograms, plus
-// the 32-bit primary depth key of every gid.
+// Per-tile buckets of instances (any order) from per-block tile histograms.
+// An instance is (32-bit primary depth key << 32 | gid); the primary key is
+// the 32 highest bits in which the view's float64 depth keys differ.
 struct BinBuffers {
     int n;                              // Gaussians (or splats)
     const unsigned long long* rect;     // per gid
     const unsigned long long* k64;      // per gid: order-preserving float64 depth key
     const unsigned long long* key_oa;   // {OR, AND} of the visible depth keys
-    unsigned int* pk;                   // out: per gid primary key
     unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets
     unsigned int* partial;              // bin_scan_blocks() partial sums
     unsigned int* tile_start;           // ntiles + 1
-    unsigned int* inst;                 // capacity: gids, depth-ordered by the tile sort
+    unsigned long long* inst;           // capacity: instances; the tile sort leaves each
+                                        // bucket's depth-ordered gids in sorted_view()
     unsigned int capacity;
 };
 constexpr int kMaxTiles = 49152;        // per-block tile histograms live in shared memory
@@ -63,15 +64,20 @@ cudaError_t bin_configure();
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
                 cudaStream_t st);
 
+// The depth-ordered gids of the bucket starting at `begin` overwrite the first
+// half of the bucket's own instance bytes.
+__host__ __device__ inline unsigned int* sorted_view(unsigned long long* inst, unsigned int begin) {
+    return reinterpret_cast<unsigned int*>(inst + begin);
+}
+
 // Inputs of the per-tile depth ordering (fs_tilesort.cuh).
 struct TileSortKeys {
-    const unsigned int* pk;          // primary key per gid
     const unsigned long long* k64;   // full depth key per gid
     const unsigned int* tie;         // tie id per gid (nullptr: the gid itself)
 };
 struct TileSortArgs {
     const unsigned int* tile_start;
-    unsigned int* inst;
+    unsigned long long* inst;
     unsigned long long* scratch64;   // 2 x capacity entries (long buckets only)
     TileSortKeys keys;
     unsigned int cap;

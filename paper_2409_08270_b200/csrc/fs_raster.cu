@@ -39,14 +39,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMini = 8;
+constexpr int kMini = 16;      // strip hits per mini-batch
 constexpr int kRing = 64;       // per-warp ring of strip hits (>= kMini - 1 + 32)
 constexpr int kRowStride = 33;  // doubles per padded w/alpha row (bank-conflict-free transpose)
 
 struct WarpSmem {
-    Rec32 rec[kRing];
+    unsigned int cm[kRing];  // candidate pixels of the hit (bit = lane)
     unsigned int gid[kRing];
-    unsigned char queue[kMini * 32];
+    unsigned short queue[kMini * 32];
     double val[kMini * kRowStride];  // alpha, then w
 };
 
@@ -99,8 +99,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     __shared__ __align__(16) RasterShared SH;
     RasterSmem& S = SH.walk;
     // prologue: the tile's bucket -> gids in the reference (depth, id) order
-    unsigned int* sorted = a.sort.inst + begin;
-    sort_tile_list(sorted, a.sort.scratch64 + 2ull * begin, n_list, a.sort.keys, SH.sort, a.sort.cap);
+    unsigned int* sorted = sorted_view(a.sort.inst, begin);
+    sort_tile_list(a.sort.inst + begin, sorted, a.sort.scratch64 + 2ull * begin, n_list, a.sort.keys,
+                   SH.sort, a.sort.cap);
     const unsigned int* __restrict__ list = sorted;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     WarpSmem& W = S.w[warp];
@@ -112,9 +113,6 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     // the warp's pixel-centre strip
     const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
     const float v_lo = (float)(y0 + 2 * warp) + 0.5f, v_hi = v_lo + 1.0f;
-    // screen lanes: k = lane & 7 (splat of the mini-batch), row = (lane >> 3) & 1
-    const int scr_k = lane & 7;
-    const float scr_v = v_lo + (float)((lane >> 3) & 1);
 
     const unsigned int inside_mask = __ballot_sync(0xffffffffu, inside);
     const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
@@ -138,22 +136,22 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     int head = 0, cnt = 0;  // ring of strip hits
 
     for (unsigned int c = 0; c < n_list && __any_sync(0xffffffffu, active); c += 32) {
-        // ---- gather: 32 entries, keep the ones whose ellipse box meets the strip ----
+        // ---- gather + A: 32 entries; float32 screen of the warp's two rows ----
         const unsigned int idx = c + lane;
-        bool hit = false;
-        Rec32 s;
-        unsigned int g = 0;
+        unsigned int g = 0, cand = 0;
         if (idx < n_list) {
             g = list[idx];
-            s = a.r32[g];
-            hit = !(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
-                    v_lo > s.my + s.hy);
+            const Rec32 s = a.r32[g];
+            if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
+                  v_lo > s.my + s.hy))
+                cand = row_candidates(s, v_lo, x0) | (row_candidates(s, v_hi, x0) << 16);
         }
         steps += min(32u, n_list - c);
+        const bool hit = cand != 0u;
         const unsigned int bal = __ballot_sync(0xffffffffu, hit);
         if (hit) {
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
-            W.rec[slot] = s;
+            W.cm[slot] = cand;
             W.gid[slot] = g;
         }
         cnt += __popc(bal);
@@ -161,18 +159,17 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         const bool last = c + 32 >= n_list;
         while (cnt >= kMini || (last && cnt > 0)) {
             const int nm = min(kMini, cnt);
-            // ---- A: float32 screen, transposed ----
-            unsigned int rowmask = 0;
-            if (scr_k < nm) rowmask = row_candidates(W.rec[(head + scr_k) & (kRing - 1)], scr_v, x0);
             const unsigned int act = __ballot_sync(0xffffffffu, active);
+            if (!act) {
+                cnt = 0;
+                break;
+            }
             unsigned int cm[kMini];
             int base[kMini];
             int total = 0;
 #pragma unroll
             for (int k = 0; k < kMini; ++k) {
-                const unsigned int r0 = __shfl_sync(0xffffffffu, rowmask, k);
-                const unsigned int r1 = __shfl_sync(0xffffffffu, rowmask, k + 8);
-                cm[k] = (r0 | (r1 << 16)) & act;
+                cm[k] = k < nm ? W.cm[(head + k) & (kRing - 1)] & act : 0u;
                 base[k] = total;
                 total += __popc(cm[k]);
             }
@@ -182,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
 #pragma unroll
                 for (int k = 0; k < kMini; ++k)
                     if ((cm[k] >> lane) & 1u)
-                        W.queue[base[k] + __popc(cm[k] & lt_mask)] = (unsigned char)((k << 5) | lane);
+                        W.queue[base[k] + __popc(cm[k] & lt_mask)] = (unsigned short)((k << 5) | lane);
                 __syncwarp();
                 for (int q0 = lane; q0 < total; q0 += 32) {
                     const unsigned int e = W.queue[q0];
@@ -223,17 +220,18 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 __syncwarp();
                 // ---- C: aggregation + float64 atomics ----
                 if (uniform) {
-                    const int k = lane & 7, seg = lane >> 3;
+                    // lane = (splat k, segment of kMini pixels)
+                    const int k = lane % kMini, seg = lane / kMini;
                     unsigned int bits = 0;
 #pragma unroll
                     for (int t = 0; t < kMini; ++t) bits = t == k ? cm[t] : bits;
-                    bits = (bits >> (seg * 8)) & 0xFFu;
+                    bits = (bits >> (seg * kMini)) & ((1u << kMini) - 1u);
                     double v = 0.0;
 #pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * 8 + t];
-                    v += __shfl_xor_sync(0xffffffffu, v, 8);
-                    v += __shfl_xor_sync(0xffffffffu, v, 16);
+                    for (int t = 0; t < kMini; ++t)
+                        if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * kMini + t];
+#pragma unroll
+                    for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                     const bool fire = lane < kMini && k < nm && v > 0.0 && lbl0_ok;
                     if (fire)
                         atomicAdd(acc + (size_t)lbl0 * n_g + W.gid[(head + k) & (kRing - 1)], v);

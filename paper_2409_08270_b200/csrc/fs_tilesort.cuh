@@ -209,9 +209,11 @@ static __device__ void fix_digit_runs(unsigned long long* e, unsigned int n, con
     }
 }
 
-// Sorts list[0, n) (gids) into the reference order.  smem: at least
-// tile_sort_smem_bytes(cap) bytes; scratch64: 2n entries of global scratch.
-static __device__ __noinline__ void sort_tile_list(unsigned int* list,
+// Sorts the instances in[0, n) into the reference order and writes their gids
+// to out[0, n) (out may alias in: every read precedes the first write).
+// smem: at least tile_sort_smem_bytes(cap) bytes; scratch64: 2n entries of
+// global scratch.
+static __device__ __noinline__ void sort_tile_list(const unsigned long long* in, unsigned int* out,
                                                    unsigned long long* scratch64, unsigned int n,
                                                    const TileSortKeys K, unsigned char* smem,
                                                    unsigned int cap) {
@@ -221,16 +223,13 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list,
     unsigned int* misc = whist + kWarps * 256;
     unsigned char* flag = reinterpret_cast<unsigned char*>(misc + 64);
     if (n <= cap) {
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
-            const unsigned int g = list[i];
-            a[i] = ((unsigned long long)K.pk[g] << 32) | g;
-        }
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) a[i] = in[i];
         __syncthreads();
         DigitMap m;
         unsigned long long* res = smem_count_sort(a, b, n, whist, misc, &m);
         fix_digit_runs(res, n, K, flag, m);
         __syncthreads();
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = (unsigned int)res[i];
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) out[i] = (unsigned int)res[i];
         __syncthreads();
         return;
     }
@@ -239,10 +238,7 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list,
     unsigned long long* g1 = scratch64 + n;
     for (unsigned int c0 = 0; c0 < n; c0 += cap) {
         const unsigned int m = min(cap, n - c0);
-        for (unsigned int i = threadIdx.x; i < m; i += kThreads) {
-            const unsigned int g = list[c0 + i];
-            a[i] = ((unsigned long long)K.pk[g] << 32) | g;
-        }
+        for (unsigned int i = threadIdx.x; i < m; i += kThreads) a[i] = in[c0 + i];
         __syncthreads();
         DigitMap dm;
         unsigned long long* res = smem_count_sort(a, b, m, whist, misc, &dm);
@@ -266,7 +262,7 @@ static __device__ __noinline__ void sort_tile_list(unsigned int* list,
     // tie fix-up flags for the long list live in the other global buffer
     fix_primary_ties(src, n, K, reinterpret_cast<unsigned char*>(dst));
     __syncthreads();
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) list[i] = (unsigned int)src[i];
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) out[i] = (unsigned int)src[i];
     __syncthreads();
 }
 
