@@ -68,6 +68,10 @@ static_assert(sizeof(RasterShared) <= 48 * 1024, "raster shared memory must stay
 // power clears the conservative cut, from the roots of the quadratic
 //   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
 // (widened by float32 rounding margins).  Returns a 16-bit column mask.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0) {
     if (!(s.cut > -INFINITY)) return 0xFFFFu;  // exact blend: no alpha floor
     const float dv = v_centre - s.my;
@@ -97,6 +101,10 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const unsigned int n_list = end - begin;
 
     __shared__ __align__(16) RasterShared SH;
+    __shared__ unsigned long long s_cnt[3];
+    __shared__ unsigned int s_done;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_done = 0;  // the tile sort's barriers publish these
     RasterSmem& S = SH.walk;
     // prologue: the tile's bucket -> gids in the reference (depth, id) order
     unsigned int* sorted = sorted_view(a.sort.inst, begin);
@@ -135,12 +143,13 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     unsigned long long steps = 0, exact = 0, atom = 0;
     int head = 0, cnt = 0;  // ring of strip hits
 
+    unsigned int g_next = (unsigned)lane < n_list ? list[lane] : 0u;
     for (unsigned int c = 0; c < n_list && __any_sync(0xffffffffu, active); c += 32) {
         // ---- gather + A: 32 entries; float32 screen of the warp's two rows ----
         const unsigned int idx = c + lane;
-        unsigned int g = 0, cand = 0;
+        unsigned int g = g_next, cand = 0;
+        if (idx + 32 < n_list) g_next = list[idx + 32];  // next chunk's gids in flight
         if (idx < n_list) {
-            g = list[idx];
             const Rec32 s = a.r32[g];
             if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
                   v_lo > s.my + s.hy))
@@ -153,6 +162,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
             W.cm[slot] = cand;
             W.gid[slot] = g;
+            prefetch_l1(a.r64 + g);  // its float64 record is read by A2
+            prefetch_l1(reinterpret_cast<const char*>(a.r64 + g) + 47);
         }
         cnt += __popc(bal);
         __syncwarp();
@@ -255,24 +266,20 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             cnt -= nm;
         }
     }
-    // per-CTA counters (one atomic each)
+    // per-CTA counters: the last warp to finish issues the global atomics (no
+    // end-of-tile barrier -- warps leave as soon as their strip is done)
     if (lane == 0) {
-        S.cnt_e[warp] = exact;
-        S.cnt_a[warp] = atom;
-        S.cnt_s[warp] = steps;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        unsigned long long e = 0, at = 0, st = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            e += S.cnt_e[w];
-            at += S.cnt_a[w];
-            st = max(st, S.cnt_s[w]);
+        atomicAdd(&s_cnt[0], exact);
+        atomicAdd(&s_cnt[1], atom);
+        atomicMax(&s_cnt[2], steps);
+        __threadfence_block();
+        if (atomicAdd(&s_done, 1u) == kWarps - 1) {
+            __threadfence_block();
+            ViewCounters* v = a.vc;
+            atomicAdd(&v->tile_steps, atomicAdd(&s_cnt[2], 0ull));
+            atomicAdd(&v->exact_evals, atomicAdd(&s_cnt[0], 0ull));
+            atomicAdd(&v->atomics, atomicAdd(&s_cnt[1], 0ull));
         }
-        ViewCounters* v = a.vc;
-        atomicAdd(&v->tile_steps, st);
-        atomicAdd(&v->exact_evals, e);
-        atomicAdd(&v->atomics, at);
     }
 }
 

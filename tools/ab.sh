@@ -8,8 +8,8 @@ B="python bench.py --config C2 --views 4 --steps 1 --warmup 1 --no-cpu --no-e2e 
 for v in _variants/*.so; do
   n=$(basename $v .so)
   cp $v $LIB
-  if [ -n "$AB_TESTS" ]; then
-    timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider $AB_TESTS > gpurun_out/ab_$n.pytest.log 2>&1
+  if [ -n "$AB_K" ]; then
+    timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "$AB_K" > gpurun_out/ab_$n.pytest.log 2>&1
     echo "$n: $(tail -1 gpurun_out/ab_$n.pytest.log)"
   fi
   $B > gpurun_out/ab_$n.log 2>&1 && \
