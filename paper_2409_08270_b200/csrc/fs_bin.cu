@@ -240,8 +240,8 @@ void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, 
 }
 
 size_t tile_sort_smem_bytes(unsigned int cap) {
-    // two packed (key, gid) buffers, per-warp digit counters, misc, run flags
-    return 16 * (size_t)cap + sizeof(unsigned int) * (kWarps * 256 + 64) + cap;
+    // packed (key, gid) entries, digit counters, misc, 16-bit entry indices
+    return 8 * (size_t)cap + sizeof(unsigned int) * (2048 + 64) + 2 * (size_t)cap;
 }
 
 cudaError_t tile_sort_configure(unsigned int cap) {

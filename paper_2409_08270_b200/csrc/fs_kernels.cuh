@@ -94,7 +94,7 @@ void launch_splat_keys(int k, const double* mean2d, const long long* radius, con
                        ViewCounters* vc, int num_sms, cudaStream_t st);
 
 // ---- fs_raster.cu ----
-constexpr unsigned int kTileSortCap = 2048;  // bucket entries sorted in shared memory
+constexpr unsigned int kTileSortCap = 3584;  // bucket entries sorted in shared memory
 struct RasterArgs {
     int width, height, tiles_x, ntiles;
     int num_objects;

@@ -57,7 +57,7 @@ struct RasterSmem {
 
 // The prologue's tile sort (fs_tilesort.cuh) and the walk share the same bytes;
 // sorting inside the raster kernel overlaps its latency with other CTAs' walks.
-constexpr size_t kSortBytes = 16 * (size_t)kTileSortCap + 4 * (kWarps * 256 + 64) + kTileSortCap;
+constexpr size_t kSortBytes = 10 * (size_t)kTileSortCap + 4 * (2048 + 64);
 union RasterShared {
     RasterSmem walk;
     unsigned char sort[kSortBytes];

@@ -9,10 +9,10 @@
 //      (primary << 32 | gid) by an 11-bit digit that is monotone in the 32-bit
 //      primary key (= the 32 highest bits in which the view's float64 depth
 //      keys differ) over the bucket's own key range;
-//   2. runs of equal digit are ordered by the full order (primary key, full
-//      64-bit depth key, tie id) -- tie id = gid for scenes, the splat's
-//      gaussian_index for explicit splat lists.  A parallel inversion check
-//      skips sorted runs; only runs that need it get a (short) insertion sort.
+//   2. entries sharing a digit are ranked within their digit run by the full
+//      order (primary key, full 64-bit depth key, tie id) -- tie id = gid for
+//      scenes, the splat's gaussian_index for explicit splat lists -- each
+//      thread ranking its own entries, so runs cost no serial passes.
 // Buckets longer than `cap` are sorted in chunks and merged through global
 // memory before step 2.  The result is exactly the reference's tile list.
 #pragma once
@@ -129,9 +129,11 @@ static __device__ __forceinline__ bool full_less(unsigned long long x, unsigned 
     return entry_less(x, y, K);
 }
 
-static __device__ unsigned long long* smem_count_sort(unsigned long long* a, unsigned long long* b,
-                                                      unsigned int n, unsigned int* hist,
-                                                      unsigned int* s_misc, DigitMap* map) {
+// a[0, n) -> b[0, n): indices into a, grouped by digit (unordered within a
+// digit); hist[d] is left at the end offset of digit d.
+static __device__ void smem_count_sort(const unsigned long long* a, unsigned short* b,
+                                       unsigned int n, unsigned int* hist, unsigned int* s_misc,
+                                       DigitMap* map) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned int lo = 0xFFFFFFFFu, hi = 0;
     for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
@@ -171,41 +173,32 @@ static __device__ unsigned long long* smem_count_sort(unsigned long long* a, uns
         run += c[j];
     }
     __syncthreads();
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
-        const unsigned long long e = a[i];
-        b[atomicAdd(&hist[digit_of(pk_of(e), m)], 1u)] = e;
-    }
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads)
+        b[atomicAdd(&hist[digit_of(pk_of(a[i]), m)], 1u)] = (unsigned short)i;
     __syncthreads();
-    return b;
 }
 
-// Orders every run of equal digit by the full order (parallel inversion check,
-// insertion sort only for runs that need it).
-static __device__ void fix_digit_runs(unsigned long long* e, unsigned int n, const TileSortKeys K,
-                                      unsigned char* flag, DigitMap m) {
-    for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads)
-        flag[i] = (digit_of(pk_of(e[i]), m) == digit_of(pk_of(e[i + 1]), m) &&
-                   full_less(e[i + 1], e[i], K)) ? 1 : 0;
-    __syncthreads();
-    for (unsigned int i = threadIdx.x; i + 1 < n; i += kThreads) {
-        const unsigned int d = digit_of(pk_of(e[i]), m);
-        if (digit_of(pk_of(e[i + 1]), m) != d || (i > 0 && digit_of(pk_of(e[i - 1]), m) == d)) continue;
-        unsigned int j = i + 1;
-        bool inverted = flag[i] != 0;
-        while (j + 1 < n && digit_of(pk_of(e[j + 1]), m) == d) {
-            inverted |= flag[j] != 0;
-            ++j;
+// Places every entry of the digit-sorted e[0, n) at its final position:
+// entries alone in their digit stay, entries of a digit run of length r are
+// ranked within the run by the full order (r comparisons each, all threads in
+// parallel).  hist[d] = end offset of digit d (as left by smem_count_sort).
+// store(pos, entry) receives every entry exactly once.
+template <class Store>
+static __device__ __forceinline__ void place_digit_runs(const unsigned long long* a,
+                                                        const unsigned short* idx, unsigned int n,
+                                                        const unsigned int* hist, DigitMap m,
+                                                        const TileSortKeys K, Store store) {
+    for (unsigned int p = threadIdx.x; p < n; p += kThreads) {
+        const unsigned long long v = a[idx[p]];
+        const unsigned int d = digit_of(pk_of(v), m);
+        const unsigned int s = d ? hist[d - 1] : 0u, t = hist[d];
+        unsigned int pos = p;
+        if (t - s > 1u) {
+            pos = s;
+            for (unsigned int q = s; q < t; ++q)  // (skipping itself: equal keys take the slow path)
+                pos += (q != p && full_less(a[idx[q]], v, K)) ? 1u : 0u;
         }
-        if (!inverted) continue;
-        for (unsigned int x = i + 1; x <= j; ++x) {
-            const unsigned long long v = e[x];
-            unsigned int y = x;
-            while (y > i && full_less(v, e[y - 1], K)) {
-                e[y] = e[y - 1];
-                --y;
-            }
-            e[y] = v;
-        }
+        store(pos, v);
     }
 }
 
@@ -218,18 +211,16 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
                                                    const TileSortKeys K, unsigned char* smem,
                                                    unsigned int cap) {
     unsigned long long* a = reinterpret_cast<unsigned long long*>(smem);
-    unsigned long long* b = a + cap;
-    unsigned int* whist = reinterpret_cast<unsigned int*>(b + cap);
-    unsigned int* misc = whist + kWarps * 256;
-    unsigned char* flag = reinterpret_cast<unsigned char*>(misc + 64);
+    unsigned int* whist = reinterpret_cast<unsigned int*>(a + cap);
+    unsigned int* misc = whist + 2048;
+    unsigned short* b = reinterpret_cast<unsigned short*>(misc + 64);
     if (n <= cap) {
         for (unsigned int i = threadIdx.x; i < n; i += kThreads) a[i] = in[i];
         __syncthreads();
         DigitMap m;
-        unsigned long long* res = smem_count_sort(a, b, n, whist, misc, &m);
-        fix_digit_runs(res, n, K, flag, m);
-        __syncthreads();
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) out[i] = (unsigned int)res[i];
+        smem_count_sort(a, b, n, whist, misc, &m);
+        place_digit_runs(a, b, n, whist, m, K,
+                         [&](unsigned int pos, unsigned long long v) { out[pos] = (unsigned int)v; });
         __syncthreads();
         return;
     }
@@ -241,10 +232,9 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
         for (unsigned int i = threadIdx.x; i < m; i += kThreads) a[i] = in[c0 + i];
         __syncthreads();
         DigitMap dm;
-        unsigned long long* res = smem_count_sort(a, b, m, whist, misc, &dm);
-        fix_digit_runs(res, m, K, flag, dm);  // chunk fully ordered
-        __syncthreads();
-        for (unsigned int i = threadIdx.x; i < m; i += kThreads) g0[c0 + i] = res[i];
+        smem_count_sort(a, b, m, whist, misc, &dm);
+        unsigned long long* dst = g0 + c0;  // chunk fully ordered
+        place_digit_runs(a, b, m, whist, dm, K, [&](unsigned int pos, unsigned long long v) { dst[pos] = v; });
         __syncthreads();
     }
     unsigned long long* src = g0;
