@@ -73,6 +73,7 @@ struct Work {
     unsigned int* count_bt = nullptr;        // ntiles x bin_blocks
     unsigned int* partial = nullptr;         // bin_scan_blocks
     unsigned int* tile_start = nullptr;
+    unsigned int* tile_order = nullptr;      // raster launch order (tile_order_kernel)
     ViewCounters* vc = nullptr;
     uint16_t* mask_dev = nullptr;
     uint16_t* pinned = nullptr;
@@ -188,7 +189,7 @@ void free_work(fs::Work& w) {
         if (p) cudaFree(p);
     };
     f(w.rect); f(w.r32); f(w.r64); f(w.k64); f(w.tie); f(w.inst); f(w.scratch64);
-    f(w.count_bt); f(w.partial); f(w.tile_start); f(w.vc); f(w.mask_dev);
+    f(w.count_bt); f(w.partial); f(w.tile_start); f(w.tile_order); f(w.vc); f(w.mask_dev);
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
     if (w.done) cudaEventDestroy(w.done);
@@ -219,6 +220,7 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
     }
     if (ntiles > w.ntiles_cap) {
         if ((rc = dev_alloc(&w.tile_start, (size_t)ntiles + 1))) return rc;
+        if ((rc = dev_alloc(&w.tile_order, (size_t)ntiles))) return rc;
         if ((rc = dev_alloc(&w.count_bt, (size_t)ntiles * fs::bin_blocks(ctx->num_sms)))) return rc;
         w.ntiles_cap = ntiles;
     }
@@ -296,7 +298,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + 5 + 1 + 1 + 1; }
+int view_launches() { return 1 + 1 + 5 + 1 + 1 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
@@ -320,6 +322,7 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.r64 = w.r64;
     ra.acc = acc;
     ra.vc = w.vc;
+    ra.tile_order = w.tile_order;
     fs::launch_mask_check(mask, (long long)cam.width * cam.height, w.vc, ctx->num_sms, w.stream);
     fs::launch_raster(ra, w.stream);
     if (ev) cudaEventRecord(ev[3], w.stream);

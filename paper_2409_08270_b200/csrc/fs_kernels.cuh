@@ -106,6 +106,7 @@ struct RasterArgs {
     const Rec64* r64;
     double* acc;                   // E x N float64 accumulator
     ViewCounters* vc;
+    unsigned int* tile_order;      // ntiles scratch: tiles by decreasing bucket length
 };
 cudaError_t raster_configure();
 void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, int num_sms,
