@@ -175,22 +175,32 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 cnt = 0;
                 break;
             }
-            unsigned int cm[kMini];
-            int base[kMini];
-            int total = 0;
+            // this lane's candidates of the mini-batch (bit k = k-th strip hit)
+            unsigned int mine = 0;
 #pragma unroll
-            for (int k = 0; k < kMini; ++k) {
-                cm[k] = k < nm ? W.cm[(head + k) & (kRing - 1)] & act : 0u;
-                base[k] = total;
-                total += __popc(cm[k]);
+            for (int k = 0; k < kMini; ++k)
+                if (k < nm) mine |= ((W.cm[(head + k) & (kRing - 1)] >> lane) & 1u) << k;
+            if (!active) mine = 0;
+            // lane-major packing of the (splat, pixel) pairs: warp prefix sum
+            const unsigned int n_mine = __popc(mine);
+            unsigned int incl = n_mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
+            const int total = (int)__shfl_sync(0xffffffffu, incl, 31);
             if (total > 0) {
                 exact += total;
                 // ---- A2: exact float64 alpha on packed (splat, pixel) pairs ----
-#pragma unroll
-                for (int k = 0; k < kMini; ++k)
-                    if ((cm[k] >> lane) & 1u)
-                        W.queue[base[k] + __popc(cm[k] & lt_mask)] = (unsigned short)((k << 5) | lane);
+                {
+                    unsigned int mm = mine, q = incl - n_mine;
+                    while (mm) {
+                        const int k = __ffs(mm) - 1;
+                        mm &= mm - 1u;
+                        W.queue[q++] = (unsigned short)((k << 5) | lane);
+                    }
+                }
                 __syncwarp();
                 for (int q0 = lane; q0 < total; q0 += 32) {
                     const unsigned int e = W.queue[q0];
@@ -211,31 +221,29 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 }
                 __syncwarp();
                 // ---- B: every lane walks its own candidates in list order ----
-                unsigned int mine = 0;
-#pragma unroll
-                for (int k = 0; k < kMini; ++k) mine |= ((cm[k] >> lane) & 1u) << k;
-                while (mine) {
-                    const int k = __ffs(mine) - 1;
-                    mine &= mine - 1u;
-                    double w = 0.0;
-                    if (active) {
-                        const double alpha = myval[k * kRowStride + lane];
-                        if (alpha >= af_eff) {                          // :148-149
-                            w = __dmul_rn(alpha, T);                     // :150
-                            T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
-                            active = !(T < tf_eff);                      // :156-157
+                {
+                    unsigned int mm = mine;
+                    while (mm) {
+                        const int k = __ffs(mm) - 1;
+                        mm &= mm - 1u;
+                        double w = 0.0;
+                        if (active) {
+                            const double alpha = myval[k * kRowStride + lane];
+                            if (alpha >= af_eff) {                          // :148-149
+                                w = __dmul_rn(alpha, T);                     // :150
+                                T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
+                                active = !(T < tf_eff);                      // :156-157
+                            }
                         }
+                        myval[k * kRowStride + lane] = w;
                     }
-                    myval[k * kRowStride + lane] = w;
                 }
                 __syncwarp();
                 // ---- C: aggregation + float64 atomics ----
                 if (uniform) {
                     // lane = (splat k, segment of kMini pixels)
                     const int k = lane % kMini, seg = lane / kMini;
-                    unsigned int bits = 0;
-#pragma unroll
-                    for (int t = 0; t < kMini; ++t) bits = t == k ? cm[t] : bits;
+                    unsigned int bits = k < nm ? W.cm[(head + k) & (kRing - 1)] & act : 0u;
                     bits = (bits >> (seg * kMini)) & ((1u << kMini) - 1u);
                     double v = 0.0;
 #pragma unroll
@@ -244,20 +252,20 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
 #pragma unroll
                     for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                     const bool fire = lane < kMini && k < nm && v > 0.0 && lbl0_ok;
-                    if (fire)
+                    if (fire) {
                         atomicAdd(acc + (size_t)lbl0 * n_g + W.gid[(head + k) & (kRing - 1)], v);
-                    atom += __popc(__ballot_sync(0xffffffffu, fire));
-                } else {
-#pragma unroll
-                    for (int k = 0; k < kMini; ++k) {
-                        bool fire = false;
-                        if ((cm[k] >> lane) & 1u) {
-                            const double w = myval[k * kRowStride + lane];
-                            fire = w > 0.0 && lbl_ok;
-                            if (fire)
-                                atomicAdd(acc + (size_t)label * n_g + W.gid[(head + k) & (kRing - 1)], w);
+                        ++atom;
+                    }
+                } else if (lbl_ok) {
+                    unsigned int mm = mine;
+                    while (mm) {
+                        const int k = __ffs(mm) - 1;
+                        mm &= mm - 1u;
+                        const double w = myval[k * kRowStride + lane];
+                        if (w > 0.0) {
+                            atomicAdd(acc + (size_t)label * n_g + W.gid[(head + k) & (kRing - 1)], w);
+                            ++atom;
                         }
-                        atom += __popc(__ballot_sync(0xffffffffu, fire));
                     }
                 }
                 __syncwarp();
@@ -268,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     }
     // per-CTA counters: the last warp to finish issues the global atomics (no
     // end-of-tile barrier -- warps leave as soon as their strip is done)
+    atom = __reduce_add_sync(0xffffffffu, (unsigned int)atom);  // per-lane counts
     if (lane == 0) {
         atomicAdd(&s_cnt[0], exact);
         atomicAdd(&s_cnt[1], atom);
