@@ -143,14 +143,22 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     unsigned long long steps = 0, exact = 0, atom = 0;
     int head = 0, cnt = 0;  // ring of strip hits
 
+    // software pipeline: records one chunk ahead, gids two chunks ahead
     unsigned int g_next = (unsigned)lane < n_list ? list[lane] : 0u;
+    Rec32 s_next;
+    if ((unsigned)lane < n_list) s_next = a.r32[g_next];
+    unsigned int g_next2 = (unsigned)lane + 32 < n_list ? list[lane + 32] : 0u;
     for (unsigned int c = 0; c < n_list && __any_sync(0xffffffffu, active); c += 32) {
         // ---- gather + A: 32 entries; float32 screen of the warp's two rows ----
         const unsigned int idx = c + lane;
         unsigned int g = g_next, cand = 0;
-        if (idx + 32 < n_list) g_next = list[idx + 32];  // next chunk's gids in flight
+        const Rec32 s = s_next;
+        if (idx + 32 < n_list) {
+            s_next = a.r32[g_next2];
+            g_next = g_next2;
+        }
+        if (idx + 64 < n_list) g_next2 = list[idx + 64];
         if (idx < n_list) {
-            const Rec32 s = a.r32[g];
             if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
                   v_lo > s.my + s.hy))
                 cand = row_candidates(s, v_lo, x0) | (row_candidates(s, v_hi, x0) << 16);
