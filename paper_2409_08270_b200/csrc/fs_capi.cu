@@ -314,8 +314,8 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.ntiles = ntiles;
     ra.num_objects = num_objects;
     ra.n_gaussians = ctx->n;
-    ra.alpha_floor = alpha_floor;
-    ra.t_floor = t_floor;
+    ra.af_eff = alpha_floor > 0.0 ? alpha_floor : -1.0;  // contributions.py:148-149
+    ra.tf_eff = t_floor > 0.0 ? t_floor : -1.0;          // contributions.py:156-157
     ra.mask = mask;
     ra.sort = tile_sort_args(w);
     ra.r32 = w.r32;

@@ -99,7 +99,9 @@ struct RasterArgs {
     int width, height, tiles_x, ntiles;
     int num_objects;
     long long n_gaussians;
-    double alpha_floor, t_floor;
+    // alpha >= af_eff and T < tf_eff reproduce the reference's floors, and their
+    // absence when a floor is 0 (alpha >= 0 > -1, T >= 0 > -1): see raster_floor()
+    double af_eff, tf_eff;
     const uint16_t* mask;          // H x W labels (device)
     TileSortArgs sort;             // bucket -> depth-ordered gid list (prologue)
     const Rec32* r32;

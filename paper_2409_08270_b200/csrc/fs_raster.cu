@@ -44,6 +44,7 @@ constexpr int kRing = 64;       // per-warp ring of strip hits (>= kMini - 1 + 3
 constexpr int kRowStride = 33;  // doubles per padded w/alpha row (bank-conflict-free transpose)
 
 struct WarpSmem {
+    Rec64 rec[kMini];        // float64 records of the mini-batch's hits
     unsigned int cm[kRing];  // candidate pixels of the hit (bit = lane)
     unsigned int gid[kRing];
     unsigned short queue[kMini * 32];
@@ -52,7 +53,6 @@ struct WarpSmem {
 
 struct RasterSmem {
     WarpSmem w[kWarps];
-    unsigned long long cnt_e[kWarps], cnt_a[kWarps], cnt_s[kWarps];
 };
 
 // The prologue's tile sort (fs_tilesort.cuh) and the walk share the same bytes;
@@ -62,7 +62,9 @@ union RasterShared {
     RasterSmem walk;
     unsigned char sort[kSortBytes];
 };
-static_assert(sizeof(RasterShared) <= 48 * 1024, "raster shared memory must stay static (<= 48 KB)");
+// dynamic shared memory per CTA; 4 CTAs per SM must stay resident
+constexpr size_t kRasterSmem = sizeof(RasterShared);
+static_assert(4 * (kRasterSmem + 1024) <= 228 * 1024, "raster needs 4 resident CTAs per SM");
 
 // Candidate columns of one pixel row for one splat: the pixels whose float32
 // power clears the conservative cut, from the roots of the quadratic
@@ -100,7 +102,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     if (begin >= end) return;
     const unsigned int n_list = end - begin;
 
-    __shared__ __align__(16) RasterShared SH;
+    extern __shared__ __align__(16) unsigned char raster_smem[];
+    RasterShared& SH = *reinterpret_cast<RasterShared*>(raster_smem);
     __shared__ unsigned long long s_cnt[3];
     __shared__ unsigned int s_done;
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
@@ -130,10 +133,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const bool lbl_ok = label < (unsigned)a.num_objects;
     const bool lbl0_ok = lbl0 < (unsigned)a.num_objects;
 
-    // alpha >= af_eff and T < tf_eff reproduce the reference's floors (and
-    // their absence when a floor is 0: alpha >= 0 > -1, T >= 0 > -1)
-    const double af_eff = a.alpha_floor > 0.0 ? a.alpha_floor : -1.0;
-    const double tf_eff = a.t_floor > 0.0 ? a.t_floor : -1.0;
+    const double af_eff = a.af_eff, tf_eff = a.tf_eff;
     const long long n_g = a.n_gaussians;
     double* __restrict__ acc = a.acc;
     double* __restrict__ myval = W.val;
@@ -170,8 +170,6 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
             W.cm[slot] = cand;
             W.gid[slot] = g;
-            prefetch_l1(a.r64 + g);  // its float64 record is read by A2
-            prefetch_l1(reinterpret_cast<const char*>(a.r64 + g) + 47);
         }
         cnt += __popc(bal);
         __syncwarp();
@@ -183,6 +181,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 cnt = 0;
                 break;
             }
+            // the batch's float64 records: loads in flight while the pairs are packed
+            Rec64 rq;
+            if (lane < nm) rq = a.r64[W.gid[(head + lane) & (kRing - 1)]];
             // this lane's candidates of the mini-batch (bit k = k-th strip hit)
             unsigned int mine = 0;
 #pragma unroll
@@ -209,11 +210,12 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         W.queue[q++] = (unsigned short)((k << 5) | lane);
                     }
                 }
+                if (lane < nm) W.rec[lane] = rq;
                 __syncwarp();
                 for (int q0 = lane; q0 < total; q0 += 32) {
                     const unsigned int e = W.queue[q0];
                     const int k = e >> 5, src = e & 31;
-                    const Rec64 q = a.r64[W.gid[(head + k) & (kRing - 1)]];
+                    const Rec64 q = W.rec[k];
                     // pixel centre (k + 0.5, j + 0.5) of the source lane, exact in float64
                     const double cx = (double)(x0 + (src & 15)) + 0.5;
                     const double cy = (double)(y0 + 2 * warp + (src >> 4)) + 0.5;
@@ -366,13 +368,16 @@ void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, 
 
 // Per device (called by fs_create after cudaSetDevice).
 cudaError_t raster_configure() {
-    return tile_sort_configure(kTileSortCap);
+    cudaError_t e = tile_sort_configure(kTileSortCap);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(raster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kRasterSmem);
 }
 
 void launch_raster(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
     tile_order_kernel<<<1, 1024, 0, st>>>(a.sort.tile_start, a.ntiles, a.tile_order);
-    raster_kernel<<<a.ntiles, kThreads, 0, st>>>(a);
+    raster_kernel<<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
 }
 
 }  // namespace fs
