@@ -5,12 +5,12 @@
 //
 //   binning   (this file) -- per-tile buckets of gids in arbitrary order:
 //     bin_count   per-block tile histogram over a contiguous gid range (shared
-//                 memory atomics), written to a tile-major count matrix; also
-//                 the 32-bit primary depth key of every gid;
+//                 memory atomics), written to a tile-major count matrix;
 //     scan        exclusive scan of the count matrix -> per-(tile, block)
 //                 write offsets, tile_start, instance total, overflow flag;
 //     bin_emit    every block re-walks its gid range and places instances
-//                 with shared-memory cursors (no global atomics);
+//                 (32-bit primary depth key << 32 | gid) with shared-memory
+//                 cursors (no global atomics);
 //   ordering  (fs_tilesort.cuh) -- each tile's bucket is sorted in shared
 //             memory by the primary key, ties resolved by (float64 key, id).
 //
@@ -27,6 +27,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kBinThreads = 1024;  // count / emit: latency-bound gid walks, full occupancy
 
 __device__ __forceinline__ void gid_range(int n, int b, int g, int& lo, int& hi) {
     const long long per = ((long long)n + g - 1) / g;
@@ -42,16 +43,16 @@ __device__ __forceinline__ int primary_shift(const unsigned long long* oa) {
 }
 
 // per-block tile histogram of a contiguous gid range -> count[t * g + b]
-__global__ void __launch_bounds__(kThreads) bin_count_kernel(BinBuffers b, int ntiles,
+__global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinBuffers b, int ntiles,
                                                              int tiles_x) {
     extern __shared__ unsigned int s_hist[];
-    for (int t = threadIdx.x; t < ntiles; t += kThreads) s_hist[t] = 0;
+    for (int t = threadIdx.x; t < ntiles; t += kBinThreads) s_hist[t] = 0;
     __syncthreads();
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
-    for (int g = lo + threadIdx.x; g < hi; g += kThreads) count_rect_tiles(b.rect[g], tiles_x, s_hist);
+    for (int g = lo + threadIdx.x; g < hi; g += kBinThreads) count_rect_tiles(b.rect[g], tiles_x, s_hist);
     __syncthreads();
-    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+    for (int t = threadIdx.x; t < ntiles; t += kBinThreads)
         b.count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
 }
 
@@ -142,18 +143,18 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(unsigned int* __re
 
 // per-block: cursors from the scanned matrix, then shared-memory atomics place
 // every instance of the block's gid range
-__global__ void __launch_bounds__(kThreads) bin_emit_kernel(BinBuffers b, int ntiles, int tiles_x,
+__global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int ntiles, int tiles_x,
                                                             const ViewCounters* __restrict__ vc) {
     if (vc->overflow) return;
     extern __shared__ unsigned int s_cur[];
-    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+    for (int t = threadIdx.x; t < ntiles; t += kBinThreads)
         s_cur[t] = b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
     __syncthreads();
     const int shift = primary_shift(b.key_oa);
     const unsigned long long z = b.key_oa[1];
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
-    for (int g = lo + threadIdx.x; g < hi; g += kThreads) {
+    for (int g = lo + threadIdx.x; g < hi; g += kBinThreads) {
         const unsigned long long rc = b.rect[g];
         if (rc == ~0ull) continue;
         unsigned long long key = b.k64[g];
@@ -232,11 +233,11 @@ void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, 
     const int g = bin_blocks(num_sms), g2 = bin_scan_blocks(num_sms);
     const size_t smem = sizeof(unsigned int) * (size_t)ntiles;
     const long long m = (long long)ntiles * g;
-    bin_count_kernel<<<g, kThreads, smem, st>>>(b, ntiles, tiles_x);
+    bin_count_kernel<<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x);
     scan_reduce_kernel<<<g2, kThreads, 0, st>>>(b.count_bt, m, b.partial);
     scan_partials_kernel<<<1, 1024, 0, st>>>(b.partial, g2, b.capacity, vc);
     scan_apply_kernel<<<g2, kThreads, 0, st>>>(b.count_bt, m, g, b.partial, ntiles, b.tile_start, vc);
-    bin_emit_kernel<<<g, kThreads, smem, st>>>(b, ntiles, tiles_x, vc);
+    bin_emit_kernel<<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, vc);
 }
 
 size_t tile_sort_smem_bytes(unsigned int cap) {

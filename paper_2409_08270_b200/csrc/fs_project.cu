@@ -74,7 +74,7 @@ __device__ __forceinline__ void warp_or_and(unsigned long long& o, unsigned long
 // binning only) Gaussians whose opacity is below the alpha floor: they can
 // never pass `alpha >= alpha_floor` (contributions.py:148), so they touch no
 // pixel.  Stats keep the reference's meaning regardless.
-__global__ void __launch_bounds__(256) project_kernel(
+__global__ void __launch_bounds__(256, 4) project_kernel(
     int n, const double* __restrict__ gmx, const double* __restrict__ gmy,
     const double* __restrict__ gmz, const double* __restrict__ sig,
     const double* __restrict__ opac, Camera cam, double alpha_floor, int cull_floor,
@@ -189,15 +189,19 @@ __global__ void __launch_bounds__(256) project_kernel(
             s.b = (float)ib;
             s.c = (float)ic;
             if (alpha_floor > 0.0 && o >= alpha_floor && alive) {
-                // alpha >= floor  <=>  power >= log(floor / o)  <=>  d^T conic d <= qmax
-                double qmax = 2.0 * log(o / alpha_floor);
-                double hx = sqrt(qmax * a) * (1.0 + 1e-5) + 0.01;
-                double hy = sqrt(qmax * c) * (1.0 + 1e-5) + 0.01;
-                double spread = (fabs(ia) + fabs(ic) + 2.0 * fabs(ib)) * (hx * hx + hy * hy);
-                double margin = 0.02 + 1e-6 * spread;
-                s.cut = (float)(log(alpha_floor / o) - margin);
-                s.hx = (float)hx;
-                s.hy = (float)hy;
+                // alpha >= floor  <=>  power >= log(floor / o)  <=>  d^T conic d <= qmax.
+                // Screen-only quantities: float32 (their ~1e-7 relative error is far
+                // inside the 1e-5 / 0.01 px / 0.02 margins).
+                const float L = logf((float)o / (float)alpha_floor);  // log(o / floor) >= 0
+                const float qmax = 2.0f * fmaxf(L, 0.0f);
+                const float hx = sqrtf(qmax * (float)a) * (1.0f + 1e-5f) + 0.01f;
+                const float hy = sqrtf(qmax * (float)c) * (1.0f + 1e-5f) + 0.01f;
+                const float spread = (fabsf((float)ia) + fabsf((float)ic) + 2.0f * fabsf((float)ib)) *
+                                     (hx * hx + hy * hy);
+                const float margin = 0.02f + 1e-6f * spread;
+                s.cut = -L - margin;
+                s.hx = hx;
+                s.hy = hy;
             } else if (alpha_floor > 0.0) {
                 s.cut = __int_as_float(0x7f800000);  // +inf: never passes
                 s.hx = 0.0f;

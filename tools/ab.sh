@@ -15,6 +15,6 @@ for v in _variants/*.so; do
   $B > gpurun_out/ab_$n.log 2>&1 && \
     ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv \
         --log-file gpurun_out/ab_$n.csv $B > /dev/null 2>&1
-  echo "$n: $(python tools/launches.py gpurun_out/ab_$n.csv 16 | grep raster_kernel)"
+  python tools/launches.py gpurun_out/ab_$n.csv 16 | grep -E "raster_kernel|project_kernel|bin_emit|bin_count|TOTAL" | sed "s/^/$n: /"
 done
 cp /tmp/lib_orig.so $LIB
