@@ -6,8 +6,10 @@
 //   binning   (this file) -- per-tile buckets of gids in arbitrary order:
 //     bin_count   per-block tile histogram over a contiguous gid range (shared
 //                 memory atomics), written to a tile-major count matrix;
-//     scan        exclusive scan of the count matrix -> per-(tile, block)
-//                 write offsets, tile_start, instance total, overflow flag;
+//     tile_scan   one warp per tile scans the tile's row of the count matrix
+//                 -> per-(tile, block) offsets inside the bucket, bucket length;
+//     tile_start  one CTA: bucket starts, instance total, overflow flag, and
+//                 the raster launch order (longest buckets first);
 //     bin_emit    every block re-walks its gid range and places instances
 //                 (32-bit primary depth key << 32 | gid) with shared-memory
 //                 cursors (no global atomics);
@@ -56,99 +58,117 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinBuffers b, in
         b.count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
 }
 
-// exclusive scan of v over the block (blockDim == kThreads); *total = block sum
-__device__ __forceinline__ unsigned int block_scan(unsigned int v, unsigned int* s_w,
-                                                   unsigned int* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned int x = v;
+// per tile (one warp each): exclusive scan of the tile's row of the count
+// matrix in place -> offsets of the blocks' runs inside the bucket; the row
+// sum is the bucket length
+__global__ void __launch_bounds__(kThreads) tile_scan_kernel(unsigned int* __restrict__ count_bt,
+                                                             int ntiles, int g,
+                                                             unsigned int* __restrict__ tile_total) {
+    const int t = (int)((blockIdx.x * kThreads + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (t >= ntiles) return;
+    unsigned int* row = count_bt + (size_t)t * g;
+    unsigned int carry = 0;
+    for (int i0 = 0; i0 < g; i0 += 32) {
+        const int i = i0 + lane;
+        const unsigned int v = i < g ? row[i] : 0u;
+        unsigned int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (i < g) row[i] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) tile_total[t] = carry;
+}
+
+// One CTA: bucket starts (exclusive scan of the bucket lengths), the instance
+// total / overflow flag, and the raster launch order -- tiles by decreasing
+// bucket length (counting sort on length / 8), so the long tiles start in the
+// first wave and the short ones fill the tail.
+__global__ void __launch_bounds__(1024) tile_start_kernel(const unsigned int* __restrict__ total,
+                                                          int ntiles, unsigned int capacity,
+                                                          ViewCounters* __restrict__ vc,
+                                                          unsigned int* __restrict__ tile_start,
+                                                          unsigned int* __restrict__ order) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned int hist[1024];
+    __shared__ unsigned int h_w[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (ntiles + 1023) / 1024;
+    const int t0 = min(ntiles, tid * per), t1 = min(ntiles, t0 + per);
+    unsigned long long sum = 0;
+    for (int t = t0; t < t1; ++t) sum += total[t];
+    unsigned long long x = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     if (lane == 31) s_w[warp] = x;
+    hist[tid] = 0;
     __syncthreads();
-    unsigned int base = 0, tot = 0;
+    if (warp == 0) {
+        const unsigned long long w = s_w[lane];
+        unsigned long long z = w;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        base += w < warp ? s_w[w] : 0u;
-        tot += s_w[w];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        s_w[lane] = z - w;
     }
     __syncthreads();
-    *total = tot;
-    return base + x - v;
-}
-
-// 3-kernel exclusive scan of the tile-major (tile, block) count matrix
-__global__ void __launch_bounds__(kThreads) scan_reduce_kernel(const unsigned int* __restrict__ a,
-                                                               long long m,
-                                                               unsigned int* __restrict__ partial) {
-    __shared__ unsigned int s_w[kWarps];
-    const long long per = (m + gridDim.x - 1) / gridDim.x;
-    const long long lo = min(m, per * blockIdx.x), hi = min(m, lo + per);
-    unsigned int s = 0;
-    for (long long i = lo + threadIdx.x; i < hi; i += kThreads) s += a[i];
-    unsigned int tot;
-    block_scan(s, s_w, &tot);
-    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) scan_partials_kernel(unsigned int* __restrict__ partial,
-                                                             int g, unsigned int capacity,
-                                                             ViewCounters* __restrict__ vc) {
-    __shared__ unsigned long long s[1024];
-    const unsigned long long v = threadIdx.x < (unsigned)g ? partial[threadIdx.x] : 0ull;
-    s[threadIdx.x] = v;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        const unsigned long long y = threadIdx.x >= (unsigned)off ? s[threadIdx.x - off] : 0ull;
-        __syncthreads();
-        s[threadIdx.x] += y;
-        __syncthreads();
+    unsigned long long run = s_w[warp] + x - sum;
+    for (int t = t0; t < t1; ++t) {
+        const unsigned int n = total[t];
+        tile_start[t] = (unsigned int)run;
+        run += n;
+        atomicAdd(&hist[1023u - min(n >> 3, 1023u)], 1u);
     }
-    if (threadIdx.x < (unsigned)g) partial[threadIdx.x] = (unsigned int)(s[threadIdx.x] - v);
-    if (threadIdx.x == 1023) {
-        const unsigned long long total = s[1023];
-        const bool over = total > capacity;
-        vc->n_instances = total > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned int)total;
+    if (tid == 1023) {  // run == grand total
+        const bool over = run > capacity;
+        vc->n_instances = run > 0xFFFFFFFFull ? 0xFFFFFFFFu : (unsigned int)run;
         vc->overflow = over ? 1u : 0u;
-        vc->n_valid = over ? 0u : (unsigned int)total;
+        vc->n_valid = over ? 0u : (unsigned int)run;
+        tile_start[ntiles] = over ? 0u : (unsigned int)run;
     }
+    __syncthreads();
+    const unsigned int v = hist[tid];
+    unsigned int hx = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, hx, o);
+        if (lane >= o) hx += y;
+    }
+    if (lane == 31) h_w[warp] = hx;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned int w = h_w[lane];
+        unsigned int z = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        h_w[lane] = z - w;
+    }
+    __syncthreads();
+    hist[tid] = h_w[warp] + hx - v;
+    __syncthreads();
+    for (int t = t0; t < t1; ++t)
+        order[atomicAdd(&hist[1023u - min(total[t] >> 3, 1023u)], 1u)] = (unsigned int)t;
 }
 
-__global__ void __launch_bounds__(kThreads) scan_apply_kernel(unsigned int* __restrict__ a,
-                                                              long long m, int g_blocks,
-                                                              const unsigned int* __restrict__ partial,
-                                                              int ntiles,
-                                                              unsigned int* __restrict__ tile_start,
-                                                              const ViewCounters* __restrict__ vc) {
-    __shared__ unsigned int s_w[kWarps];
-    const long long per = (m + gridDim.x - 1) / gridDim.x;
-    const long long lo = min(m, per * blockIdx.x), hi = min(m, lo + per);
-    // each thread scans a contiguous sub-segment
-    const long long sub = (hi - lo + kThreads - 1) / kThreads;
-    const long long s0 = min(hi, lo + sub * threadIdx.x), s1 = min(hi, s0 + sub);
-    unsigned int sum = 0;
-    for (long long i = s0; i < s1; ++i) sum += a[i];
-    unsigned int tot;
-    unsigned int run = partial[blockIdx.x] + block_scan(sum, s_w, &tot);
-    for (long long i = s0; i < s1; ++i) {
-        const unsigned int c = a[i];
-        a[i] = run;
-        if (i % g_blocks == 0) tile_start[i / g_blocks] = run;
-        run += c;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) tile_start[ntiles] = vc->n_valid;
-}
-
-// per-block: cursors from the scanned matrix, then shared-memory atomics place
-// every instance of the block's gid range
+// per-block: cursors = bucket start + the block's offset inside the bucket,
+// then shared-memory atomics place every instance of the block's gid range
 __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int ntiles, int tiles_x,
                                                             const ViewCounters* __restrict__ vc) {
     if (vc->overflow) return;
     extern __shared__ unsigned int s_cur[];
     for (int t = threadIdx.x; t < ntiles; t += kBinThreads)
-        s_cur[t] = b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
+        s_cur[t] = b.tile_start[t] + b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
     __syncthreads();
     const int shift = primary_shift(b.key_oa);
     const unsigned long long z = b.key_oa[1];
@@ -218,7 +238,6 @@ __global__ void splat_keys_kernel(int k, const double* __restrict__ mean2d,
 }  // namespace
 
 int bin_blocks(int num_sms) { return 2 * num_sms; }
-int bin_scan_blocks(int num_sms) { return 4 * num_sms; }
 
 cudaError_t bin_configure() {
     cudaError_t e = cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -230,13 +249,13 @@ cudaError_t bin_configure() {
 
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
                 cudaStream_t st) {
-    const int g = bin_blocks(num_sms), g2 = bin_scan_blocks(num_sms);
+    const int g = bin_blocks(num_sms);
     const size_t smem = sizeof(unsigned int) * (size_t)ntiles;
-    const long long m = (long long)ntiles * g;
     bin_count_kernel<<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x);
-    scan_reduce_kernel<<<g2, kThreads, 0, st>>>(b.count_bt, m, b.partial);
-    scan_partials_kernel<<<1, 1024, 0, st>>>(b.partial, g2, b.capacity, vc);
-    scan_apply_kernel<<<g2, kThreads, 0, st>>>(b.count_bt, m, g, b.partial, ntiles, b.tile_start, vc);
+    tile_scan_kernel<<<(ntiles + kWarps - 1) / kWarps, kThreads, 0, st>>>(b.count_bt, ntiles, g,
+                                                                         b.tile_total);
+    tile_start_kernel<<<1, 1024, 0, st>>>(b.tile_total, ntiles, b.capacity, vc, b.tile_start,
+                                          b.tile_order);
     bin_emit_kernel<<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, vc);
 }
 

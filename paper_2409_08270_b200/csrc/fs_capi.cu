@@ -71,9 +71,9 @@ struct Work {
     unsigned long long* inst = nullptr;      // per-tile buckets of instances -> sorted gids
     unsigned long long* scratch64 = nullptr; // 2 x capacity: long-bucket merge scratch
     unsigned int* count_bt = nullptr;        // ntiles x bin_blocks
-    unsigned int* partial = nullptr;         // bin_scan_blocks
+    unsigned int* tile_total = nullptr;      // bucket lengths
     unsigned int* tile_start = nullptr;
-    unsigned int* tile_order = nullptr;      // raster launch order (tile_order_kernel)
+    unsigned int* tile_order = nullptr;      // raster launch order (tile_start_kernel)
     ViewCounters* vc = nullptr;
     uint16_t* mask_dev = nullptr;
     uint16_t* pinned = nullptr;
@@ -189,7 +189,7 @@ void free_work(fs::Work& w) {
         if (p) cudaFree(p);
     };
     f(w.rect); f(w.r32); f(w.r64); f(w.k64); f(w.tie); f(w.inst); f(w.scratch64);
-    f(w.count_bt); f(w.partial); f(w.tile_start); f(w.tile_order); f(w.vc); f(w.mask_dev);
+    f(w.count_bt); f(w.tile_total); f(w.tile_start); f(w.tile_order); f(w.vc); f(w.mask_dev);
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
     if (w.done) cudaEventDestroy(w.done);
@@ -211,7 +211,6 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
     }
     if (!w.vc) {
         if ((rc = dev_alloc(&w.vc, 1))) return rc;
-        if ((rc = dev_alloc(&w.partial, (size_t)fs::bin_scan_blocks(ctx->num_sms)))) return rc;
     }
     if (inst > w.inst_cap) {
         if ((rc = dev_alloc(&w.inst, inst))) return rc;
@@ -221,6 +220,7 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
     if (ntiles > w.ntiles_cap) {
         if ((rc = dev_alloc(&w.tile_start, (size_t)ntiles + 1))) return rc;
         if ((rc = dev_alloc(&w.tile_order, (size_t)ntiles))) return rc;
+        if ((rc = dev_alloc(&w.tile_total, (size_t)ntiles))) return rc;
         if ((rc = dev_alloc(&w.count_bt, (size_t)ntiles * fs::bin_blocks(ctx->num_sms)))) return rc;
         w.ntiles_cap = ntiles;
     }
@@ -265,7 +265,8 @@ fs::BinBuffers bin_buffers(fs::Work& w, int n) {
     b.k64 = w.k64;
     b.key_oa = &w.vc->key_or;  // key_or, key_and are adjacent
     b.count_bt = w.count_bt;
-    b.partial = w.partial;
+    b.tile_total = w.tile_total;
+    b.tile_order = w.tile_order;
     b.tile_start = w.tile_start;
     b.inst = w.inst;
     b.capacity = w.inst_cap;
@@ -298,7 +299,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + 5 + 1 + 1 + 1 + 1; }
+int view_launches() { return 1 + 1 + 4 + 1 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,

@@ -50,16 +50,16 @@ struct BinBuffers {
     const unsigned long long* rect;     // per gid
     const unsigned long long* k64;      // per gid: order-preserving float64 depth key
     const unsigned long long* key_oa;   // {OR, AND} of the visible depth keys
-    unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets
-    unsigned int* partial;              // bin_scan_blocks() partial sums
+    unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets in the tile
+    unsigned int* tile_total;           // ntiles: bucket lengths
     unsigned int* tile_start;           // ntiles + 1
+    unsigned int* tile_order;           // ntiles: tiles by decreasing bucket length (raster launch order)
     unsigned long long* inst;           // capacity: instances; the tile sort leaves each
                                         // bucket's depth-ordered gids in sorted_view()
     unsigned int capacity;
 };
 constexpr int kMaxTiles = 49152;        // per-block tile histograms live in shared memory
 int bin_blocks(int num_sms);
-int bin_scan_blocks(int num_sms);
 cudaError_t bin_configure();
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
                 cudaStream_t st);
@@ -108,7 +108,7 @@ struct RasterArgs {
     const Rec64* r64;
     double* acc;                   // E x N float64 accumulator
     ViewCounters* vc;
-    unsigned int* tile_order;      // ntiles scratch: tiles by decreasing bucket length
+    const unsigned int* tile_order;  // ntiles: launch order (tile_start_kernel)
 };
 cudaError_t raster_configure();
 void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, int num_sms,

@@ -302,48 +302,6 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     }
 }
 
-// Launch order of the raster CTAs: tiles by decreasing bucket length (a
-// counting sort on length / 8, one CTA), so the long tiles start in the first
-// wave and the short ones fill the tail.
-__global__ void __launch_bounds__(1024) tile_order_kernel(const unsigned int* __restrict__ tile_start,
-                                                          int ntiles, unsigned int* __restrict__ order) {
-    __shared__ unsigned int hist[1024];
-    __shared__ unsigned int wsum[32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    hist[tid] = 0;
-    __syncthreads();
-    for (int t = tid; t < ntiles; t += 1024) {
-        const unsigned int n = tile_start[t + 1] - tile_start[t];
-        atomicAdd(&hist[1023u - min(n >> 3, 1023u)], 1u);
-    }
-    __syncthreads();
-    const unsigned int v = hist[tid];
-    unsigned int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        unsigned int w = wsum[lane], z = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned int y = __shfl_up_sync(0xffffffffu, z, o);
-            if (lane >= o) z += y;
-        }
-        wsum[lane] = z - w;
-    }
-    __syncthreads();
-    hist[tid] = wsum[warp] + x - v;
-    __syncthreads();
-    for (int t = tid; t < ntiles; t += 1024) {
-        const unsigned int n = tile_start[t + 1] - tile_start[t];
-        order[atomicAdd(&hist[1023u - min(n >> 3, 1023u)], 1u)] = (unsigned int)t;
-    }
-}
-
 // Largest label of a view's mask (contributions.py:108-114 is checked by the
 // host from this value; empty tiles are not visited by the raster kernel).
 __global__ void mask_check_kernel(const uint16_t* __restrict__ mask, long long count,
@@ -376,7 +334,6 @@ cudaError_t raster_configure() {
 
 void launch_raster(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
-    tile_order_kernel<<<1, 1024, 0, st>>>(a.sort.tile_start, a.ntiles, a.tile_order);
     raster_kernel<<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
 }
 
