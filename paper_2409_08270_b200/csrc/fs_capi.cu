@@ -299,7 +299,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + 4 + 1 + 1 + 1; }
+int view_launches() { return 1 + 1 + 4 + 1 + 1; }
 
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
@@ -324,7 +324,6 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.acc = acc;
     ra.vc = w.vc;
     ra.tile_order = w.tile_order;
-    fs::launch_mask_check(mask, (long long)cam.width * cam.height, w.vc, ctx->num_sms, w.stream);
     fs::launch_raster(ra, w.stream);
     if (ev) cudaEventRecord(ev[3], w.stream);
     if (log) fs::view_end_kernel<<<1, 32, 0, w.stream>>>(w.vc, log);

@@ -51,7 +51,7 @@ struct ViewCounters {
     unsigned int n_instances;    // (tile, gaussian) pairs emitted
     unsigned int n_valid;        // n_instances, or 0 when it overflowed the buffers
     unsigned int overflow;       // instances exceeded capacity -> view skipped
-    unsigned int max_label;      // largest mask label seen by the raster kernel
+    unsigned int max_label;      // largest out-of-range mask label (>= E) seen by the raster kernel, else 0
     unsigned long long tile_steps;   // list entries walked by the raster kernel
     unsigned long long exact_evals;  // float64 alpha evaluations
     unsigned long long atomics;      // global accumulator atomics issued

@@ -111,8 +111,6 @@ struct RasterArgs {
     const unsigned int* tile_order;  // ntiles: launch order (tile_start_kernel)
 };
 cudaError_t raster_configure();
-void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, int num_sms,
-                       cudaStream_t st);
 void launch_raster(const RasterArgs& a, cudaStream_t st);
 
 // ---- fs_assign.cu ----

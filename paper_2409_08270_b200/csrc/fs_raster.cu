@@ -98,6 +98,17 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const ViewCounters* vc = a.vc;
     if (vc->overflow) return;
     const int tile = (int)a.tile_order[blockIdx.x];  // longest buckets first
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int x0 = (tile % a.tiles_x) * kTile, y0 = (tile / a.tiles_x) * kTile;
+    const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
+    const bool inside = px < a.width && py < a.height;
+    const unsigned int label = inside ? a.mask[(size_t)py * a.width + px] : 0u;
+    {
+        // label range check of every pixel, empty tiles included
+        // (contributions.py:108-114; the host reports the first bad view)
+        const unsigned int m = __reduce_max_sync(0xffffffffu, label);
+        if (lane == 0 && m >= (unsigned)a.num_objects) atomicMax(&a.vc->max_label, m);
+    }
     const unsigned int begin = a.sort.tile_start[tile], end = a.sort.tile_start[tile + 1];
     if (begin >= end) return;
     const unsigned int n_list = end - begin;
@@ -114,13 +125,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     sort_tile_list(a.sort.inst + begin, sorted, a.sort.scratch64 + 2ull * begin, n_list, a.sort.keys,
                    SH.sort, a.sort.cap);
     const unsigned int* __restrict__ list = sorted;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     WarpSmem& W = S.w[warp];
     const unsigned int lt_mask = (1u << lane) - 1u;
-    const int x0 = (tile % a.tiles_x) * kTile, y0 = (tile / a.tiles_x) * kTile;
-    const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
-    const bool inside = px < a.width && py < a.height;
-    const unsigned int label = inside ? a.mask[(size_t)py * a.width + px] : 0u;
     // the warp's pixel-centre strip
     const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
     const float v_lo = (float)(y0 + 2 * warp) + 0.5f, v_hi = v_lo + 1.0f;
@@ -129,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
     const unsigned int lbl0 = __shfl_sync(0xffffffffu, label, first);
     const bool uniform = __all_sync(0xffffffffu, !inside || label == lbl0);
-    // out-of-range labels (reported by mask_check_kernel) never address the accumulator
+    // out-of-range labels (reported through max_label) never address the accumulator
     const bool lbl_ok = label < (unsigned)a.num_objects;
     const bool lbl0_ok = lbl0 < (unsigned)a.num_objects;
 
@@ -302,27 +308,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     }
 }
 
-// Largest label of a view's mask (contributions.py:108-114 is checked by the
-// host from this value; empty tiles are not visited by the raster kernel).
-__global__ void mask_check_kernel(const uint16_t* __restrict__ mask, long long count,
-                                  ViewCounters* __restrict__ vc) {
-    unsigned int m = 0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (long long)gridDim.x * blockDim.x)
-        m = max(m, (unsigned int)mask[i]);
-    m = __reduce_max_sync(0xffffffffu, m);
-    if ((threadIdx.x & 31) == 0 && m) atomicMax(&vc->max_label, m);
-}
-
 }  // namespace
-
-void launch_mask_check(const uint16_t* mask, long long count, ViewCounters* vc, int num_sms,
-                       cudaStream_t st) {
-    if (count <= 0) return;
-    long long blocks = (count + 255) / 256;
-    if (blocks > num_sms * 4) blocks = num_sms * 4;
-    mask_check_kernel<<<(int)blocks, 256, 0, st>>>(mask, count, vc);
-}
 
 // Per device (called by fs_create after cudaSetDevice).
 cudaError_t raster_configure() {
