@@ -13,8 +13,10 @@ Two halves:
 
 * ``fs_oracle.c`` (built by ``oracle/Makefile`` into ``oracle/build/liborc.so``):
   float64 restatement of projection (scene.py:228-312), binning
-  (rasterizer.py:72-130) and the blending walk / accumulation
-  (contributions.py:90-160), view-parallel with an ordered f64 merge.
+  (rasterizer.py:72-130), the blending walk / accumulation
+  (contributions.py:90-160, view-parallel with an ordered f64 merge) and
+  novel-view compositing (rasterizer.py:133-203; ``render_view`` /
+  ``render_mask`` below follow rasterizer.py:206-234 and maskrender.py:45-95).
 * ``one_vs_rest_wins`` / ``assign_binary`` / ``assign_scene`` below: numpy
   restatement of the float32 op sequence of solver.py:111-172.
 """
@@ -72,6 +74,9 @@ def lib() -> ctypes.CDLL:
         L.orc_accumulate.argtypes = [ctypes.c_int64, P, P, P, P, ctypes.c_int, P, P, ctypes.c_int,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_int, P]
         L.orc_accumulate.restype = ctypes.c_int
+        L.orc_render.argtypes = [ctypes.c_int64, P, P, P, P, P, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_int, P, P, ctypes.c_double, ctypes.c_double, P, P, P]
+        L.orc_render.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -177,6 +182,68 @@ def accumulate(means, quats, scales, opac, cams, masks, num_objects,
                          ctypes.addressof(cam_arr), ctypes.addressof(mptrs), int(num_objects),
                          float(alpha_floor), float(t_floor), int(threads), _ptr(total))
     return total.astype(np.float32) if as_float32 else total
+
+
+def render_splats(mean2d, conic, depth, opac, channel, width, height, offsets, items,
+                  alpha_floor=1.0 / 255.0, t_floor=1e-4):
+    """render_property (rasterizer.py:133-203) over a binning given as CSR.
+
+    Splat arrays (and ``opac`` / ``channel``, already gathered per splat) are
+    indexed by ``items``.  Returns (value | None, alpha, depth).
+    """
+    mean2d = np.ascontiguousarray(mean2d, dtype=np.float64).reshape(-1, 2)
+    k = mean2d.shape[0]
+    conic = np.ascontiguousarray(conic, dtype=np.float64).reshape(k, 3)
+    depth = np.ascontiguousarray(depth, dtype=np.float64).reshape(k)
+    opac = np.ascontiguousarray(opac, dtype=np.float64).reshape(k)
+    channels = 0
+    ch = np.zeros(1)
+    if channel is not None:
+        ch = np.ascontiguousarray(channel, dtype=np.float64)
+        channels = 1 if ch.ndim == 1 else ch.shape[1]
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    items = np.ascontiguousarray(items, dtype=np.int64)
+    if items.size == 0:
+        items = np.zeros(1, np.int64)
+    rho = np.zeros((height, width))
+    dep = np.zeros((height, width))
+    value = np.zeros((height, width, channels) if channels > 1 else (height, width)) \
+        if channels else np.zeros(1)
+    lib().orc_render(k, _ptr(mean2d), _ptr(conic), _ptr(depth), _ptr(opac), _ptr(ch), channels,
+                     int(width), int(height), _ptr(offsets), _ptr(items), float(alpha_floor),
+                     float(t_floor), _ptr(value), _ptr(rho), _ptr(dep))
+    return (value if channels else None), rho, dep
+
+
+def render_view(means, quats, scales, opac, cam: OrcCamera, channel=None, member=None,
+                alpha_floor=1.0 / 255.0, t_floor=1e-4):
+    """render_view / render_subset_alpha_depth (rasterizer.py:206-234):
+    project (scene.py:252-312), bin (rasterizer.py:72-100) and composite."""
+    means, quats, scales, opac = _scene_arrays(means, quats, scales, opac)
+    alive, mean2d, conic, depth, radius, _ = project(means, quats, scales, cam)
+    if member is not None:
+        alive = alive & np.asarray(member, dtype=bool)
+    offs, items = bin_tiles(alive, mean2d, depth, radius, cam.width, cam.height)
+    return render_splats(mean2d, conic, depth, opac, channel, cam.width, cam.height, offs, items,
+                         alpha_floor, t_floor)
+
+
+def render_mask(means, quats, scales, opac, cam: OrcCamera, membership, tau,
+                alpha_floor=1.0 / 255.0, t_floor=1e-4):
+    """render_scene_mask (maskrender.py:69-95); render_binary_mask is the E = 2 case
+    with membership [~fg, fg] (maskrender.py:45-66).  uint16 H x W labels."""
+    membership = np.asarray(membership).astype(bool)
+    labels = np.zeros((cam.height, cam.width), np.uint16)
+    best = np.full((cam.height, cam.width), np.inf)
+    for obj in range(1, membership.shape[0]):
+        if not membership[obj].any():
+            continue
+        _, rho, dep = render_view(means, quats, scales, opac, cam, None, membership[obj],
+                                  alpha_floor, t_floor)
+        wins = (rho > tau) & (dep < best)
+        labels[wins] = obj
+        best[wins] = dep[wins]
+    return labels
 
 
 # ---------------------------------------------------------------------------

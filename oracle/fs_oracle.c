@@ -25,6 +25,7 @@
  *   _tile_pixel_grid        rasterizer.py:123-130
  *   _accumulate_view        contributions.py:119-160
  *   accumulate_contributions contributions.py:90-116 (f64 partials summed in view order)
+ *   render_property          rasterizer.py:133-203 (per-pixel compositing of a binning)
  */
 #include <math.h>
 #include <pthread.h>
@@ -443,5 +444,78 @@ int orc_accumulate(int64_t n, const double *means, const double *quats, const do
     free(th);
     pthread_mutex_destroy(&job.mu);
     pthread_cond_destroy(&job.cv);
+    return 0;
+}
+
+/* ---- render_property (rasterizer.py:133-203) ----
+ * Splat arrays are indexed by the CSR items (positions into them); opac and
+ * channel are per splat (the caller gathers scene.opacities[indices] and
+ * channel[indices]).  channels: 0 (no value), 1 (scalar) or 3 (vector).
+ * value (H*W*channels), rho and depth_out (H*W) are overwritten.  Per pixel,
+ * every sum runs in list order exactly as the numpy tile arrays accumulate. */
+int orc_render(int64_t k, const double *mean2d, const double *conic, const double *depth,
+               const double *opac, const double *channel, int channels, int W, int H,
+               const int64_t *offs, const int64_t *items, double alpha_floor, double t_floor,
+               double *value, double *rho, double *depth_out) {
+    (void)k;
+    const size_t px = (size_t)W * (size_t)H;
+    memset(rho, 0, sizeof(double) * px);
+    memset(depth_out, 0, sizeof(double) * px);
+    if (channels > 0) memset(value, 0, sizeof(double) * px * (size_t)channels);
+    int tx_n = (W + ORC_TILE - 1) / ORC_TILE, ty_n = (H + ORC_TILE - 1) / ORC_TILE;
+    double trans[ORC_TILE * ORC_TILE], racc[ORC_TILE * ORC_TILE], dacc[ORC_TILE * ORC_TILE];
+    double vacc[ORC_TILE * ORC_TILE * 3];
+    uint8_t act[ORC_TILE * ORC_TILE];
+    for (int ty = 0; ty < ty_n; ++ty) {
+        for (int tx = 0; tx < tx_n; ++tx) {
+            int64_t t = (int64_t)ty * tx_n + tx;
+            int64_t beg = offs[t], end = offs[t + 1];
+            if (beg == end) continue; /* :163-164 */
+            int x0 = tx * ORC_TILE, y0 = ty * ORC_TILE;
+            int x1 = x0 + ORC_TILE < W ? x0 + ORC_TILE : W;
+            int y1 = y0 + ORC_TILE < H ? y0 + ORC_TILE : H;
+            int tw = x1 - x0, th = y1 - y0, np_ = tw * th;
+            for (int p = 0; p < np_; ++p) {
+                trans[p] = 1.0;
+                act[p] = 1;
+                racc[p] = 0.0;
+                dacc[p] = 0.0;
+                for (int c = 0; c < channels; ++c) vacc[p * 3 + c] = 0.0;
+            }
+            int n_active = np_;
+            for (int64_t s = beg; s < end; ++s) {
+                int64_t g = items[s];
+                double mx = mean2d[2 * g], my = mean2d[2 * g + 1];
+                double a = conic[3 * g], b = conic[3 * g + 1], c = conic[3 * g + 2];
+                double o = opac[g], z = depth[g];
+                for (int p = 0; p < np_; ++p) {
+                    if (!act[p]) continue; /* use == False: weight 0 (adds nothing) */
+                    double du = ((double)(x0 + p % tw) + 0.5) - mx;
+                    double dv = ((double)(y0 + p / tw) + 0.5) - my;
+                    double power = -0.5 * (a * du * du + c * dv * dv) - b * du * dv; /* :178 */
+                    double alpha = o * exp(power);
+                    if (alpha > ORC_ALPHA_CLAMP) alpha = ORC_ALPHA_CLAMP; /* :179-180 */
+                    if (alpha_floor > 0.0 && !(alpha >= alpha_floor)) continue; /* :181-182 */
+                    double w = alpha * trans[p];                                 /* :183 */
+                    for (int ch = 0; ch < channels; ++ch)                        /* :184-189 */
+                        vacc[p * 3 + ch] += w * channel[(size_t)g * channels + ch];
+                    racc[p] += w;                                                /* :190 */
+                    dacc[p] += z * w;                                            /* :191 */
+                    trans[p] = trans[p] * (1.0 - alpha);                         /* :192 */
+                    if (t_floor > 0.0 && !(trans[p] >= t_floor)) {               /* :193-194 */
+                        act[p] = 0;
+                        --n_active;
+                    }
+                }
+                if (t_floor > 0.0 && n_active == 0) break; /* :195-196 */
+            }
+            for (int p = 0; p < np_; ++p) {
+                size_t at = (size_t)(y0 + p / tw) * (size_t)W + (size_t)(x0 + p % tw);
+                rho[at] = racc[p];
+                depth_out[at] = racc[p] > 0.0 ? dacc[p] / racc[p] : 0.0; /* :202-203 */
+                for (int ch = 0; ch < channels; ++ch) value[at * channels + ch] = vacc[p * 3 + ch];
+            }
+        }
+    }
     return 0;
 }

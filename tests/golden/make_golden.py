@@ -6,8 +6,9 @@ Run in the build container (the only place /root/reference exists):
 
 It imports ``splatlift`` from /root/reference/pkg/src, runs the reference's
 own projection (scene.py:252-312), binning (rasterizer.py:72-100),
-accumulation (contributions.py:90-160) and assignment (solver.py:111-172) on
-seeded inputs, and writes small ``.npz`` files next to this script.  Nothing
+accumulation (contributions.py:90-160), assignment (solver.py:111-172) and
+novel-view rendering (rasterizer.py:133-234, maskrender.py:45-95) on seeded
+inputs, and writes small ``.npz`` files next to this script.  Nothing
 at test time reads /root/reference; the GPU box only sees these files.
 
 Inputs of reference-generated fixtures are stored verbatim.  Inputs of the
@@ -248,6 +249,97 @@ def gen_assign(acc_cases):
     return cases
 
 
+# ---------------------------------------------------------------- rendering
+def render_case(scene, view, channel, blend, member=None):
+    """render_view / render_subset_alpha_depth (rasterizer.py:133-234) on one view."""
+    if member is None:
+        out = ref.render_view(scene, view, channel, blend)
+    else:
+        out = ref.render_subset_alpha_depth(scene, view, member, blend)
+    c = dict(**{f"in_{a}": v for a, v in scene_arrays(scene).items()}, cam=cam_row(view),
+             floors=np.array([blend.alpha_floor, blend.transmittance_floor]),
+             alpha=out.alpha, depth=out.depth)
+    if channel is not None:
+        c["channel"] = np.asarray(channel, np.float64)
+        c["value"] = out.value
+    if member is not None:
+        c["member"] = np.asarray(member, np.uint8)
+    return c
+
+
+def mask_case(scene, view, labels_or_membership, mode, tau):
+    """render_binary_mask / render_scene_mask (maskrender.py:45-95)."""
+    if mode == "binary":
+        asn = ref.Assignment(mode="binary", gamma=0.0,
+                             labels=np.asarray(labels_or_membership, np.uint8))
+        out = ref.render_binary_mask(scene, asn, view, tau)
+    else:
+        asn = ref.Assignment(mode="scene", gamma=0.0,
+                             membership=np.asarray(labels_or_membership, np.uint8))
+        out = ref.render_scene_mask(scene, asn, view, tau)
+    return dict(**{f"in_{a}": v for a, v in scene_arrays(scene).items()}, cam=cam_row(view),
+                assignment=np.asarray(labels_or_membership, np.uint8),
+                mode=np.frombuffer(mode.encode(), np.uint8), tau=np.float64(tau),
+                labels=out.labels)
+
+
+def iso(center, sigma, opacity):
+    # reference tests/conftest.py:28-36
+    return ref.Gaussian(center=np.asarray(center, np.float64), rotation=(1.0, 0.0, 0.0, 0.0),
+                        scale=np.full(3, sigma), opacity=opacity)
+
+
+def gen_render():
+    D, X = ref.DEFAULT_BLEND, ref.EXACT_BLEND
+    cases = {}
+    v16 = frontal_view()
+    # test_rasterizer.py:82-97 known answers
+    cases["single"] = render_case(ref.GaussianScene.from_gaussians([iso((0, 0, 2.0), 0.02, 0.6)]),
+                                  v16, np.array([1.0]), D)
+    cases["two"] = render_case(ref.GaussianScene.from_gaussians(
+        [iso((0, 0, 2.0), 0.02, 0.5), iso((0, 0, 4.0), 0.04, 0.5)]), v16, np.array([1.0, 0.0]), D)
+    rng = np.random.default_rng(20240811)
+    v32 = frontal_view(32, 32, 40.0)
+    sc = random_scene(rng, 30)
+    ch = rng.random(30)
+    cases["rand_exact"] = render_case(sc, v32, ch, X)
+    cases["rand_default"] = render_case(sc, v32, ch, D)
+    cases["rand_nochannel"] = render_case(sc, v32, None, D)
+    sc = random_scene(rng, 20)
+    cases["rand_vector"] = render_case(sc, v32, rng.random((20, 3)), D)
+    sc = random_scene(rng, 25)
+    cases["subset"] = render_case(sc, v32, None, D, member=rng.random(25) < 0.5)
+    cases["subset_empty"] = render_case(sc, v32, None, D, member=np.zeros(25, bool))
+    # occluder in front must not dim the subset (test_rasterizer.py:183-191)
+    sc = ref.GaussianScene.from_gaussians([iso((0, 0, 1.0), 0.02, 0.95), iso((0, 0, 3.0), 0.06, 0.7)])
+    cases["subset_local"] = render_case(sc, v16, None, D, member=np.array([False, True]))
+    # a denser synthetic view, ragged edge tiles, both blends
+    fx = ref_synth.make_random(seed=77, n_gaussians=400, n_views=1, width=100, height=70,
+                               num_objects=2)
+    vw = fx.views[0]
+    ch = np.random.default_rng(3).random(len(fx.scene))
+    cases["synth_default"] = render_case(fx.scene, vw, ch, D)
+    cases["synth_exact"] = render_case(fx.scene, vw, ch, X)
+    # novel-view masks (test_maskrender.py)
+    fx = ref_synth.make_two_cluster(seed=3, n_gaussians=600, n_views=8, width=96, height=96,
+                                    n_mask_views=4)
+    novel = fx.view(fx.heldout_view_ids()[0])
+    fg = (fx.membership == 1).astype(np.uint8)
+    for tau in (0.1, 0.5):
+        cases[f"binary_tau{int(tau * 10)}"] = mask_case(fx.scene, novel, fg, "binary", tau)
+    rng = np.random.default_rng(99)
+    sc = random_scene(rng, 40)
+    memb = np.zeros((4, 40), np.uint8)
+    obj = rng.integers(1, 4, size=40)
+    memb[obj, np.arange(40)] = 1
+    memb[0] = 1 - memb[1:].max(axis=0)
+    cases["scene3"] = mask_case(sc, v32, memb, "scene", 0.1)
+    sc = ref.GaussianScene.from_gaussians([iso((0, 0, 2.0), 0.08, 0.9), iso((0, 0, 2.0), 0.08, 0.9)])
+    cases["scene_tie"] = mask_case(sc, frontal_view(16, 16, 24.0),
+                                   np.array([[0, 0], [1, 0], [0, 1]]), "scene", 0.1)
+    return cases
+
+
 def save(name, cases):
     flat = {}
     for case, arrays in cases.items():
@@ -258,7 +350,11 @@ def save(name, cases):
     print(f"wrote {path} ({path.stat().st_size / 1e6:.2f} MB, {len(cases)} cases)")
 
 
-def main():
+def main(which=None):
+    if which in (None, "render"):
+        save("render", gen_render())
+    if which == "render":
+        return
     save("projection", gen_projection())
     save("binning", gen_binning())
     acc = gen_accumulate()
@@ -267,4 +363,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1] if len(sys.argv) > 1 else None)
