@@ -137,6 +137,38 @@ int fs_finalize(fs_context *ctx, const double *acc, int64_t count, float *out, i
 int fs_assign(fs_context *ctx, const float *A, int64_t n, int num_objects, float gamma, int mode,
               uint8_t *out, int on_device);
 
+/* ---- novel-view rendering ---- */
+
+/* render_view / render_subset_alpha_depth (rasterizer.py:206-234) over the
+ * resident scene: project (members only when member != NULL, N bytes,
+ * scene.py:346-350), bin, and composite front to back per pixel
+ * (render_property, rasterizer.py:133-203).  Host outputs: alpha and depth
+ * H x W float64 (depth = blended depth / alpha, 0 where alpha == 0); with
+ * channels 1 or 3, channel is N x channels float64 and value H x W x channels. */
+int fs_render(fs_context *ctx, const fs_camera *cam, const uint8_t *member, double alpha_floor,
+              double transmittance_floor, const double *channel, int channels, double *value,
+              double *alpha, double *depth);
+
+/* render_property (rasterizer.py:133-203) over a caller's TileBinning: k
+ * splats (mean2d k x 2, conic k x 3 = inv_cov (a, b, c), depth, opacity =
+ * scene.opacities[indices], channel k x channels gathered the same way) and
+ * per-tile lists as CSR (tile_offsets[ntiles + 1], items = splat positions in
+ * the order the lists are walked). */
+int fs_render_splats(fs_context *ctx, int width, int height, int64_t k, const double *mean2d,
+                     const double *conic, const double *depth, const double *opacity,
+                     const int64_t *tile_offsets, const int64_t *items, double alpha_floor,
+                     double transmittance_floor, const double *channel, int channels,
+                     double *value, double *alpha, double *depth_out);
+
+/* render_scene_mask (maskrender.py:69-95) -- and render_binary_mask
+ * (maskrender.py:45-66) as num_objects = 2 with rows (~fg, fg): membership is
+ * num_objects x N uint8; every non-empty object 1.. is rendered as a subset
+ * and a pixel takes the object whose alpha exceeds tau with the smallest
+ * blended depth (ties: smaller id).  labels: H x W uint16 (host). */
+int fs_render_mask(fs_context *ctx, const fs_camera *cam, const uint8_t *membership,
+                   int num_objects, double tau, double alpha_floor, double transmittance_floor,
+                   uint16_t *labels);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,7 +5,11 @@ Drop-in for the reference package's solver path (``splatlift``):
 * ``accumulate_contributions`` (reference ``contributions.py:90``)
 * ``assign_binary`` / ``assign_scene`` (reference ``solver.py:140,156``)
 * the stage functions they are built from -- ``project_scene``,
-  ``bin_gaussians_to_tiles`` -- and the input / output types.
+  ``bin_gaussians_to_tiles`` -- and the input / output types;
+* novel-view rendering on the same kernels: ``render_property`` /
+  ``render_view`` / ``render_subset_alpha_depth`` (reference
+  ``rasterizer.py:133-234``) and ``render_binary_mask`` /
+  ``render_scene_mask`` (reference ``maskrender.py``).
 
 All compute runs in hand-written sm_100a CUDA kernels
 (``csrc/`` -> ``_lib/libflashsplat_b200.so``) behind the C ABI of
@@ -15,13 +19,20 @@ All compute runs in hand-written sm_100a CUDA kernels
 """
 
 from .contributions import ContributionMatrix, LabelMask, accumulate_contributions
+from .maskrender import DEFAULT_TAU, RenderedMask, render_binary_mask, render_scene_mask
 from .rasterizer import (
     DEFAULT_BLEND,
     EXACT_BLEND,
     TILE_SIZE,
     BlendConfig,
+    RenderOutput,
     TileBinning,
     bin_gaussians_to_tiles,
+    load_render_grid,
+    render_property,
+    render_subset_alpha_depth,
+    render_view,
+    save_render_grid,
     tile_range,
 )
 from .scene import (
@@ -45,9 +56,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Assignment", "BlendConfig", "CameraView", "ContributionMatrix", "DEFAULT_BLEND",
-    "EXACT_BLEND", "Gaussian", "GaussianScene", "LabelMask", "LabelSolver", "ProjectedGaussian",
-    "ProjectionStats", "SceneDataError", "SceneFormatError", "TILE_SIZE", "TileBinning",
-    "accumulate_contributions", "assign_binary", "assign_scene", "bin_gaussians_to_tiles",
-    "evaluate_alpha", "load_cameras", "project_gaussian", "project_scene", "save_cameras",
-    "solve", "tile_range",
+    "DEFAULT_TAU", "EXACT_BLEND", "Gaussian", "GaussianScene", "LabelMask", "LabelSolver",
+    "ProjectedGaussian", "ProjectionStats", "RenderOutput", "RenderedMask", "SceneDataError",
+    "SceneFormatError", "TILE_SIZE", "TileBinning", "accumulate_contributions", "assign_binary",
+    "assign_scene", "bin_gaussians_to_tiles", "evaluate_alpha", "load_cameras",
+    "load_render_grid", "project_gaussian", "project_scene", "render_binary_mask",
+    "render_property", "render_scene_mask", "render_subset_alpha_depth", "render_view",
+    "save_cameras", "save_render_grid", "solve", "tile_range",
 ]

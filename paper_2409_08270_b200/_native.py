@@ -25,7 +25,7 @@ EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
     "fs_copy_to_host", "fs_synchronize", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
-    "fs_accumulate", "fs_finalize", "fs_assign",
+    "fs_accumulate", "fs_finalize", "fs_assign", "fs_render", "fs_render_splats", "fs_render_mask",
 )
 
 
@@ -102,6 +102,9 @@ def load() -> ctypes.CDLL:
             "fs_accumulate": ([P, I, P, P, I, I, D, D, P, P], I),
             "fs_finalize": ([P, P, I64, P, I], I),
             "fs_assign": ([P, P, I64, I, F, I, P, I], I),
+            "fs_render": ([P, P, P, D, D, P, I, P, P, P], I),
+            "fs_render_splats": ([P, I, I, I64, P, P, P, P, P, P, D, D, P, I, P, P, P], I),
+            "fs_render_mask": ([P, P, P, I, D, D, D, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -136,8 +139,8 @@ def camera_struct(view) -> FsCamera:
     return c
 
 
-def _p(a: np.ndarray) -> int:
-    return a.ctypes.data
+def _p(a) -> int:
+    return None if a is None else a.ctypes.data
 
 
 class DeviceBuffer:
@@ -249,6 +252,33 @@ class Context:
                                  _p(conic), _p(depth), _p(radius), ctypes.byref(st)))
         stats = (st.n_input, st.n_emitted, st.n_behind, st.n_degenerate, st.n_offscreen)
         return alive.astype(bool), mean2d, conic, depth, radius, stats
+
+    def render(self, view, member, alpha_floor: float, t_floor: float, channel=None):
+        """fs_render over the resident scene: (value | None, alpha, depth)."""
+        h, w = view.height, view.width
+        alpha = np.zeros((h, w))
+        depth = np.zeros((h, w))
+        channels, value, ch = 0, None, None
+        if channel is not None:
+            ch = np.ascontiguousarray(channel, dtype=np.float64)
+            channels = 1 if ch.ndim == 1 else ch.shape[1]
+            value = np.zeros((h, w) if channels == 1 else (h, w, channels))
+        mem = None if member is None else np.ascontiguousarray(member, dtype=np.uint8)
+        cam = camera_struct(view)
+        _check(load().fs_render(self.handle, ctypes.byref(cam), _p(mem), float(alpha_floor),
+                                float(t_floor), _p(ch), channels, _p(value), _p(alpha),
+                                _p(depth)))
+        return value, alpha, depth
+
+    def render_mask(self, view, membership, tau: float, alpha_floor: float, t_floor: float):
+        """fs_render_mask: H x W uint16 labels (membership: E x N)."""
+        membership = np.ascontiguousarray(membership, dtype=np.uint8)
+        labels = np.zeros((view.height, view.width), np.uint16)
+        cam = camera_struct(view)
+        _check(load().fs_render_mask(self.handle, ctypes.byref(cam), _p(membership),
+                                     int(membership.shape[0]), float(tau), float(alpha_floor),
+                                     float(t_floor), _p(labels)))
+        return labels
 
     def bin(self, view):
         cam = camera_struct(view)
@@ -370,6 +400,32 @@ def bin_splats(mean2d, depth, radius, index, width: int, height: int, device: in
                                int(width), int(height), _p(offs), _p(items), items.size,
                                ctypes.byref(count)))
     return offs, items[:count.value]
+
+
+def render_splats(width: int, height: int, mean2d, conic, depth, opacity, offsets, items,
+                  alpha_floor: float, t_floor: float, channel=None, device: int = None):
+    """fs_render_splats: composite a caller's binning -> (value | None, alpha, depth)."""
+    ctx = context(device)
+    mean2d = np.ascontiguousarray(mean2d, dtype=np.float64).reshape(-1, 2)
+    k = mean2d.shape[0]
+    conic = np.ascontiguousarray(conic, dtype=np.float64).reshape(k, 3)
+    depth = np.ascontiguousarray(depth, dtype=np.float64).reshape(k)
+    opacity = np.ascontiguousarray(opacity, dtype=np.float64).reshape(k)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    items = np.ascontiguousarray(items, dtype=np.int64)
+    alpha = np.zeros((height, width))
+    dep = np.zeros((height, width))
+    channels, value, ch = 0, None, None
+    if channel is not None:
+        ch = np.ascontiguousarray(channel, dtype=np.float64)
+        channels = 1 if ch.ndim == 1 else ch.shape[1]
+        value = np.zeros((height, width) if channels == 1 else (height, width, channels))
+    with ctx.lock:
+        _check(load().fs_render_splats(ctx.handle, int(width), int(height), k, _p(mean2d),
+                                       _p(conic), _p(depth), _p(opacity), _p(offsets), _p(items),
+                                       float(alpha_floor), float(t_floor), _p(ch), channels,
+                                       _p(value), _p(alpha), _p(dep)))
+    return value, alpha, dep
 
 
 def project(means, quats, scales, view, device: int = None):

@@ -112,6 +112,17 @@ struct fs_context {
     float* asg_in = nullptr;      // fs_assign with host buffers
     uint8_t* asg_out = nullptr;
     size_t asg_in_cap = 0, asg_out_cap = 0;
+    // novel-view rendering (fs_render*): outputs, inputs, mask combine
+    double* rn_f64 = nullptr;     // alpha | depth | value (H*W*(2 + C))
+    size_t rn_f64_cap = 0;
+    double* rn_in = nullptr;      // channel (N x C) or splat arrays
+    size_t rn_in_cap = 0;
+    uint8_t* rn_member = nullptr;
+    size_t rn_member_cap = 0;
+    unsigned int* rn_u32 = nullptr;  // caller's tile lists, launch order
+    size_t rn_u32_cap = 0;
+    uint16_t* rn_labels = nullptr;
+    size_t rn_labels_cap = 0;
 };
 
 
@@ -308,7 +319,7 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr);
     if (ev) cudaEventRecord(ev[2], w.stream);
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
-    fs::RasterArgs ra;
+    fs::RasterArgs ra{};
     ra.width = cam.width;
     ra.height = cam.height;
     ra.tiles_x = tx;
@@ -411,7 +422,9 @@ void fs_destroy(fs_context* ctx) {
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
                     (void*)ctx->opac, (void*)ctx->tile_oa_table, (void*)ctx->view_log,
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
-                    (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out})
+                    (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out,
+                    (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
+                    (void*)ctx->rn_u32, (void*)ctx->rn_labels})
         if (p) cudaFree(p);
     for (int k = 0; k < 2; ++k) {
         if (ctx->pinned_up[k]) cudaFreeHost(ctx->pinned_up[k]);
@@ -857,6 +870,246 @@ int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float
         if (tmpO) CK(cudaFreeAsync(tmpO, st));
     }
     CK(cudaStreamSynchronize(st));
+    return FS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- rendering
+namespace {
+
+fs::RasterArgs render_args(fs::Work& w, int width, int height, double alpha_floor,
+                           double t_floor, double* out, int channels, const double* ch_dev) {
+    const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
+    const size_t px = (size_t)width * height;
+    fs::RasterArgs ra{};
+    ra.width = width;
+    ra.height = height;
+    ra.tiles_x = tx;
+    ra.ntiles = ntiles;
+    ra.num_objects = 1;
+    ra.af_eff = alpha_floor > 0.0 ? alpha_floor : -1.0;  // rasterizer.py:181-182
+    ra.tf_eff = t_floor > 0.0 ? t_floor : -1.0;          // rasterizer.py:193-194
+    ra.sort = tile_sort_args(w);
+    ra.r32 = w.r32;
+    ra.r64 = w.r64;
+    ra.vc = w.vc;
+    ra.tile_order = w.tile_order;
+    ra.render.alpha = out;
+    ra.render.depth = out + px;
+    ra.render.value = channels ? out + 2 * px : nullptr;
+    ra.render.channel = ch_dev;
+    ra.render.channels = channels;
+    return ra;
+}
+
+// render_view / render_subset_alpha_depth over the resident scene into the
+// device buffer out = alpha | depth | value (zeroed here).  Re-runs the view
+// with larger buckets on instance overflow.
+int render_scene_device(fs_context* ctx, const fs_camera* cam, const uint8_t* member_dev,
+                        double alpha_floor, double t_floor, const double* ch_dev, int channels,
+                        double* out) {
+    fs::Work& w = ctx->work[0];
+    const int tx = fs::tiles_x_of(cam->width), ntiles = tx * fs::tiles_y_of(cam->height);
+    const size_t px = (size_t)cam->width * cam->height;
+    unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
+    int rc;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if ((rc = ensure_work(ctx, w, std::max<long long>(ctx->n, 1), ntiles, cap, 1))) return rc;
+        CK(cudaMemsetAsync(out, 0, sizeof(double) * px * (2 + (size_t)channels), w.stream));
+        fs::ProjectExport ex{};
+        ex.member = member_dev;
+        enqueue_bin(ctx, w, to_cam(*cam), alpha_floor, 1, ex);
+        fs::launch_raster_render(render_args(w, cam->width, cam->height, alpha_floor, t_floor, out,
+                                             channels, ch_dev),
+                                 w.stream);
+        CK(cudaGetLastError());
+        fs::ViewCounters vc{};
+        CK(cudaMemcpyAsync(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost, w.stream));
+        CK(cudaStreamSynchronize(w.stream));
+        if (!vc.overflow) return FS_OK;
+        cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull,
+                                                         (unsigned long long)vc.n_instances + 1024);
+    }
+    return fail(FS_ENOMEM, "fs_render: instance buffer overflow");
+}
+
+// labels[p] = obj where alpha > tau and depth beats the best so far (strict <:
+// ties keep the smaller object id); label 0 <=> best depth still +inf
+// (maskrender.py:88-93)
+__global__ void mask_combine_kernel(const double* __restrict__ alpha,
+                                    const double* __restrict__ depth, long long px, double tau,
+                                    unsigned int obj, uint16_t* __restrict__ labels,
+                                    double* __restrict__ best) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < px;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double d = depth[i];
+        if (alpha[i] > tau && (labels[i] == 0 || d < best[i])) {
+            labels[i] = (uint16_t)obj;
+            best[i] = d;
+        }
+    }
+}
+
+int check_render_cam(const fs_camera* cam) { return check_cam(*cam, 0); }
+
+}  // namespace
+
+extern "C" {
+
+int fs_render(fs_context* ctx, const fs_camera* cam, const uint8_t* member, double alpha_floor,
+              double transmittance_floor, const double* channel, int channels, double* value,
+              double* alpha, double* depth) {
+    if (!ctx || !cam || !alpha || !depth) return fail(FS_EINVAL, "fs_render: NULL argument");
+    if (channels != 0 && channels != 1 && channels != 3)
+        return fail(FS_EINVAL, "fs_render: channels must be 0, 1 or 3, got %d", channels);
+    if (channels && (!channel || !value)) return fail(FS_EINVAL, "fs_render: NULL channel/value");
+    int rc = check_render_cam(cam);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    fs::Work& w = ctx->work[0];
+    const size_t px = (size_t)cam->width * cam->height, n = (size_t)std::max<long long>(ctx->n, 0);
+    if ((rc = grow(&ctx->rn_f64, &ctx->rn_f64_cap, px * (2 + (size_t)channels)))) return rc;
+    const double* ch_dev = nullptr;
+    if (channels && n) {
+        if ((rc = grow(&ctx->rn_in, &ctx->rn_in_cap, n * channels))) return rc;
+        if ((rc = upload(ctx, ctx->rn_in, channel, sizeof(double) * n * channels, w.stream))) return rc;
+        ch_dev = ctx->rn_in;
+    }
+    const uint8_t* member_dev = nullptr;
+    if (member && n) {
+        if ((rc = grow(&ctx->rn_member, &ctx->rn_member_cap, n))) return rc;
+        if ((rc = upload(ctx, ctx->rn_member, member, n, w.stream))) return rc;
+        member_dev = ctx->rn_member;
+    }
+    if ((rc = render_scene_device(ctx, cam, member_dev, alpha_floor, transmittance_floor, ch_dev,
+                                  channels, ctx->rn_f64)))
+        return rc;
+    CK(cudaMemcpy(alpha, ctx->rn_f64, sizeof(double) * px, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(depth, ctx->rn_f64 + px, sizeof(double) * px, cudaMemcpyDeviceToHost));
+    if (channels)
+        CK(cudaMemcpy(value, ctx->rn_f64 + 2 * px, sizeof(double) * px * channels,
+                      cudaMemcpyDeviceToHost));
+    return FS_OK;
+}
+
+int fs_render_splats(fs_context* ctx, int width, int height, int64_t k, const double* mean2d,
+                     const double* conic, const double* depth, const double* opacity,
+                     const int64_t* tile_offsets, const int64_t* items, double alpha_floor,
+                     double transmittance_floor, const double* channel, int channels,
+                     double* value, double* alpha, double* depth_out) {
+    if (!ctx || !tile_offsets || !alpha || !depth_out ||
+        (k > 0 && (!mean2d || !conic || !depth || !opacity)))
+        return fail(FS_EINVAL, "fs_render_splats: NULL argument");
+    if (k < 0 || k > 0x7fffffffLL) return fail(FS_EINVAL, "fs_render_splats: bad splat count");
+    if (channels != 0 && channels != 1 && channels != 3)
+        return fail(FS_EINVAL, "fs_render_splats: channels must be 0, 1 or 3, got %d", channels);
+    if (channels && k > 0 && (!channel || !value))
+        return fail(FS_EINVAL, "fs_render_splats: NULL channel/value");
+    fs_camera c{};
+    c.width = width;
+    c.height = height;
+    int rc = check_render_cam(&c);
+    if (rc) return rc;
+    const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
+    const int64_t total = tile_offsets[ntiles];
+    if (tile_offsets[0] != 0 || total < 0 || total > 0xffffffffLL)
+        return fail(FS_EINVAL, "fs_render_splats: bad tile offsets");
+    std::vector<unsigned int> starts(ntiles + 1), order(ntiles), lists((size_t)std::max<int64_t>(total, 1));
+    for (int t = 0; t <= ntiles; ++t) {
+        if (t && tile_offsets[t] < tile_offsets[t - 1])
+            return fail(FS_EINVAL, "fs_render_splats: tile offsets not monotone");
+        starts[t] = (unsigned int)tile_offsets[t];
+    }
+    for (int64_t i = 0; i < total; ++i) {
+        if (!items || items[i] < 0 || items[i] >= k)
+            return fail(FS_EINVAL, "fs_render_splats: item %lld out of range", (long long)i);
+        lists[i] = (unsigned int)items[i];
+    }
+    for (int t = 0; t < ntiles; ++t) order[t] = (unsigned int)t;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    fs::Work& w = ctx->work[0];
+    const size_t px = (size_t)width * height, kk = (size_t)std::max<int64_t>(k, 1);
+    if ((rc = ensure_work(ctx, w, (long long)kk, ntiles, std::max(w.inst_cap, 1u), 1))) return rc;
+    if ((rc = grow(&ctx->rn_f64, &ctx->rn_f64_cap, px * (2 + (size_t)channels)))) return rc;
+    if ((rc = grow(&ctx->rn_in, &ctx->rn_in_cap, kk * (7 + (size_t)channels)))) return rc;
+    if ((rc = grow(&ctx->rn_u32, &ctx->rn_u32_cap, lists.size() + ntiles))) return rc;
+    double* d_mean = ctx->rn_in;
+    double* d_conic = d_mean + 2 * kk;
+    double* d_depth = d_conic + 3 * kk;
+    double* d_opac = d_depth + kk;
+    double* d_ch = d_opac + kk;
+    cudaStream_t st = w.stream;
+    if (k > 0) {
+        CK(cudaMemcpyAsync(d_mean, mean2d, 16 * (size_t)k, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_conic, conic, 24 * (size_t)k, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_depth, depth, 8 * (size_t)k, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_opac, opacity, 8 * (size_t)k, cudaMemcpyHostToDevice, st));
+        if (channels)
+            CK(cudaMemcpyAsync(d_ch, channel, 8 * (size_t)k * channels, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(ctx->rn_u32, lists.data(), 4 * lists.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->rn_u32 + lists.size(), order.data(), 4 * (size_t)ntiles,
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w.tile_start, starts.data(), 4 * (size_t)(ntiles + 1), cudaMemcpyHostToDevice,
+                       st));
+    CK(cudaMemsetAsync(ctx->rn_f64, 0, sizeof(double) * px * (2 + (size_t)channels), st));
+    fs::launch_view_begin(w.vc, st);
+    fs::launch_splat_records((int)k, d_mean, d_conic, d_depth, d_opac, alpha_floor, w.r32, w.r64,
+                             w.k64, ctx->num_sms, st);
+    fs::RasterArgs ra = render_args(w, width, height, alpha_floor, transmittance_floor, ctx->rn_f64,
+                                    channels, channels ? d_ch : nullptr);
+    ra.render.lists = ctx->rn_u32;
+    ra.tile_order = ctx->rn_u32 + lists.size();
+    fs::launch_raster_render(ra, st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(alpha, ctx->rn_f64, sizeof(double) * px, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(depth_out, ctx->rn_f64 + px, sizeof(double) * px, cudaMemcpyDeviceToHost));
+    if (channels)
+        CK(cudaMemcpy(value, ctx->rn_f64 + 2 * px, sizeof(double) * px * channels,
+                      cudaMemcpyDeviceToHost));
+    return FS_OK;
+}
+
+int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* membership,
+                   int num_objects, double tau, double alpha_floor, double transmittance_floor,
+                   uint16_t* labels) {
+    if (!ctx || !cam || !labels || (!membership && ctx->n > 0))
+        return fail(FS_EINVAL, "fs_render_mask: NULL argument");
+    if (num_objects < 1 || num_objects > 65536)
+        return fail(FS_EINVAL, "fs_render_mask: num_objects must be in [1, 65536], got %d",
+                    num_objects);
+    if (!(tau > 0.0 && tau < 1.0)) return fail(FS_EINVAL, "tau must lie in (0, 1), got %g", tau);
+    int rc = check_render_cam(cam);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    fs::Work& w = ctx->work[0];
+    const size_t px = (size_t)cam->width * cam->height, n = (size_t)std::max<long long>(ctx->n, 0);
+    if ((rc = grow(&ctx->rn_f64, &ctx->rn_f64_cap, 3 * px))) return rc;  // alpha | depth | best
+    if ((rc = grow(&ctx->rn_labels, &ctx->rn_labels_cap, px))) return rc;
+    if ((rc = grow(&ctx->rn_member, &ctx->rn_member_cap, std::max<size_t>(n, 1)))) return rc;
+    CK(cudaMemsetAsync(ctx->rn_labels, 0, sizeof(uint16_t) * px, w.stream));
+    double* best = ctx->rn_f64 + 2 * px;
+    int grid = (int)std::min<size_t>((px + 255) / 256, (size_t)ctx->num_sms * 8);
+    for (int obj = 1; obj < num_objects; ++obj) {
+        const uint8_t* row = membership + (size_t)obj * n;
+        bool any = false;  // maskrender.py:82-83: empty objects are skipped
+        for (size_t i = 0; i < n && !any; ++i) any = row[i] != 0;
+        if (!any) continue;
+        if ((rc = upload(ctx, ctx->rn_member, row, n, w.stream))) return rc;
+        if ((rc = render_scene_device(ctx, cam, ctx->rn_member, alpha_floor, transmittance_floor,
+                                      nullptr, 0, ctx->rn_f64)))
+            return rc;
+        mask_combine_kernel<<<std::max(grid, 1), 256, 0, w.stream>>>(
+            ctx->rn_f64, ctx->rn_f64 + px, (long long)px, tau, (unsigned int)obj, ctx->rn_labels, best);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(w.stream));
+    CK(cudaMemcpy(labels, ctx->rn_labels, sizeof(uint16_t) * px, cudaMemcpyDeviceToHost));
     return FS_OK;
 }
 

@@ -64,6 +64,8 @@ struct ProjectExport {
     double* conic;   // N x 3
     double* depth;   // N
     int64_t* radius; // N
+    const uint8_t* member;  // N, input, nullable: only members are binned (render subsets,
+                            // project_scene(member_mask=...), scene.py:346-350)
 };
 
 __host__ __device__ inline int tiles_x_of(int w) { return (w + kTile - 1) / kTile; }

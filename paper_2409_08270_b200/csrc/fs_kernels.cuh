@@ -40,6 +40,9 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
                     unsigned long long* rect, unsigned int* tile_count, Rec32* r32, Rec64* r64,
                     ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st);
 void launch_view_begin(ViewCounters* vc, cudaStream_t st);
+void launch_splat_records(int k, const double* mean2d, const double* conic, const double* depth,
+                          const double* opac, double alpha_floor, Rec32* r32, Rec64* r64,
+                          unsigned long long* k64, int num_sms, cudaStream_t st);
 
 // ---- fs_bin.cu ----
 // Per-tile buckets of instances (any order) from per-block tile histograms.
@@ -95,6 +98,16 @@ void launch_splat_keys(int k, const double* mean2d, const long long* radius, con
 
 // ---- fs_raster.cu ----
 constexpr unsigned int kTileSortCap = 3584;  // bucket entries sorted in shared memory
+// Novel-view compositing outputs (render_property, rasterizer.py:133-203).
+struct RenderArgs {
+    double* alpha;                 // H x W accumulated alpha (rho)
+    double* depth;                 // H x W blended depth (0 where alpha == 0)
+    double* value;                 // H x W x channels (channels > 0)
+    const double* channel;         // per gid x channels
+    int channels;                  // 0, 1 or 3
+    const unsigned int* lists;     // caller's ordered gid lists (tile_start offsets), or
+                                   // nullptr: sort the binning's buckets
+};
 struct RasterArgs {
     int width, height, tiles_x, ntiles;
     int num_objects;
@@ -109,9 +122,11 @@ struct RasterArgs {
     double* acc;                   // E x N float64 accumulator
     ViewCounters* vc;
     const unsigned int* tile_order;  // ntiles: launch order (tile_start_kernel)
+    RenderArgs render;             // launch_raster_render only
 };
 cudaError_t raster_configure();
 void launch_raster(const RasterArgs& a, cudaStream_t st);
+void launch_raster_render(const RasterArgs& a, cudaStream_t st);
 
 // ---- fs_assign.cu ----
 void launch_finalize(const double* acc, float* out, long long count, cudaStream_t st);

@@ -68,6 +68,43 @@ __device__ __forceinline__ void warp_or_and(unsigned long long& o, unsigned long
     a = ((unsigned long long)ahi << 32) | alo;
 }
 
+// float32 screen record of a splat with mean (mx, my), conic (ia, ib, ic),
+// 2-D covariance diagonal (ca, cc) and opacity o.  alpha >= floor  <=>
+// power >= log(floor / o)  <=>  d^T conic d <= qmax.  Screen-only quantities
+// are float32: their ~1e-7 relative error is far inside the 1e-5 / 0.01 px /
+// 0.02 margins, so the screen stays conservative.
+__device__ __forceinline__ Rec32 screen_record(double mx, double my, double ia, double ib,
+                                               double ic, double ca, double cc, double o,
+                                               double alpha_floor, bool alive) {
+    Rec32 s;
+    s.mx = (float)mx;
+    s.my = (float)my;
+    s.a = (float)ia;
+    s.b = (float)ib;
+    s.c = (float)ic;
+    if (alpha_floor > 0.0 && o >= alpha_floor && alive) {
+        const float L = logf((float)o / (float)alpha_floor);  // log(o / floor) >= 0
+        const float qmax = 2.0f * fmaxf(L, 0.0f);
+        const float hx = sqrtf(qmax * (float)ca) * (1.0f + 1e-5f) + 0.01f;
+        const float hy = sqrtf(qmax * (float)cc) * (1.0f + 1e-5f) + 0.01f;
+        const float spread = (fabsf((float)ia) + fabsf((float)ic) + 2.0f * fabsf((float)ib)) *
+                             (hx * hx + hy * hy);
+        const float margin = 0.02f + 1e-6f * spread;
+        s.cut = -L - margin;
+        s.hx = hx;
+        s.hy = hy;
+    } else if (alpha_floor > 0.0) {
+        s.cut = __int_as_float(0x7f800000);  // +inf: never passes
+        s.hx = 0.0f;
+        s.hy = 0.0f;
+    } else {
+        s.cut = __int_as_float(0xff800000);  // -inf: exact blend, no screen
+        s.hx = __int_as_float(0x7f800000);
+        s.hy = __int_as_float(0x7f800000);
+    }
+    return s;
+}
+
 // K1: one thread per Gaussian.  Mirrors _project_arrays (scene.py:252-312)
 // and tile_range (rasterizer.py:106-113); emits the depth sort key, the tile
 // rectangle and the walk records.  cull_floor > 0 additionally drops (from
@@ -160,6 +197,7 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
             }
             double o = opac[i];
             unsigned long long key = ~0ull, rc = ~0ull;
+            if (ex.member && !ex.member[i]) alive = false;  // not in the rendered subset
             if (alive) {
                 ++c_emit;
                 key = f64_sort_key(z);
@@ -182,35 +220,7 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
             q.c = ic;
             q.o = o;
             r64[i] = q;
-            Rec32 s;
-            s.mx = (float)mxp;
-            s.my = (float)myp;
-            s.a = (float)ia;
-            s.b = (float)ib;
-            s.c = (float)ic;
-            if (alpha_floor > 0.0 && o >= alpha_floor && alive) {
-                // alpha >= floor  <=>  power >= log(floor / o)  <=>  d^T conic d <= qmax.
-                // Screen-only quantities: float32 (their ~1e-7 relative error is far
-                // inside the 1e-5 / 0.01 px / 0.02 margins).
-                const float L = logf((float)o / (float)alpha_floor);  // log(o / floor) >= 0
-                const float qmax = 2.0f * fmaxf(L, 0.0f);
-                const float hx = sqrtf(qmax * (float)a) * (1.0f + 1e-5f) + 0.01f;
-                const float hy = sqrtf(qmax * (float)c) * (1.0f + 1e-5f) + 0.01f;
-                const float spread = (fabsf((float)ia) + fabsf((float)ic) + 2.0f * fabsf((float)ib)) *
-                                     (hx * hx + hy * hy);
-                const float margin = 0.02f + 1e-6f * spread;
-                s.cut = -L - margin;
-                s.hx = hx;
-                s.hy = hy;
-            } else if (alpha_floor > 0.0) {
-                s.cut = __int_as_float(0x7f800000);  // +inf: never passes
-                s.hx = 0.0f;
-                s.hy = 0.0f;
-            } else {
-                s.cut = __int_as_float(0xff800000);  // -inf: exact blend, no screen
-                s.hx = __int_as_float(0x7f800000);
-                s.hy = __int_as_float(0x7f800000);
-            }
+            const Rec32 s = screen_record(mxp, myp, ia, ib, ic, a, c, o, alpha_floor, alive);
             r32[i] = s;
             if (ex.alive) {
                 ex.alive[i] = alive ? 1 : 0;
@@ -285,6 +295,51 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
     if (grid > cap) grid = cap;
     project_kernel<<<grid, 256, 0, st>>>(n, mx, my, mz, sig, opac, cam, alpha_floor, cull_floor,
                                          keys, vals, rect, tile_count, r32, r64, vc, ex);
+}
+
+// Records of an explicit splat list (render_property over a caller's
+// TileBinning, rasterizer.py:133-203): the float64 walk record, the float32
+// screen (covariance diagonal recovered from the conic) and the depth key.
+__global__ void splat_records_kernel(int k, const double* __restrict__ mean2d,
+                                     const double* __restrict__ conic,
+                                     const double* __restrict__ depth,
+                                     const double* __restrict__ opac, double alpha_floor,
+                                     Rec32* __restrict__ r32, Rec64* __restrict__ r64,
+                                     unsigned long long* __restrict__ k64) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+        const double mx = mean2d[2 * i], my = mean2d[2 * i + 1];
+        const double ia = conic[3 * i], ib = conic[3 * i + 1], ic = conic[3 * i + 2];
+        const double o = opac[i];
+        Rec64 q;
+        q.mx = mx;
+        q.my = my;
+        q.a = ia;
+        q.b = ib;
+        q.c = ic;
+        q.o = o;
+        r64[i] = q;
+        const double det = ia * ic - ib * ib;  // conic = inverse covariance
+        const bool ok = det > 0.0;
+        r32[i] = screen_record(mx, my, ia, ib, ic, ok ? ic / det : 0.0, ok ? ia / det : 0.0, o,
+                               alpha_floor, true);
+        if (!ok && alpha_floor > 0.0) {  // degenerate conic: no finite screen box
+            Rec32 s = r32[i];
+            s.cut = __int_as_float(0xff800000);
+            s.hx = s.hy = __int_as_float(0x7f800000);
+            r32[i] = s;
+        }
+        k64[i] = f64_sort_key(depth[i]);
+    }
+}
+
+void launch_splat_records(int k, const double* mean2d, const double* conic, const double* depth,
+                          const double* opac, double alpha_floor, Rec32* r32, Rec64* r64,
+                          unsigned long long* k64, int num_sms, cudaStream_t st) {
+    if (k <= 0) return;
+    int grid = (k + 255) / 256;
+    if (grid > num_sms * 8) grid = num_sms * 8;
+    splat_records_kernel<<<grid, 256, 0, st>>>(k, mean2d, conic, depth, opac, alpha_floor, r32, r64,
+                                               k64);
 }
 
 }  // namespace fs

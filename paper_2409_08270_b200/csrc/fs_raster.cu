@@ -94,6 +94,15 @@ __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_c
     return (2u << c1) - (1u << c0);
 }
 
+// float64 depth of a gid from its order-preserving key (inverse of f64_sort_key)
+__device__ __forceinline__ double depth_of_key(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+// kRender = false: accumulate alpha*T into the E x N matrix (contributions.py:119-160).
+// kRender = true:  composite alpha, depth and an optional channel per pixel
+//                  (render_property, rasterizer.py:133-203); no mask, no atomics.
+template <bool kRender>
 __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const ViewCounters* vc = a.vc;
     if (vc->overflow) return;
@@ -102,8 +111,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const int x0 = (tile % a.tiles_x) * kTile, y0 = (tile / a.tiles_x) * kTile;
     const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
     const bool inside = px < a.width && py < a.height;
-    const unsigned int label = inside ? a.mask[(size_t)py * a.width + px] : 0u;
-    {
+    const unsigned int label = (!kRender && inside) ? a.mask[(size_t)py * a.width + px] : 0u;
+    if (!kRender) {
         // label range check of every pixel, empty tiles included
         // (contributions.py:108-114; the host reports the first bad view)
         const unsigned int m = __reduce_max_sync(0xffffffffu, label);
@@ -120,11 +129,17 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_done = 0;  // the tile sort's barriers publish these
     RasterSmem& S = SH.walk;
-    // prologue: the tile's bucket -> gids in the reference (depth, id) order
-    unsigned int* sorted = sorted_view(a.sort.inst, begin);
-    sort_tile_list(a.sort.inst + begin, sorted, a.sort.scratch64 + 2ull * begin, n_list, a.sort.keys,
-                   SH.sort, a.sort.cap);
-    const unsigned int* __restrict__ list = sorted;
+    const unsigned int* __restrict__ list;
+    if (kRender && a.render.lists) {
+        list = a.render.lists + begin;  // caller's binning, already in reference order
+        __syncthreads();
+    } else {
+        // prologue: the tile's bucket -> gids in the reference (depth, id) order
+        unsigned int* sorted = sorted_view(a.sort.inst, begin);
+        sort_tile_list(a.sort.inst + begin, sorted, a.sort.scratch64 + 2ull * begin, n_list,
+                       a.sort.keys, SH.sort, a.sort.cap);
+        list = sorted;
+    }
     WarpSmem& W = S.w[warp];
     const unsigned int lt_mask = (1u << lane) - 1u;
     // the warp's pixel-centre strip
@@ -146,6 +161,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
 
     double T = 1.0;
     bool active = inside;
+    // render accumulators (rasterizer.py:168-172)
+    double r_acc = 0.0, d_acc = 0.0, v_acc[3] = {0.0, 0.0, 0.0};
+    const int n_ch = kRender ? a.render.channels : 0;
     unsigned long long steps = 0, exact = 0, atom = 0;
     int head = 0, cnt = 0;  // ring of strip hits
 
@@ -249,6 +267,19 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                                 w = __dmul_rn(alpha, T);                     // :150
                                 T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
                                 active = !(T < tf_eff);                      // :156-157
+                                if (kRender) {
+                                    // rasterizer.py:184-191, summed in list order per pixel
+                                    const unsigned int g = W.gid[(head + k) & (kRing - 1)];
+                                    const double z = depth_of_key(a.sort.keys.k64[g]);
+                                    r_acc = __dadd_rn(r_acc, w);
+                                    d_acc = __dadd_rn(d_acc, __dmul_rn(z, w));
+#pragma unroll
+                                    for (int ch = 0; ch < 3; ++ch)
+                                        if (ch < n_ch)
+                                            v_acc[ch] = __dadd_rn(
+                                                v_acc[ch],
+                                                __dmul_rn(w, a.render.channel[(size_t)g * n_ch + ch]));
+                                }
                             }
                         }
                         myval[k * kRowStride + lane] = w;
@@ -256,7 +287,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 }
                 __syncwarp();
                 // ---- C: aggregation + float64 atomics ----
-                if (uniform) {
+                if (kRender) {
+                    // no scatter: the pixel keeps its own sums
+                } else if (uniform) {
                     // lane = (splat k, segment of kMini pixels)
                     const int k = lane % kMini, seg = lane / kMini;
                     unsigned int bits = k < nm ? W.cm[(head + k) & (kRing - 1)] & act : 0u;
@@ -290,6 +323,15 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             cnt -= nm;
         }
     }
+    if (kRender && inside) {
+        // rasterizer.py:197-203 (depth = depth_acc / rho where rho > 0)
+        const size_t at = (size_t)py * a.width + px;
+        a.render.alpha[at] = r_acc;
+        a.render.depth[at] = r_acc > 0.0 ? __ddiv_rn(d_acc, r_acc) : 0.0;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+            if (ch < n_ch) a.render.value[at * n_ch + ch] = v_acc[ch];
+    }
     // per-CTA counters: the last warp to finish issues the global atomics (no
     // end-of-tile barrier -- warps leave as soon as their strip is done)
     atom = __reduce_add_sync(0xffffffffu, (unsigned int)atom);  // per-lane counts
@@ -314,13 +356,21 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
 cudaError_t raster_configure() {
     cudaError_t e = tile_sort_configure(kTileSortCap);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(raster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(raster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kRasterSmem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(raster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kRasterSmem);
 }
 
 void launch_raster(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
-    raster_kernel<<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
+    raster_kernel<false><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
+}
+
+void launch_raster_render(const RasterArgs& a, cudaStream_t st) {
+    if (a.ntiles <= 0) return;
+    raster_kernel<true><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
 }
 
 }  // namespace fs

@@ -113,3 +113,16 @@ def test_shard_views_partition():
             flat = [i for s in shards for i in s]
             assert flat == list(range(n))
             assert max(map(len, shards)) - min(map(len, shards)) <= 1
+
+
+def test_render_grid_round_trip(tmp_path):
+    """save_render_grid / load_render_grid (reference rasterizer.py:237-252)."""
+    from paper_2409_08270_b200 import load_render_grid, save_render_grid
+    grid = np.random.default_rng(0).random((12, 9)).astype(np.float32)
+    path = tmp_path / "rho.f32"
+    save_render_grid(path, grid)
+    assert path.stat().st_size == 8 + 12 * 9 * 4
+    assert np.array_equal(load_render_grid(path), grid)
+    path.write_bytes(path.read_bytes()[:-4])
+    with pytest.raises(ValueError, match="truncated"):
+        load_render_grid(path)
