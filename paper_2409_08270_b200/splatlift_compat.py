@@ -8,6 +8,10 @@ its FastAPI service and user code run on the B200 kernels unchanged:
     splatlift.cli.accumulate_contributions                (reference cli.py:17)
     splatlift.assign_binary / assign_scene, splatlift.solver.*,
     splatlift.cli.*  (cli.py:25), splatlift.service.*     (service.py:28)
+    splatlift.render_view / render_property / render_subset_alpha_depth,
+    splatlift.rasterizer.*, splatlift.maskrender.*        (maskrender.py:15-21)
+    splatlift.render_binary_mask / render_scene_mask,
+    splatlift.maskrender.*, splatlift.cli.*               (cli.py:19)
 
 The replacement functions accept the reference's own ``GaussianScene``,
 ``CameraView``, ``LabelMask`` and ``ContributionMatrix`` objects (they only
@@ -22,17 +26,44 @@ from __future__ import annotations
 import importlib
 
 from . import contributions as _contrib
+from . import maskrender as _maskrender
+from . import rasterizer as _rasterizer
 from . import solver as _solver
 
 _TARGETS = {
     "accumulate_contributions": ["splatlift", "splatlift.contributions", "splatlift.cli"],
     "assign_binary": ["splatlift", "splatlift.solver", "splatlift.cli", "splatlift.service"],
     "assign_scene": ["splatlift", "splatlift.solver", "splatlift.cli", "splatlift.service"],
+    "render_view": ["splatlift", "splatlift.rasterizer"],
+    "render_property": ["splatlift", "splatlift.rasterizer", "splatlift.maskrender"],
+    "render_subset_alpha_depth": ["splatlift", "splatlift.rasterizer", "splatlift.maskrender"],
+    "render_binary_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli"],
+    "render_scene_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli"],
 }
 _saved: dict = {}
 
 
 def _replacement(name):
+    if name.startswith("render_") and name.endswith("_mask"):
+        ref_mask = importlib.import_module("splatlift.maskrender").RenderedMask
+        impl = getattr(_maskrender, name)
+
+        def render_mask(*args, **kw):
+            m = impl(*args, **kw)
+            return ref_mask(view_id=m.view_id, labels=m.labels, gamma=m.gamma, tau=m.tau)
+
+        render_mask.__name__ = name
+        return render_mask
+    if name.startswith("render_"):
+        ref_out = importlib.import_module("splatlift.rasterizer").RenderOutput
+        impl = getattr(_rasterizer, name)
+
+        def render(*args, **kw):
+            o = impl(*args, **kw)
+            return ref_out(value=o.value, alpha=o.alpha, depth=o.depth)
+
+        render.__name__ = name
+        return render
     if name == "accumulate_contributions":
         ref_matrix = importlib.import_module("splatlift.contributions").ContributionMatrix
 

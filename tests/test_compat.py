@@ -41,3 +41,26 @@ def test_install_rebinds_every_import_site(splatlift):
     finally:
         splatlift_compat.uninstall()
     assert (cli.accumulate_contributions, solver.assign_binary, service.assign_scene) == before
+
+
+def test_install_rebinds_render_import_sites(splatlift):
+    from paper_2409_08270_b200 import splatlift_compat
+    import splatlift.cli as cli
+    import splatlift.maskrender as maskrender
+    import splatlift.rasterizer as rasterizer
+    before = (rasterizer.render_view, maskrender.render_subset_alpha_depth, cli.render_scene_mask)
+    splatlift_compat.install()
+    try:
+        mod_name = "paper_2409_08270_b200.splatlift_compat"
+        for mod in (splatlift, rasterizer):
+            assert mod.render_view.__module__ == mod_name
+        for mod in (splatlift, rasterizer, maskrender):
+            assert mod.render_property.__module__ == mod_name
+            assert mod.render_subset_alpha_depth.__module__ == mod_name
+        for mod in (splatlift, maskrender, cli):
+            assert mod.render_binary_mask.__module__ == mod_name
+            assert mod.render_scene_mask.__module__ == mod_name
+    finally:
+        splatlift_compat.uninstall()
+    assert (rasterizer.render_view, maskrender.render_subset_alpha_depth,
+            cli.render_scene_mask) == before
