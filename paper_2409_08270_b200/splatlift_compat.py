@@ -11,7 +11,7 @@ its FastAPI service and user code run on the B200 kernels unchanged:
     splatlift.render_view / render_property / render_subset_alpha_depth,
     splatlift.rasterizer.*, splatlift.maskrender.*        (maskrender.py:15-21)
     splatlift.render_binary_mask / render_scene_mask,
-    splatlift.maskrender.*, splatlift.cli.*               (cli.py:19)
+    splatlift.maskrender.*, splatlift.cli.* (cli.py:19), splatlift.service.* (service.py:24-26)
 
 The replacement functions accept the reference's own ``GaussianScene``,
 ``CameraView``, ``LabelMask`` and ``ContributionMatrix`` objects (they only
@@ -34,11 +34,13 @@ _TARGETS = {
     "accumulate_contributions": ["splatlift", "splatlift.contributions", "splatlift.cli"],
     "assign_binary": ["splatlift", "splatlift.solver", "splatlift.cli", "splatlift.service"],
     "assign_scene": ["splatlift", "splatlift.solver", "splatlift.cli", "splatlift.service"],
-    "render_view": ["splatlift", "splatlift.rasterizer"],
+    "render_view": ["splatlift", "splatlift.rasterizer", "splatlift.service"],
     "render_property": ["splatlift", "splatlift.rasterizer", "splatlift.maskrender"],
     "render_subset_alpha_depth": ["splatlift", "splatlift.rasterizer", "splatlift.maskrender"],
-    "render_binary_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli"],
-    "render_scene_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli"],
+    "render_binary_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli",
+                           "splatlift.service"],
+    "render_scene_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli",
+                          "splatlift.service"],
 }
 _saved: dict = {}
 
