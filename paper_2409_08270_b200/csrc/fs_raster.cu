@@ -74,6 +74,21 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+// 32 x 32 bit-matrix transpose across the warp: lane i holds row i (bit j =
+// M[i][j]); on return lane j holds column j (bit i = M[i][j]).  Five
+// shuffle stages swap the off-diagonal blocks of halving size.
+__device__ __forceinline__ unsigned int warp_transpose32(unsigned int x, int lane) {
+    const unsigned int masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int b = 16 >> s;
+        const unsigned int m = masks[s];
+        const unsigned int y = __shfl_xor_sync(0xffffffffu, x, b);
+        x = (lane & b) ? ((x & ~m) | ((y & ~m) >> b)) : ((x & m) | ((y & m) << b));
+    }
+    return x;
+}
+
 __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0) {
     if (!(s.cut > -INFINITY)) return 0xFFFFu;  // exact blend: no alpha floor
     const float dv = v_centre - s.my;
@@ -209,10 +224,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             Rec64 rq;
             if (lane < nm) rq = a.r64[W.gid[(head + lane) & (kRing - 1)]];
             // this lane's candidates of the mini-batch (bit k = k-th strip hit)
-            unsigned int mine = 0;
-#pragma unroll
-            for (int k = 0; k < kMini; ++k)
-                if (k < nm) mine |= ((W.cm[(head + k) & (kRing - 1)] >> lane) & 1u) << k;
+            unsigned int mine = lane < nm ? W.cm[(head + lane) & (kRing - 1)] : 0u;
+            mine = warp_transpose32(mine, lane);
             if (!active) mine = 0;
             // lane-major packing of the (splat, pixel) pairs: warp prefix sum
             const unsigned int n_mine = __popc(mine);
