@@ -268,7 +268,10 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                     const double t3 = __dmul_rn(__dmul_rn(q.b, ddu), ddv);
                     const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), t3);
                     const double alpha = __dmul_rn(q.o, exp(power));  // :146-147
-                    myval[k * kRowStride + src] = alpha < kAlphaClamp ? alpha : kAlphaClamp;
+                    const double ac = alpha < kAlphaClamp ? alpha : kAlphaClamp;
+                    // below the floor: no weight, no transmittance update (:148-149) --
+                    // exactly what alpha = 0 does in B (w = 0 * T, T * (1 - 0) = T)
+                    myval[k * kRowStride + src] = ac >= af_eff ? ac : 0.0;
                 }
                 __syncwarp();
                 // ---- B: every lane walks its own candidates in list order ----
@@ -279,8 +282,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         mm &= mm - 1u;
                         double w = 0.0;
                         if (active) {
-                            const double alpha = myval[k * kRowStride + lane];
-                            if (alpha >= af_eff) {                          // :148-149
+                            const double alpha = myval[k * kRowStride + lane];  // 0: below floor
+                            {
                                 w = __dmul_rn(alpha, T);                     // :150
                                 T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
                                 active = !(T < tf_eff);                      // :156-157
