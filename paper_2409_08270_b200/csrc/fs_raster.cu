@@ -21,9 +21,10 @@
 //      T, so the expensive part runs on full warps);
 //   B  every lane walks its own candidates in list order: alpha floor,
 //      w = alpha*T, T *= (1-alpha), T floor after the update (:148-157);
-//   C  label-uniform warps reduce w with a padded transpose in shared memory
-//      + 2 shuffles and issue one float64 atomic per splat; mixed-label warps
-//      issue one atomic per contributing pixel.
+//   C  warps with at most 4 distinct labels reduce w per (splat, label) with a
+//      padded transpose in shared memory + a shuffle and issue one float64
+//      atomic each; warps with more labels issue one atomic per contributing
+//      pixel.
 // A warp stops when none of its pixels is active (contributions.py:158-159:
 // pixels are independent, the reference's tile-level break is an
 // optimisation of the same rule).
@@ -42,6 +43,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMini = 16;      // strip hits per mini-batch
 constexpr int kRing = 64;       // per-warp ring of strip hits (>= kMini - 1 + 32)
 constexpr int kRowStride = 33;  // doubles per padded w/alpha row (bank-conflict-free transpose)
+constexpr int kMaxGroups = 4;   // label groups per warp reduced before the atomics
 
 struct WarpSmem {
     Rec64 rec[kMini];        // float64 records of the mini-batch's hits
@@ -165,13 +167,14 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
     const float v_lo = (float)(y0 + 2 * warp) + 0.5f, v_hi = v_lo + 1.0f;
 
-    const unsigned int inside_mask = __ballot_sync(0xffffffffu, inside);
-    const int first = inside_mask ? __ffs(inside_mask) - 1 : 0;
-    const unsigned int lbl0 = __shfl_sync(0xffffffffu, label, first);
-    const bool uniform = __all_sync(0xffffffffu, !inside || label == lbl0);
+    // The warp's label groups (fixed for the whole walk): lanes sharing a label.
+    // With at most kMaxGroups distinct labels, C reduces w per (splat, label)
+    // and issues one atomic each; otherwise one atomic per contributing pixel.
+    const unsigned int grp = __match_any_sync(0xffffffffu, inside ? label : 0xffffffffu);
+    const unsigned int leaders = __ballot_sync(0xffffffffu, inside && lane == __ffs(grp) - 1);
+    const bool grouped = __popc(leaders) <= kMaxGroups;
     // out-of-range labels (reported through max_label) never address the accumulator
     const bool lbl_ok = label < (unsigned)a.num_objects;
-    const bool lbl0_ok = lbl0 < (unsigned)a.num_objects;
 
     const double af_eff = a.af_eff, tf_eff = a.tf_eff;
     const long long n_g = a.n_gaussians;
@@ -309,21 +312,28 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 // ---- C: aggregation + float64 atomics ----
                 if (kRender) {
                     // no scatter: the pixel keeps its own sums
-                } else if (uniform) {
-                    // lane = (splat k, segment of kMini pixels)
+                } else if (grouped) {
+                    // lane = (splat k, segment of kMini pixels); one pass per label group
                     const int k = lane % kMini, seg = lane / kMini;
-                    unsigned int bits = k < nm ? W.cm[(head + k) & (kRing - 1)] & act : 0u;
-                    bits = (bits >> (seg * kMini)) & ((1u << kMini) - 1u);
-                    double v = 0.0;
+                    const unsigned int cmk = k < nm ? W.cm[(head + k) & (kRing - 1)] & act : 0u;
+                    unsigned int lead = leaders;
+                    while (lead) {
+                        const int ld = __ffs(lead) - 1;
+                        lead &= lead - 1u;
+                        const unsigned int gmask = __shfl_sync(0xffffffffu, grp, ld);
+                        const unsigned int gl = __shfl_sync(0xffffffffu, label, ld);
+                        const unsigned int bits = ((cmk & gmask) >> (seg * kMini)) & ((1u << kMini) - 1u);
+                        double v = 0.0;
 #pragma unroll
-                    for (int t = 0; t < kMini; ++t)
-                        if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * kMini + t];
+                        for (int t = 0; t < kMini; ++t)
+                            if ((bits >> t) & 1u) v += myval[k * kRowStride + seg * kMini + t];
 #pragma unroll
-                    for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    const bool fire = lane < kMini && k < nm && v > 0.0 && lbl0_ok;
-                    if (fire) {
-                        atomicAdd(acc + (size_t)lbl0 * n_g + W.gid[(head + k) & (kRing - 1)], v);
-                        ++atom;
+                        for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                        const bool fire = lane < kMini && k < nm && v > 0.0 && gl < (unsigned)a.num_objects;
+                        if (fire) {
+                            atomicAdd(acc + (size_t)gl * n_g + W.gid[(head + k) & (kRing - 1)], v);
+                            ++atom;
+                        }
                     }
                 } else if (lbl_ok) {
                     unsigned int mm = mine;

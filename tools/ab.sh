@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 LIB=paper_2409_08270_b200/_lib/libflashsplat_b200.so
 cp $LIB /tmp/lib_orig.so
-B="python bench.py --config C2 --views 4 --steps 1 --warmup 1 --no-cpu --no-e2e --streams 1"
+B="python bench.py --config ${AB_CFG:-C2} --views 4 --steps 1 --warmup 1 --no-cpu --no-e2e --streams 1"
 for v in _variants/*.so; do
   n=$(basename $v .so)
   cp $v $LIB
