@@ -85,6 +85,11 @@ int fs_copy_to_device(fs_context *ctx, void *dst, const void *src, uint64_t byte
 int fs_copy_to_host(fs_context *ctx, void *dst, const void *src, uint64_t bytes);
 int fs_synchronize(fs_context *ctx);
 
+/* Page-locked host memory (DMA at full PCIe/C2C speed) for result arrays the
+ * caller hands back to numpy -- the contribution matrix and the labels. */
+int fs_host_alloc(fs_context *ctx, uint64_t bytes, void **out);
+int fs_host_free(fs_context *ctx, void *ptr);
+
 /* Per-stage CUDA-event timing inside fs_accumulate (events on each view's
  * stream around its stages; adds ~3 event records per view). */
 int fs_set_timing(fs_context *ctx, int enable);

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -24,7 +25,7 @@ MODE_BINARY, MODE_SCENE = 0, 1
 EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
-    "fs_copy_to_host", "fs_synchronize", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_copy_to_host", "fs_synchronize", "fs_host_alloc", "fs_host_free", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
     "fs_accumulate", "fs_finalize", "fs_assign", "fs_render", "fs_render_splats", "fs_render_mask",
 )
 
@@ -94,6 +95,8 @@ def load() -> ctypes.CDLL:
             "fs_copy_to_device": ([P, P, P, ctypes.c_uint64], I),
             "fs_copy_to_host": ([P, P, P, ctypes.c_uint64], I),
             "fs_synchronize": ([P], I),
+            "fs_host_alloc": ([P, ctypes.c_uint64, ctypes.POINTER(P)], I),
+            "fs_host_free": ([P, P], I),
             "fs_set_timing": ([P, I], I),
             "fs_set_scene": ([P, I64, P, P, P, P], I),
             "fs_project": ([P, P, P, P, P, P, P, P], I),
@@ -195,6 +198,8 @@ class Context:
         self.n = 0
         self.lock = threading.RLock()
         self._buffers: dict = {}
+        self._pinned_pool: dict = {}
+        self._pin_lock = threading.Lock()
 
     def set_timing(self, enable: bool) -> None:
         _check(load().fs_set_timing(self.handle, 1 if enable else 0))
@@ -204,6 +209,10 @@ class Context:
             buf.release()
         self._buffers = {}
         if self.handle:
+            for ptrs in getattr(self, "_pinned_pool", {}).values():
+                for ptr in ptrs:
+                    load().fs_host_free(self.handle, ptr)
+            self._pinned_pool = {}
             load().fs_destroy(self.handle)
             self.handle = None
 
@@ -332,6 +341,33 @@ class Context:
 
     def alloc(self, nbytes: int) -> DeviceBuffer:
         return DeviceBuffer(self, nbytes)
+
+    def pinned_empty(self, shape, dtype) -> np.ndarray:
+        """numpy array in page-locked host memory (device -> host copies at full
+        DMA speed).  Blocks are pooled by size: when the array (or any view of
+        it) is garbage-collected its block returns to the pool."""
+        dtype = np.dtype(dtype)
+        count = int(np.prod(shape)) if len(shape) else 1
+        nbytes = max(count * dtype.itemsize, 1)
+        with self._pin_lock:
+            pool = self._pinned_pool.setdefault(nbytes, [])
+            ptr = pool.pop() if pool else None
+        if ptr is None:
+            p = ctypes.c_void_p()
+            _check(load().fs_host_alloc(self.handle, nbytes, ctypes.byref(p)))
+            ptr = p.value
+        holder = (ctypes.c_char * nbytes).from_address(ptr)
+        weakref.finalize(holder, self._pinned_release, nbytes, ptr)
+        return np.frombuffer(holder, dtype=dtype, count=count).reshape(shape)
+
+    def _pinned_release(self, nbytes: int, ptr: int) -> None:
+        with self._pin_lock:
+            pool = self._pinned_pool.setdefault(nbytes, [])
+            if len(pool) < 4 and self.handle:
+                pool.append(ptr)
+                return
+        if self.handle:
+            load().fs_host_free(self.handle, ptr)
 
 
 def assign(values: np.ndarray, gamma: float, mode: int, ctx: Context = None,

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "flashsplat_b200.h"
@@ -156,6 +157,26 @@ int dev_alloc(T** p, size_t count) {
 
 constexpr size_t kUploadChunk = 8u << 20;  // pinned staging chunk (bytes)
 
+// Host memcpy into pinned staging, split over a few threads: one core copies
+// ~10 GB/s, well below the DMA rate, so the scene upload was memcpy-bound.
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    static const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const unsigned parts = bytes < (2u << 20) ? 1u : hw;
+    if (parts == 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = (bytes + parts - 1) / parts;
+    std::vector<std::thread> th;
+    th.reserve(parts - 1);
+    for (unsigned p = 1; p < parts; ++p) {
+        const size_t off = std::min(bytes, per * p), m = std::min(bytes - off, per);
+        th.emplace_back([=] { memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, m); });
+    }
+    memcpy(dst, src, std::min(bytes, per));
+    for (auto& t : th) t.join();
+}
+
 // Pageable host -> device copy through the context's two pinned chunks, so the
 // host memcpy of chunk i overlaps the DMA of chunk i-1.
 int upload(fs_context* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
@@ -172,7 +193,7 @@ int upload(fs_context* ctx, void* dst, const void* src, size_t bytes, cudaStream
     for (size_t off = 0; off < bytes; off += kUploadChunk) {
         const size_t m = std::min(kUploadChunk, bytes - off);
         CK(cudaEventSynchronize(ctx->pinned_free[slot]));
-        memcpy(ctx->pinned_up[slot], s + off, m);
+        parallel_memcpy(ctx->pinned_up[slot], s + off, m);
         CK(cudaMemcpyAsync(d + off, ctx->pinned_up[slot], m, cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(ctx->pinned_free[slot], st));
         slot ^= 1;
@@ -472,6 +493,23 @@ int fs_copy_to_host(fs_context* ctx, void* dst, const void* src, uint64_t bytes)
     return FS_OK;
 }
 
+int fs_host_alloc(fs_context* ctx, uint64_t bytes, void** out) {
+    if (!ctx || !out) return fail(FS_EINVAL, "fs_host_alloc: NULL argument");
+    CK(cudaSetDevice(ctx->device));
+    cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FS_ENOMEM, "cudaHostAlloc of %llu bytes failed", (unsigned long long)bytes);
+    }
+    return FS_OK;
+}
+
+int fs_host_free(fs_context* ctx, void* ptr) {
+    if (!ctx) return fail(FS_EINVAL, "fs_host_free: NULL context");
+    if (ptr) CK(cudaFreeHost(ptr));
+    return FS_OK;
+}
+
 int fs_synchronize(fs_context* ctx) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
@@ -714,7 +752,7 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         if (!masks_on_device) {
             const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
             if (w.h2d_pending) CK(cudaEventSynchronize(w.h2d_done));
-            memcpy(w.pinned, masks[v], bytes);
+            parallel_memcpy(w.pinned, masks[v], bytes);
             CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
             CK(cudaEventRecord(w.h2d_done, w.stream));
             w.h2d_pending = true;
@@ -763,7 +801,7 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         const uint16_t* mask = masks[v];
         if (!masks_on_device) {
             const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
-            memcpy(w.pinned, masks[v], bytes);
+            parallel_memcpy(w.pinned, masks[v], bytes);
             CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
             mask = w.mask_dev;
         }

@@ -93,7 +93,7 @@ class LabelSolver:
         self.num_objects = e
         if not download:
             return None
-        values = np.empty((e, n), dtype=np.float32)
+        values = ctx.pinned_empty((e, n), np.float32)  # full-speed D2H
         if values.size:
             A.to_host(values)
         return ContributionMatrix(values=values)
@@ -109,7 +109,7 @@ class LabelSolver:
                 raise ValueError(f"binary assignment requires E=2, got E={e}")
             nat.assign(None, gamma, nat.MODE_BINARY, ctx=self.ctx, on_device_ptr=self._A_cur.ptr,
                        n=n, e=e, out_ptr=self._out_cur.ptr)
-            labels = np.empty(n, np.uint8)
+            labels = self.ctx.pinned_empty((n,), np.uint8)
             self._out_cur.to_host(labels)
             return Assignment(mode="binary", gamma=gamma, labels=labels)
         if mode == "scene":
@@ -117,7 +117,7 @@ class LabelSolver:
                 raise ValueError(f"scene assignment requires E>=2, got E={e}")
             nat.assign(None, gamma, nat.MODE_SCENE, ctx=self.ctx, on_device_ptr=self._A_cur.ptr,
                        n=n, e=e, out_ptr=self._out_cur.ptr)
-            member = np.empty((e, n), np.uint8)
+            member = self.ctx.pinned_empty((e, n), np.uint8)
             self._out_cur.to_host(member)
             return Assignment(mode="scene", gamma=gamma, membership=member)
         raise ValueError(f"unknown assignment mode {mode!r}")
