@@ -153,8 +153,8 @@ def accumulate_contributions(
         validate_views(views, num_objects)
         return ContributionMatrix(values=np.zeros((num_objects, 0), dtype=np.float32))
     if process_group is not None:
-        # every rank checks every view so all ranks raise the same error
-        validate_views(views, num_objects)
+        # shapes were checked above on every rank; label ranges are checked per
+        # shard and agreed on (distributed.accumulate_shard_checked)
         from .distributed import accumulate_sharded
         values = accumulate_sharded(scene, views, num_objects, blend, process_group,
                                     device=device, stats=stats)

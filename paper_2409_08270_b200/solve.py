@@ -59,13 +59,13 @@ class LabelSolver:
         views = list(views)
         e = int(num_objects)
         n = len(self.scene)
-        if process_group is not None or n == 0:
+        if n == 0:
             validate_views(views, e)
         else:
             check_shapes(views, e)
         ctx = self.ctx
         acc_t = None
-        sel = views
+        mine = None
         if process_group is not None:
             import torch
             import torch.distributed as dist
@@ -73,15 +73,18 @@ class LabelSolver:
             from .distributed import shard_views
             rank = dist.get_rank(process_group)
             world = dist.get_world_size(process_group)
-            sel = [views[i] for i in shard_views(len(views), rank, world)]
+            mine = shard_views(len(views), rank, world)
             acc_t = torch.zeros(e * max(n, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
         with ctx.lock:
             ctx.set_scene(self.scene)
             if acc_t is None:
                 acc_ptr = ctx.buffer("acc64", 8 * e * max(n, 1)).zero().ptr
+                self.stats = run_device_accumulate(ctx, views, e, blend, acc_ptr) if n else {}
             else:
+                from .distributed import accumulate_shard_checked
                 acc_ptr = acc_t.data_ptr()
-            self.stats = run_device_accumulate(ctx, sel, e, blend, acc_ptr) if n else {}
+                self.stats = (accumulate_shard_checked(ctx, views, mine, e, blend, acc_ptr,
+                                                       process_group, ctx.device) if n else {})
         if acc_t is not None:
             import torch.distributed as dist
             dist.all_reduce(acc_t, group=process_group)
