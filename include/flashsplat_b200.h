@@ -174,6 +174,16 @@ int fs_render_mask(fs_context *ctx, const fs_camera *cam, const uint8_t *members
                    int num_objects, double tau, double alpha_floor, double transmittance_floor,
                    uint16_t *labels);
 
+/* ---- mask ingestion ---- */
+
+/* Decode one label-mask PNG held in memory (masks.py:30-40 wire format:
+ * non-interlaced 8- or 16-bit grayscale, pixel value = object id) into
+ * out[height * width] uint16.  out == NULL only reports the dimensions.
+ * Other PNG flavours return FS_EINVAL ("unsupported ...") so the caller can
+ * use a general decoder.  Host-only and thread-safe (no CUDA, no context). */
+int fs_decode_mask_png(const uint8_t *data, int64_t size, uint16_t *out, int64_t out_capacity,
+                       int *width, int *height);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,7 +9,10 @@ Drop-in for the reference package's solver path (``splatlift``):
 * novel-view rendering on the same kernels: ``render_property`` /
   ``render_view`` / ``render_subset_alpha_depth`` (reference
   ``rasterizer.py:133-234``) and ``render_binary_mask`` /
-  ``render_scene_mask`` (reference ``maskrender.py``).
+  ``render_scene_mask`` (reference ``maskrender.py``);
+* mask ingestion: ``load_mask_png`` / ``read_masks`` and the pipelined
+  ``accumulate_mask_files`` (PNG decode on a thread pool overlapped with the
+  device accumulation).
 
 All compute runs in hand-written sm_100a CUDA kernels
 (``csrc/`` -> ``_lib/libflashsplat_b200.so``) behind the C ABI of
@@ -20,6 +23,7 @@ All compute runs in hand-written sm_100a CUDA kernels
 
 from .contributions import ContributionMatrix, LabelMask, accumulate_contributions
 from .maskrender import DEFAULT_TAU, RenderedMask, render_binary_mask, render_scene_mask
+from .masks import accumulate_mask_files, load_mask_png, read_masks, save_mask_png
 from .rasterizer import (
     DEFAULT_BLEND,
     EXACT_BLEND,
@@ -58,6 +62,7 @@ __all__ = [
     "Assignment", "BlendConfig", "CameraView", "ContributionMatrix", "DEFAULT_BLEND",
     "DEFAULT_TAU", "EXACT_BLEND", "Gaussian", "GaussianScene", "LabelMask", "LabelSolver",
     "ProjectedGaussian", "ProjectionStats", "RenderOutput", "RenderedMask", "SceneDataError",
+    "accumulate_mask_files", "load_mask_png", "read_masks", "save_mask_png",
     "SceneFormatError", "TILE_SIZE", "TileBinning", "accumulate_contributions", "assign_binary",
     "assign_scene", "bin_gaussians_to_tiles", "evaluate_alpha", "load_cameras",
     "load_render_grid", "project_gaussian", "project_scene", "render_binary_mask",

@@ -27,6 +27,7 @@ EXPORTS = (
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
     "fs_copy_to_host", "fs_synchronize", "fs_host_alloc", "fs_host_free", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
     "fs_accumulate", "fs_finalize", "fs_assign", "fs_render", "fs_render_splats", "fs_render_mask",
+    "fs_decode_mask_png",
 )
 
 
@@ -108,6 +109,7 @@ def load() -> ctypes.CDLL:
             "fs_render": ([P, P, P, D, D, P, I, P, P, P], I),
             "fs_render_splats": ([P, I, I, I64, P, P, P, P, P, P, D, D, P, I, P, P, P], I),
             "fs_render_mask": ([P, P, P, I, D, D, D, P], I),
+            "fs_decode_mask_png": ([P, I64, P, I64, ctypes.POINTER(I), ctypes.POINTER(I)], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -462,6 +464,20 @@ def render_splats(width: int, height: int, mean2d, conic, depth, opacity, offset
                                        float(alpha_floor), float(t_floor), _p(ch), channels,
                                        _p(value), _p(alpha), _p(dep)))
     return value, alpha, dep
+
+
+def decode_mask_png(data: bytes):
+    """fs_decode_mask_png: uint16 H x W labels, or None for PNG flavours the
+    native decoder does not handle (caller falls back to Pillow)."""
+    L = load()
+    w, h = ctypes.c_int(0), ctypes.c_int(0)
+    buf = ctypes.c_char_p(data)
+    rc = L.fs_decode_mask_png(buf, len(data), None, 0, ctypes.byref(w), ctypes.byref(h))
+    if rc != FS_OK:
+        return None
+    out = np.empty((h.value, w.value), np.uint16)
+    rc = L.fs_decode_mask_png(buf, len(data), _p(out), out.size, ctypes.byref(w), ctypes.byref(h))
+    return out if rc == FS_OK else None
 
 
 def project(means, quats, scales, view, device: int = None):

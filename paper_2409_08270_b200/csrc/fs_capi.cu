@@ -128,6 +128,11 @@ struct fs_context {
 
 
 
+namespace fs {
+// error reporting for the host-only translation units (fs_ingest.cpp)
+int report_error(int code, const char* msg) { return fail(code, "%s", msg); }
+}  // namespace fs
+
 using fs::fail;
 
 namespace {

@@ -126,3 +126,57 @@ def test_render_grid_round_trip(tmp_path):
     path.write_bytes(path.read_bytes()[:-4])
     with pytest.raises(ValueError, match="truncated"):
         load_render_grid(path)
+
+
+def test_mask_png_round_trip_and_errors(tmp_path):
+    """load_mask_png / save_mask_png keep the reference wire format (masks.py:25-40)."""
+    from PIL import Image
+
+    from paper_2409_08270_b200 import CameraView, load_mask_png, read_masks, save_mask_png
+    lab = np.random.default_rng(0).integers(0, 65536, size=(13, 17)).astype(np.uint16)
+    lab[0, 0] = 65535
+    save_mask_png(tmp_path / "0.png", lab)
+    assert np.array_equal(load_mask_png(tmp_path / "0.png"), lab)
+    Image.fromarray(np.full((4, 5), 7, np.uint8)).save(tmp_path / "1.png")  # 8-bit L
+    assert np.array_equal(load_mask_png(tmp_path / "1.png"), np.full((4, 5), 7, np.uint16))
+    Image.fromarray(np.zeros((4, 5, 3), np.uint8)).save(tmp_path / "2.png")  # RGB
+    with pytest.raises(ValueError, match="unsupported mask mode"):
+        load_mask_png(tmp_path / "2.png")
+    views = [CameraView(view_id=i, width=17, height=13, fx=10, fy=10, cx=8, cy=6,
+                        world_to_camera=np.eye(4)) for i in (0, 3, 1)]
+    pairs = read_masks(tmp_path, views, workers=2)  # view 3 has no file: skipped
+    assert [v.view_id for v, _ in pairs] == [0, 1]
+    assert np.array_equal(pairs[0][1].labels, lab)
+
+
+def test_native_png_decoder_matches_pillow():
+    """fs_decode_mask_png (C++, zlib) == Pillow on 8/16-bit grayscale PNGs with every
+    filter mix Pillow produces; palette PNGs are declined (Pillow path)."""
+    import io
+
+    from PIL import Image
+
+    from paper_2409_08270_b200 import _native
+    rng = np.random.default_rng(0)
+    for trial in range(40):
+        h, w = (int(x) for x in rng.integers(1, 200, 2))
+        kind = trial % 4
+        if kind == 0:
+            a = rng.integers(0, 65536, (h, w)).astype(np.uint16)
+        elif kind == 1:
+            a = (rng.integers(0, 4, (h, w)) * 1000).astype(np.uint16)
+        elif kind == 2:
+            a = np.cumsum(rng.integers(0, 3, (h, w)), axis=1).astype(np.uint16)
+        else:
+            a = rng.integers(0, 256, (h, w)).astype(np.uint8)
+        buf = io.BytesIO()
+        Image.fromarray(a).save(buf, format="PNG", optimize=trial % 2 == 0)
+        data = buf.getvalue()
+        ref = np.asarray(Image.open(io.BytesIO(data)).convert("I"), np.int32).astype(np.uint16)
+        got = _native.decode_mask_png(data)
+        assert got is not None and np.array_equal(got, ref)
+    pal = Image.fromarray(rng.integers(0, 5, (9, 9)).astype(np.uint8)).convert("P")
+    buf = io.BytesIO()
+    pal.save(buf, format="PNG")
+    assert _native.decode_mask_png(buf.getvalue()) is None
+    assert _native.decode_mask_png(b"not a png") is None
