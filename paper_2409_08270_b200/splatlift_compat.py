@@ -12,6 +12,7 @@ its FastAPI service and user code run on the B200 kernels unchanged:
     splatlift.rasterizer.*, splatlift.maskrender.*        (maskrender.py:15-21)
     splatlift.render_binary_mask / render_scene_mask,
     splatlift.maskrender.*, splatlift.cli.* (cli.py:19), splatlift.service.* (service.py:24-26)
+    splatlift.load_mask_png, splatlift.masks/cli/metrics   (cli.py:20, metrics.py:10)
 
 The replacement functions accept the reference's own ``GaussianScene``,
 ``CameraView``, ``LabelMask`` and ``ContributionMatrix`` objects (they only
@@ -41,11 +42,15 @@ _TARGETS = {
                            "splatlift.service"],
     "render_scene_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli",
                           "splatlift.service"],
+    "load_mask_png": ["splatlift", "splatlift.masks", "splatlift.cli", "splatlift.metrics"],
 }
 _saved: dict = {}
 
 
 def _replacement(name):
+    if name == "load_mask_png":
+        from .masks import load_mask_png  # same array, native decode of the wire format
+        return load_mask_png
     if name.startswith("render_") and name.endswith("_mask"):
         ref_mask = importlib.import_module("splatlift.maskrender").RenderedMask
         impl = getattr(_maskrender, name)

@@ -64,3 +64,17 @@ def test_install_rebinds_render_import_sites(splatlift):
         splatlift_compat.uninstall()
     assert (rasterizer.render_view, maskrender.render_subset_alpha_depth,
             cli.render_scene_mask) == before
+
+
+def test_install_rebinds_mask_loading(splatlift):
+    from paper_2409_08270_b200 import splatlift_compat
+    import splatlift.cli as cli
+    import splatlift.masks as masks
+    before = masks.load_mask_png
+    splatlift_compat.install()
+    try:
+        for mod in (splatlift, masks, cli):
+            assert mod.load_mask_png.__module__ == "paper_2409_08270_b200.masks"
+    finally:
+        splatlift_compat.uninstall()
+    assert masks.load_mask_png is before
