@@ -24,6 +24,7 @@ All compute runs in hand-written sm_100a CUDA kernels
 from .contributions import ContributionMatrix, LabelMask, accumulate_contributions
 from .maskrender import DEFAULT_TAU, RenderedMask, render_binary_mask, render_scene_mask
 from .masks import accumulate_mask_files, load_mask_png, read_masks, save_mask_png
+from .scene_io import export_ply, load_scene_ply
 from .rasterizer import (
     DEFAULT_BLEND,
     EXACT_BLEND,
@@ -62,7 +63,8 @@ __all__ = [
     "Assignment", "BlendConfig", "CameraView", "ContributionMatrix", "DEFAULT_BLEND",
     "DEFAULT_TAU", "EXACT_BLEND", "Gaussian", "GaussianScene", "LabelMask", "LabelSolver",
     "ProjectedGaussian", "ProjectionStats", "RenderOutput", "RenderedMask", "SceneDataError",
-    "accumulate_mask_files", "load_mask_png", "read_masks", "save_mask_png",
+    "accumulate_mask_files", "load_mask_png", "read_masks", "save_mask_png", "export_ply",
+    "load_scene_ply",
     "SceneFormatError", "TILE_SIZE", "TileBinning", "accumulate_contributions", "assign_binary",
     "assign_scene", "bin_gaussians_to_tiles", "evaluate_alpha", "load_cameras",
     "load_render_grid", "project_gaussian", "project_scene", "render_binary_mask",

@@ -43,6 +43,7 @@ _TARGETS = {
     "render_scene_mask": ["splatlift", "splatlift.maskrender", "splatlift.cli",
                           "splatlift.service"],
     "load_mask_png": ["splatlift", "splatlift.masks", "splatlift.cli", "splatlift.metrics"],
+    "load_scene_ply": ["splatlift", "splatlift.ply", "splatlift.cli"],
 }
 _saved: dict = {}
 
@@ -51,6 +52,17 @@ def _replacement(name):
     if name == "load_mask_png":
         from .masks import load_mask_png  # same array, native decode of the wire format
         return load_mask_png
+    if name == "load_scene_ply":
+        ref_scene = importlib.import_module("splatlift.scene").GaussianScene
+        from .scene_io import load_scene_ply as impl
+
+        def load_scene_ply(path):
+            s = impl(path)  # memory-mapped columns; the caller's own scene type
+            return ref_scene(means=s.means, rotations=s.rotations, scales=s.scales,
+                             opacities=s.opacities, colors_dc=s.colors_dc,
+                             source_path=s.source_path)
+
+        return load_scene_ply
     if name.startswith("render_") and name.endswith("_mask"):
         ref_mask = importlib.import_module("splatlift.maskrender").RenderedMask
         impl = getattr(_maskrender, name)
