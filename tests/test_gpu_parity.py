@@ -401,3 +401,68 @@ def test_label_errors_detected_on_device_in_reference_order():
     # the context stays usable after a label error
     A = accumulate_contributions(g, [(v, ok)], 2).values
     assert A[0, 0] > 0
+
+
+def _oracle_A(wl_scene, pairs, E, blend=DEFAULT_BLEND):
+    cams = [oracle.camera_of(v) for v, _ in pairs]
+    return oracle.accumulate(wl_scene.means, wl_scene.rotations, wl_scene.scales,
+                             wl_scene.opacities, cams, [m.labels for _, m in pairs], E,
+                             blend.alpha_floor, blend.transmittance_floor, threads=8,
+                             as_float32=False)
+
+
+def test_mixed_view_sizes_and_many_labels_per_warp():
+    """Views of different resolutions in one call (workspaces sized per call) and
+    iid masks with up to 40 labels -- warps with > 4 distinct labels take the
+    per-pixel atomic path, warps with <= 4 the grouped reduction."""
+    from paper_2409_08270_b200 import CameraView
+    rng = np.random.default_rng(11)
+    wl = synth.make_workload(seed=12, n_gaussians=8000, n_views=1, width=160, height=120,
+                             num_objects=2)
+    base = wl.views[0]
+    pairs = []
+    for i, (w, h) in enumerate([(160, 120), (333, 77), (48, 300), (1, 1)]):
+        v = CameraView(i, w, h, base.fx * w / 160, base.fy * h / 120, w / 2.0, h / 2.0,
+                       base.world_to_camera)
+        E = 40
+        if i % 2:
+            lab = rng.integers(0, E, size=(h, w)).astype(np.uint16)       # > 4 per warp
+        else:
+            lab = (rng.integers(0, 3, size=(h, w)) * 13).astype(np.uint16)  # <= 3 per warp
+        pairs.append((v, LabelMask(i, lab)))
+    A = accumulate_contributions(wl.scene, pairs, 40).values
+    np.testing.assert_allclose(A, _oracle_A(wl.scene, pairs, 40), rtol=1e-6, atol=1e-9)
+
+
+def test_large_label_ids():
+    """Label ids near the uint16 top (E = 65 000): row addressing in 64-bit."""
+    wl = synth.make_workload(seed=13, n_gaussians=600, n_views=2, width=64, height=48,
+                             num_objects=2)
+    rng = np.random.default_rng(2)
+    pairs = [(v, LabelMask(v.view_id, rng.choice([0, 64_999, 40_000], size=m.labels.shape)
+                           .astype(np.uint16))) for v, m in wl.pairs()]
+    A = accumulate_contributions(wl.scene, pairs, 65_000).values
+    ref = _oracle_A(wl.scene, pairs, 65_000)
+    rows = [0, 40_000, 64_999]
+    np.testing.assert_allclose(A[rows], ref[rows], rtol=1e-6, atol=1e-9)
+    assert A.sum() == pytest.approx(A[rows].sum(), rel=1e-12)
+
+
+def test_near_maximum_tile_count():
+    """A 4096 x 2992 view (47 872 tiles, just under the 49 152 limit)."""
+    from paper_2409_08270_b200 import CameraView
+    rng = np.random.default_rng(3)
+    n = 3000
+    scene = GaussianScene(np.stack([rng.uniform(-2, 2, n), rng.uniform(-1.5, 1.5, n),
+                                    rng.uniform(3, 6, n)], 1),
+                          rng.normal(size=(n, 4)), rng.uniform(0.01, 0.05, (n, 3)),
+                          rng.uniform(0.2, 0.9, n))
+    v = CameraView(0, 4096, 2992, 3000.0, 3000.0, 2048.0, 1496.0, np.eye(4))
+    lab = np.zeros((2992, 4096), np.uint16)
+    lab[:, 2048:] = 1
+    pairs = [(v, LabelMask(0, lab))]
+    A = accumulate_contributions(scene, pairs, 2).values
+    np.testing.assert_allclose(A, _oracle_A(scene, pairs, 2), rtol=1e-6, atol=1e-9)
+    too_big = CameraView(0, 4096, 3200, 3000.0, 3000.0, 2048.0, 1600.0, np.eye(4))
+    with pytest.raises(Exception, match="too large"):
+        accumulate_contributions(scene, [(too_big, LabelMask(0, np.zeros((3200, 4096), np.uint16)))], 2)
