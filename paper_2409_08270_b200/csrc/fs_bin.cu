@@ -261,7 +261,7 @@ void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, 
 
 size_t tile_sort_smem_bytes(unsigned int cap) {
     // packed (key, gid) entries, digit counters, misc, 16-bit entry indices
-    return 8 * (size_t)cap + sizeof(unsigned int) * (2048 + 64) + 2 * (size_t)cap;
+    return 8 * ((size_t)cap + 2) + sizeof(unsigned int) * (2048 + 64) + 2 * (size_t)cap;
 }
 
 cudaError_t tile_sort_configure(unsigned int cap) {

@@ -250,7 +250,7 @@ int ensure_work(fs_context* ctx, fs::Work& w, long long n, int ntiles, unsigned 
         if ((rc = dev_alloc(&w.vc, 1))) return rc;
     }
     if (inst > w.inst_cap) {
-        if ((rc = dev_alloc(&w.inst, inst))) return rc;
+        if ((rc = dev_alloc(&w.inst, (size_t)inst + 2))) return rc;  // +2: bulk-copy slack
         if ((rc = dev_alloc(&w.scratch64, 2 * (size_t)inst))) return rc;
         w.inst_cap = inst;
     }

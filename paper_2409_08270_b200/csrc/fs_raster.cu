@@ -59,7 +59,7 @@ struct RasterSmem {
 
 // The prologue's tile sort (fs_tilesort.cuh) and the walk share the same bytes;
 // sorting inside the raster kernel overlaps its latency with other CTAs' walks.
-constexpr size_t kSortBytes = 10 * (size_t)kTileSortCap + 4 * (2048 + 64);
+constexpr size_t kSortBytes = 8 * ((size_t)kTileSortCap + 2) + 4 * (2048 + 64) + 2 * (size_t)kTileSortCap;
 union RasterShared {
     RasterSmem walk;
     unsigned char sort[kSortBytes];

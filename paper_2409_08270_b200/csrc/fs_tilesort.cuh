@@ -202,6 +202,48 @@ static __device__ __forceinline__ void place_digit_runs(const unsigned long long
     }
 }
 
+// ---- TMA bulk copy of a bucket into shared memory (cp.async.bulk + mbarrier) ----
+static __device__ __forceinline__ unsigned int smem_addr(const void* p) {
+    return (unsigned int)__cvta_generic_to_shared(p);
+}
+
+// Copies in[0, n) (8-byte entries) into shared memory with one bulk-copy
+// instruction issued by thread 0 and completed on an mbarrier; returns where
+// in[0] landed.  The copy starts at the 16-byte aligned address at or below
+// `in` (one extra leading entry when `in` is 8 mod 16) and is rounded up to a
+// multiple of 16 bytes, so the global buffer carries 2 entries of slack and
+// `region` has room for n + 2 entries.  Every thread returns after the data
+// has arrived.
+static __device__ unsigned long long* bulk_load_bucket(const unsigned long long* in, unsigned int n,
+                                                       unsigned long long* region,
+                                                       unsigned long long* bar) {
+    const unsigned int head = (unsigned int)((reinterpret_cast<uintptr_t>(in) >> 3) & 1u);
+    const unsigned int bytes = ((n + head) * 8u + 15u) & ~15u;
+    const unsigned int b = smem_addr(bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(region)), "l"(in - head), "r"(bytes), "r"(b)
+            : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    unsigned int done = 0;
+    while (!done)
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(b)
+            : "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(b) : "memory");
+    return region + head;
+}
+
 // Sorts the instances in[0, n) into the reference order and writes their gids
 // to out[0, n) (out may alias in: every read precedes the first write).
 // smem: at least tile_sort_smem_bytes(cap) bytes; scratch64: 2n entries of
@@ -210,13 +252,14 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
                                                    unsigned long long* scratch64, unsigned int n,
                                                    const TileSortKeys K, unsigned char* smem,
                                                    unsigned int cap) {
-    unsigned long long* a = reinterpret_cast<unsigned long long*>(smem);
-    unsigned int* whist = reinterpret_cast<unsigned int*>(a + cap);
+    unsigned long long* region = reinterpret_cast<unsigned long long*>(smem);  // cap + 2 entries
+    unsigned long long* a = region;
+    unsigned int* whist = reinterpret_cast<unsigned int*>(region + cap + 2);
     unsigned int* misc = whist + 2048;
     unsigned short* b = reinterpret_cast<unsigned short*>(misc + 64);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(misc + 62);
     if (n <= cap) {
-        for (unsigned int i = threadIdx.x; i < n; i += kThreads) a[i] = in[i];
-        __syncthreads();
+        a = bulk_load_bucket(in, n, region, bar);  // TMA: global bucket -> shared memory
         DigitMap m;
         smem_count_sort(a, b, n, whist, misc, &m);
         place_digit_runs(a, b, n, whist, m, K,
