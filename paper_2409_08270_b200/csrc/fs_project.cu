@@ -83,10 +83,14 @@ __device__ __forceinline__ Rec32 screen_record(double mx, double my, double ia, 
     s.b = (float)ib;
     s.c = (float)ic;
     if (alpha_floor > 0.0 && o >= alpha_floor && alive) {
-        const float L = logf((float)o / (float)alpha_floor);  // log(o / floor) >= 0
+        // MUFU log2 / sqrt: a few 1e-7 relative, far inside the margins below
+        const float L = __logf(__fdividef((float)o, (float)alpha_floor));  // log(o / floor) >= 0
         const float qmax = 2.0f * fmaxf(L, 0.0f);
-        const float hx = sqrtf(qmax * (float)ca) * (1.0f + 1e-5f) + 0.01f;
-        const float hy = sqrtf(qmax * (float)cc) * (1.0f + 1e-5f) + 0.01f;
+        float sx, sy;
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sx) : "f"(qmax * (float)ca));
+        asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sy) : "f"(qmax * (float)cc));
+        const float hx = sx * (1.0f + 1e-5f) + 0.01f;
+        const float hy = sy * (1.0f + 1e-5f) + 0.01f;
         const float spread = (fabsf((float)ia) + fabsf((float)ic) + 2.0f * fabsf((float)ib)) *
                              (hx * hx + hy * hy);
         const float margin = 0.02f + 1e-6f * spread;
