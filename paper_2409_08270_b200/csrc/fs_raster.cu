@@ -1,33 +1,39 @@
 // fs_raster.cu -- K3: per-tile front-to-back compositing that scatters alpha*T
 // into the E x N float64 contribution accumulator (reference
-// contributions.py:119-160, the `_accumulate_view` walk).
+// contributions.py:119-160, the `_accumulate_view` walk), and -- instantiated
+// with kRender -- the per-pixel compositing of render_property
+// (rasterizer.py:133-203).
 //
-// One CTA per 16x16 tile (its bucket already depth-ordered by the tile sort,
-// fs_tilesort.cuh), one thread per pixel; warp w owns tile rows 2w and 2w+1.
-// The eight warps walk the tile's list independently -- no block barriers:
+// One CTA per 16x16 tile, launched longest bucket first; prologue: the tile's
+// bucket is TMA-copied into shared memory and sorted into the reference's
+// (depth, id) order (fs_tilesort.cuh).  One thread per pixel; warp w owns tile
+// rows 2w and 2w+1, and the eight warps walk the list independently -- no
+// block barriers after the sort:
 //
-//   gather   32 list entries per step: each lane loads one gid and its float32
-//            screen record, tests the record's alpha-floor ellipse box
-//            against the warp's 2x16 pixel strip, and the hits are appended
-//            (in list order) to a per-warp shared-memory ring;
-//   per mini-batch of 8 ring entries:
-//   A  transposed float32 screen: lane (splat k, row r) solves the quadratic
-//      for the columns of its row whose float32 power clears a conservative
-//      cut -- samples certainly below alpha_floor are dropped (the reference
-//      gives them no weight and no transmittance update, contributions.py:148);
-//   A2 the surviving (splat, pixel) pairs are packed and the exact float64
-//      alpha -- reference expression order, no FMA contraction, float64 exp,
-//      0.99 clamp -- is computed 32 pairs per round (alpha does not depend on
-//      T, so the expensive part runs on full warps);
-//   B  every lane walks its own candidates in list order: alpha floor,
-//      w = alpha*T, T *= (1-alpha), T floor after the update (:148-157);
+//   gather   32 list entries per step (software-pipelined: records one step
+//            ahead, gids two ahead): each lane tests its entry's alpha-floor
+//            ellipse box against the warp's 2x16 strip and solves the float32
+//            quadratic for both rows (conservative margins: samples certainly
+//            below alpha_floor are dropped -- the reference gives them no
+//            weight and no transmittance update, contributions.py:148); hits
+//            with candidate pixels go, in list order, to a per-warp ring;
+//   per mini-batch of 16 hits:
+//   A  their float64 records are staged in shared memory; a warp bit-matrix
+//      transpose gives every lane (pixel) its 16-bit candidate mask; the
+//      (splat, pixel) pairs are packed lane-major by one prefix sum;
+//   A2 exact float64 alpha per pair -- reference expression order, no FMA
+//      contraction, float64 exp, 0.99 clamp, 0 below the floor -- 32 pairs per
+//      round on full warps (alpha does not depend on T);
+//   B  every lane walks its own candidates in list order: w = alpha*T,
+//      T *= (1-alpha), T floor after the update (:150-157);
 //   C  warps with at most 4 distinct labels reduce w per (splat, label) with a
 //      padded transpose in shared memory + a shuffle and issue one float64
 //      atomic each; warps with more labels issue one atomic per contributing
 //      pixel.
 // A warp stops when none of its pixels is active (contributions.py:158-159:
 // pixels are independent, the reference's tile-level break is an
-// optimisation of the same rule).
+// optimisation of the same rule).  The label range check of
+// contributions.py:108-114 runs here too, for every tile.
 #include <algorithm>
 
 #include "fs_common.cuh"
@@ -68,10 +74,6 @@ union RasterShared {
 constexpr size_t kRasterSmem = sizeof(RasterShared);
 static_assert(4 * (kRasterSmem + 1024) <= 228 * 1024, "raster needs 4 resident CTAs per SM");
 
-// Candidate columns of one pixel row for one splat: the pixels whose float32
-// power clears the conservative cut, from the roots of the quadratic
-//   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
-// (widened by float32 rounding margins).  Returns a 16-bit column mask.
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -91,6 +93,10 @@ __device__ __forceinline__ unsigned int warp_transpose32(unsigned int x, int lan
     return x;
 }
 
+// Candidate columns of one pixel row for one splat: the pixels whose float32
+// power clears the conservative cut, from the roots of the quadratic
+//   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
+// (widened by float32 rounding margins).  Returns a 16-bit column mask.
 __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0) {
     if (!(s.cut > -INFINITY)) return 0xFFFFu;  // exact blend: no alpha floor
     const float dv = v_centre - s.my;
