@@ -3,9 +3,10 @@
 ``accumulate_contributions`` keeps the reference signature
 (``contributions.py:90-95``), validation order and messages
 (``contributions.py:104-114``) and result type; the work runs in the CUDA
-library (``fs_accumulate``: projection, depth/tile radix sorts and the
-raster-accumulate kernel per view, float64 accumulation on the device, one
-float32 cast at the end -- ``contributions.py:116``).
+library (``fs_accumulate``: projection, tile binning and the raster kernel --
+in-kernel per-tile depth sort, exact float64 walk, atomics -- per view,
+float64 accumulation on the device, one float32 cast at the end --
+``contributions.py:116``).
 
 Views are independent and A is additive over views
 (``contributions.py:103-116``), so with ``process_group`` set (a

@@ -3,8 +3,9 @@
 // One fs_context owns a CUDA device, S streams and one workspace per stream.
 // fs_accumulate hands views out round-robin to the streams; each view runs
 // the device pipeline
-//     K1 project -> K2a depth radix sort -> K2b emit instances ->
-//     K2c tile radix sort -> K2d tile ranges -> K3 raster-accumulate
+//     K1 project -> K2a per-block tile histograms -> K2b per-tile scans ->
+//     K2c bucket starts + launch order -> K2d emit instances ->
+//     K3 raster (in-kernel bucket sort, walk, atomics, label check)
 // entirely on its stream with device-side counts (no host sync inside the
 // loop).  Host masks are staged through a pinned buffer per stream and
 // copied on the same stream, so the copy of view v+S overlaps the kernels of
@@ -94,7 +95,6 @@ struct fs_context {
     double* mz = nullptr;
     double* sig = nullptr;
     double* opac = nullptr;
-    unsigned long long* tile_oa_table = nullptr;  // [33][2] = {(1<<b)-1, 0}
     fs::ViewCounters* view_log = nullptr;
     int view_log_cap = 0;
     std::vector<fs::Work> work;
@@ -329,7 +329,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
     const int n = (int)ctx->n;
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
-                       cull_floor, w.k64, nullptr, w.rect, nullptr, w.r32, w.r64, w.vc, ex,
+                       cull_floor, w.k64, w.rect, w.r32, w.r64, w.vc, ex,
                        ctx->num_sms, w.stream);
     if (after_project) cudaEventRecord(after_project, w.stream);
     fs::launch_bin(ntiles, tx, bin_buffers(w, n), w.vc, ctx->num_sms, w.stream);
@@ -425,17 +425,6 @@ int fs_create(int device, int n_streams, fs_context** out) {
     }
     CK(cudaEventCreate(&ctx->ev_start));
     CK(cudaEventCreate(&ctx->ev_stop));
-    unsigned long long table[33 * 2];
-    for (int b = 0; b <= 32; ++b) {
-        table[2 * b] = b == 32 ? 0xFFFFFFFFull : ((1ull << b) - 1ull);
-        table[2 * b + 1] = 0ull;
-    }
-    int rc = dev_alloc(&ctx->tile_oa_table, 66);
-    if (rc) {
-        fs_destroy(ctx);
-        return rc;
-    }
-    CK(cudaMemcpy(ctx->tile_oa_table, table, sizeof(table), cudaMemcpyHostToDevice));
     *out = ctx;
     return FS_OK;
 }
@@ -446,7 +435,7 @@ void fs_destroy(fs_context* ctx) {
     cudaDeviceSynchronize();
     for (auto& w : ctx->work) free_work(w);
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
-                    (void*)ctx->opac, (void*)ctx->tile_oa_table, (void*)ctx->view_log,
+                    (void*)ctx->opac, (void*)ctx->view_log,
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
                     (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out,
                     (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
@@ -576,7 +565,7 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
         (rc = dev_alloc(&ex.radius, n1)))
         return rc;
     fs::launch_project((int)n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, to_cam(*cam), 0.0,
-                       0, w.k64, nullptr, w.rect, nullptr, w.r32, w.r64, w.vc, ex,
+                       0, w.k64, w.rect, w.r32, w.r64, w.vc, ex,
                        ctx->num_sms, w.stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(w.stream));

@@ -36,8 +36,8 @@ void launch_scene_setup(int n, const double* means, const double* quats, const d
                         double* mx, double* my, double* mz, double* sig, cudaStream_t st);
 void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
-                    int cull_floor, unsigned long long* keys, unsigned int* vals,
-                    unsigned long long* rect, unsigned int* tile_count, Rec32* r32, Rec64* r64,
+                    int cull_floor, unsigned long long* keys, unsigned long long* rect,
+                    Rec32* r32, Rec64* r64,
                     ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st);
 void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 void launch_splat_records(int k, const double* mean2d, const double* conic, const double* depth,

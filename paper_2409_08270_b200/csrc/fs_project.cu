@@ -119,8 +119,7 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
     int n, const double* __restrict__ gmx, const double* __restrict__ gmy,
     const double* __restrict__ gmz, const double* __restrict__ sig,
     const double* __restrict__ opac, Camera cam, double alpha_floor, int cull_floor,
-    unsigned long long* __restrict__ keys, unsigned int* __restrict__ vals,
-    unsigned long long* __restrict__ rect, unsigned int* __restrict__ tile_count,
+    unsigned long long* __restrict__ keys, unsigned long long* __restrict__ rect,
     Rec32* __restrict__ r32, Rec64* __restrict__ r64, ViewCounters* __restrict__ vc,
     ProjectExport ex) {
     const double* W = cam.w2c;
@@ -210,10 +209,8 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
                 // tile_range (rasterizer.py:106-113), inclusive floor box
                 const bool transparent = cull_floor && alpha_floor > 0.0 && !(o >= alpha_floor);
                 if (!transparent) rc = tile_rect(mxp, myp, rad, tx_n, ty_n);
-                count_rect_tiles(rc, tx_n, tile_count);
             }
             keys[i] = key;
-            if (vals) vals[i] = (unsigned int)i;
             rect[i] = rc;
             // walk records (float64 exact, float32 screen)
             Rec64 q;
@@ -289,8 +286,8 @@ void launch_scene_setup(int n, const double* means, const double* quats, const d
 
 void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
-                    int cull_floor, unsigned long long* keys, unsigned int* vals,
-                    unsigned long long* rect, unsigned int* tile_count, Rec32* r32, Rec64* r64,
+                    int cull_floor, unsigned long long* keys, unsigned long long* rect,
+                    Rec32* r32, Rec64* r64,
                     ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st) {
     view_begin_kernel<<<1, 32, 0, st>>>(vc);
     if (n <= 0) return;
@@ -298,7 +295,7 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
     int cap = num_sms * 8;
     if (grid > cap) grid = cap;
     project_kernel<<<grid, 256, 0, st>>>(n, mx, my, mz, sig, opac, cam, alpha_floor, cull_floor,
-                                         keys, vals, rect, tile_count, r32, r64, vc, ex);
+                                         keys, rect, r32, r64, vc, ex);
 }
 
 // Records of an explicit splat list (render_property over a caller's
