@@ -30,6 +30,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBinThreads = 1024;  // count / emit: latency-bound gid walks, full occupancy
+constexpr int kUnroll = 4;         // gids per thread with their loads issued together
 
 __device__ __forceinline__ void gid_range(int n, int b, int g, int& lo, int& hi) {
     const long long per = ((long long)n + g - 1) / g;
@@ -52,7 +53,17 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinBuffers b, in
     __syncthreads();
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
-    for (int g = lo + threadIdx.x; g < hi; g += kBinThreads) count_rect_tiles(b.rect[g], tiles_x, s_hist);
+    // kUnroll independent loads in flight per thread (the walk is latency-bound)
+    for (int g0 = lo + threadIdx.x; g0 < hi; g0 += kUnroll * kBinThreads) {
+        unsigned long long rc[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {
+            const int g = g0 + j * kBinThreads;
+            rc[j] = g < hi ? b.rect[g] : ~0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) count_rect_tiles(rc[j], tiles_x, s_hist);
+    }
     __syncthreads();
     for (int t = threadIdx.x; t < ntiles; t += kBinThreads)
         b.count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
@@ -174,18 +185,27 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int
     const unsigned long long z = b.key_oa[1];
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
-    for (int g = lo + threadIdx.x; g < hi; g += kBinThreads) {
-        const unsigned long long rc = b.rect[g];
-        if (rc == ~0ull) continue;
-        unsigned long long key = b.k64[g];
-        if (key == ~0ull) key = z;
-        // instance = (32-bit primary depth key, gid)
-        const unsigned long long e = ((key >> shift) << 32) | (unsigned int)g;
-        const unsigned int tx0 = rc & 0xFFFF, tx1 = (rc >> 16) & 0xFFFF;
-        const unsigned int ty0 = (rc >> 32) & 0xFFFF, ty1 = (rc >> 48) & 0xFFFF;
-        for (unsigned int ty = ty0; ty <= ty1; ++ty)
-            for (unsigned int tx = tx0; tx <= tx1; ++tx)
-                b.inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = e;
+    for (int g0 = lo + threadIdx.x; g0 < hi; g0 += kUnroll * kBinThreads) {
+        unsigned long long rc[kUnroll], key[kUnroll];
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {  // all loads first: kUnroll in flight
+            const int g = g0 + j * kBinThreads;
+            rc[j] = g < hi ? b.rect[g] : ~0ull;
+            key[j] = g < hi ? b.k64[g] : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < kUnroll; ++j) {
+            const unsigned long long r = rc[j];
+            if (r == ~0ull) continue;
+            const unsigned long long k = key[j] == ~0ull ? z : key[j];
+            // instance = (32-bit primary depth key, gid)
+            const unsigned long long e = ((k >> shift) << 32) | (unsigned int)(g0 + j * kBinThreads);
+            const unsigned int tx0 = r & 0xFFFF, tx1 = (r >> 16) & 0xFFFF;
+            const unsigned int ty0 = (r >> 32) & 0xFFFF, ty1 = (r >> 48) & 0xFFFF;
+            for (unsigned int ty = ty0; ty <= ty1; ++ty)
+                for (unsigned int tx = tx0; tx <= tx1; ++tx)
+                    b.inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = e;
+        }
     }
 }
 
