@@ -40,7 +40,7 @@ __device__ __forceinline__ void gid_range(int n, int b, int g, int& lo, int& hi)
 
 // Primary key: the 32 highest bits in which the view's depth keys differ.
 __device__ __forceinline__ int primary_shift(const unsigned long long* oa) {
-    const unsigned long long vary = oa[0] ^ oa[1];
+    const unsigned long long vary = oa[0] ^ ~oa[1];  // OR ^ AND
     const int hb = vary ? 63 - __clzll((long long)vary) : 0;
     return hb > 31 ? hb - 31 : 0;
 }
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int
         s_cur[t] = b.tile_start[t] + b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
     __syncthreads();
     const int shift = primary_shift(b.key_oa);
-    const unsigned long long z = b.key_oa[1];
+    const unsigned long long z = ~b.key_oa[1];  // AND of the visible keys
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
     for (int g0 = lo + threadIdx.x; g0 < hi; g0 += kUnroll * kBinThreads) {
@@ -227,7 +227,7 @@ __device__ __forceinline__ void block_or_and(unsigned long long o, unsigned long
     }
     if ((threadIdx.x & 31) == 0) {
         atomicOr(dst, o);
-        atomicAnd(dst + 1, a);
+        atomicOr(dst + 1, ~a);
     }
 }
 

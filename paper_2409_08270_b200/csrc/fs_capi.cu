@@ -42,10 +42,6 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
-__global__ void view_end_kernel(const ViewCounters* vc, ViewCounters* log) {
-    if (threadIdx.x == 0) *log = *vc;
-}
-
 int bits_for(unsigned int v) {  // bits needed to represent values 0..v
     int b = 0;
     while (b < 32 && (v >> b) != 0u) ++b;
@@ -295,12 +291,14 @@ int check_cam(const fs_camera& c, int idx) {
     return FS_OK;
 }
 
-fs::BinBuffers bin_buffers(fs::Work& w, int n) {
+// vc: the view's counters (the workspace's own, or a slot of the view log)
+fs::BinBuffers bin_buffers(fs::Work& w, int n, fs::ViewCounters* vc = nullptr) {
+    if (!vc) vc = w.vc;
     fs::BinBuffers b;
     b.n = n;
     b.rect = w.rect;
     b.k64 = w.k64;
-    b.key_oa = &w.vc->key_or;  // key_or, key_and are adjacent
+    b.key_oa = &vc->key_or;  // key_or, key_nand are adjacent
     b.count_bt = w.count_bt;
     b.tile_total = w.tile_total;
     b.tile_order = w.tile_order;
@@ -310,7 +308,8 @@ fs::BinBuffers bin_buffers(fs::Work& w, int n) {
     return b;
 }
 
-fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr) {
+fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr,
+                                fs::ViewCounters* vc = nullptr) {
     fs::TileSortArgs t;
     t.tile_start = w.tile_start;
     t.inst = w.inst;
@@ -318,31 +317,37 @@ fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr) 
     t.keys.k64 = w.k64;
     t.keys.tie = tie;
     t.cap = fs::kTileSortCap;
-    t.vc = w.vc;
+    t.vc = vc ? vc : w.vc;
     return t;
 }
 
 // Projection + per-tile buckets of one view on workspace w (the buckets are
 // depth-ordered by the raster prologue or launch_tile_sort).
+// vc == nullptr: the workspace's counters, reset first; otherwise the caller's
+// zeroed slot (the accumulate loop's view log -- no reset/copy kernels per view).
 void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
-                 int cull_floor, fs::ProjectExport ex, cudaEvent_t after_project = nullptr) {
+                 int cull_floor, fs::ProjectExport ex, cudaEvent_t after_project = nullptr,
+                 fs::ViewCounters* vc = nullptr) {
     const int n = (int)ctx->n;
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
+    const bool own = vc == nullptr;
+    if (own) vc = w.vc;
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
-                       cull_floor, w.k64, w.rect, w.r32, w.r64, w.vc, ex,
-                       ctx->num_sms, w.stream);
+                       cull_floor, w.k64, w.rect, w.r32, w.r64, vc, ex,
+                       ctx->num_sms, w.stream, own);
     if (after_project) cudaEventRecord(after_project, w.stream);
-    fs::launch_bin(ntiles, tx, bin_buffers(w, n), w.vc, ctx->num_sms, w.stream);
+    fs::launch_bin(ntiles, tx, bin_buffers(w, n, vc), vc, ctx->num_sms, w.stream);
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
-int view_launches() { return 1 + 1 + 4 + 1 + 1; }
+int view_launches() { return 1 + 4 + 1; }
 
+// One view of fs_accumulate; its counters live in `log` (zeroed by the caller).
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
                   int num_objects, double alpha_floor, double t_floor, double* acc,
                   fs::ViewCounters* log, cudaEvent_t* ev = nullptr) {
     if (ev) cudaEventRecord(ev[0], w.stream);
-    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr);
+    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr, log);
     if (ev) cudaEventRecord(ev[2], w.stream);
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     fs::RasterArgs ra{};
@@ -355,15 +360,14 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.af_eff = alpha_floor > 0.0 ? alpha_floor : -1.0;  // contributions.py:148-149
     ra.tf_eff = t_floor > 0.0 ? t_floor : -1.0;          // contributions.py:156-157
     ra.mask = mask;
-    ra.sort = tile_sort_args(w);
+    ra.sort = tile_sort_args(w, nullptr, log);
     ra.r32 = w.r32;
     ra.r64 = w.r64;
     ra.acc = acc;
-    ra.vc = w.vc;
+    ra.vc = log;
     ra.tile_order = w.tile_order;
     fs::launch_raster(ra, w.stream);
     if (ev) cudaEventRecord(ev[3], w.stream);
-    if (log) fs::view_end_kernel<<<1, 32, 0, w.stream>>>(w.vc, log);
 }
 
 unsigned int initial_inst_cap(long long n) {
@@ -737,7 +741,8 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
             ctx->stage_events.push_back(e);
         }
     }
-    long long launches = 0;
+    long long launches = 0;  // our kernels (the log memset is a driver memset)
+    CK(cudaMemsetAsync(ctx->view_log, 0, sizeof(fs::ViewCounters) * (size_t)n_views, w0.stream));
     CK(cudaEventRecord(ctx->ev_start, w0.stream));
     for (int s = 1; s < S; ++s) CK(cudaStreamWaitEvent(ctx->work[s].stream, ctx->ev_start, 0));
     for (int v = 0; v < n_views; ++v) {
@@ -799,6 +804,7 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
             CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
             mask = w.mask_dev;
         }
+        CK(cudaMemsetAsync(ctx->view_log + v, 0, sizeof(fs::ViewCounters), w.stream));
         enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
                      ctx->view_log + v);
         CK(cudaGetLastError());

@@ -43,7 +43,7 @@ struct __align__(16) Rec64 {
 // Per-view device counters (reset at the start of every view).
 struct ViewCounters {
     unsigned long long key_or;   // OR of visible depth keys
-    unsigned long long key_and;  // AND of visible depth keys
+    unsigned long long key_nand; // OR of the complemented keys (= ~AND): all-zero is the empty state
     unsigned int n_emitted;      // visible after all culls (scene.py:311)
     unsigned int n_behind;
     unsigned int n_degenerate;

@@ -38,7 +38,8 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
                     int cull_floor, unsigned long long* keys, unsigned long long* rect,
                     Rec32* r32, Rec64* r64,
-                    ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st);
+                    ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st,
+                    bool reset_counters = true);
 void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 void launch_splat_records(int k, const double* mean2d, const double* conic, const double* depth,
                           const double* opac, double alpha_floor, Rec32* r32, Rec64* r64,
@@ -52,7 +53,7 @@ struct BinBuffers {
     int n;                              // Gaussians (or splats)
     const unsigned long long* rect;     // per gid
     const unsigned long long* k64;      // per gid: order-preserving float64 depth key
-    const unsigned long long* key_oa;   // {OR, AND} of the visible depth keys
+    const unsigned long long* key_oa;   // {OR, ~AND} of the visible depth keys
     unsigned int* count_bt;             // ntiles x bin_blocks(): counts, then offsets in the tile
     unsigned int* tile_total;           // ntiles: bucket lengths
     unsigned int* tile_start;           // ntiles + 1

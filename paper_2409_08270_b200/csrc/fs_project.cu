@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
         }
         if (s_cnt[0]) {
             atomicOr(&vc->key_or, o);
-            atomicAnd(&vc->key_and, a);
+            atomicOr(&vc->key_nand, ~a);
             atomicAdd(&vc->n_emitted, s_cnt[0]);
         }
         if (s_cnt[1]) atomicAdd(&vc->n_behind, s_cnt[1]);
@@ -268,9 +268,7 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
 __global__ void view_begin_kernel(ViewCounters* vc) {
     if (threadIdx.x == 0) {
         ViewCounters z{};
-        z.key_or = 0;
-        z.key_and = ~0ull;
-        *vc = z;
+        *vc = z;  // every field's empty state is zero
     }
 }
 
@@ -288,8 +286,9 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
                     int cull_floor, unsigned long long* keys, unsigned long long* rect,
                     Rec32* r32, Rec64* r64,
-                    ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st) {
-    view_begin_kernel<<<1, 32, 0, st>>>(vc);
+                    ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st,
+                    bool reset_counters) {
+    if (reset_counters) view_begin_kernel<<<1, 32, 0, st>>>(vc);
     if (n <= 0) return;
     int grid = (n + 255) / 256;
     int cap = num_sms * 8;
