@@ -466,3 +466,23 @@ def test_near_maximum_tile_count():
     too_big = CameraView(0, 4096, 3200, 3000.0, 3000.0, 2048.0, 1600.0, np.eye(4))
     with pytest.raises(Exception, match="too large"):
         accumulate_contributions(scene, [(too_big, LabelMask(0, np.zeros((3200, 4096), np.uint16)))], 2)
+
+
+@pytest.mark.parametrize("blend", [DEFAULT_BLEND, EXACT_BLEND], ids=["default", "exact"])
+def test_needle_splats_screen_is_conservative(blend):
+    """Long thin rotated splats (conic determinant ~1e-3 of a*c after the 0.3 px
+    dilation) stress the float32 row screen's margins: nothing the exact
+    float64 walk keeps may be screened out."""
+    from paper_2409_08270_b200 import CameraView
+    rng = np.random.default_rng(17)
+    n = 400
+    means = np.stack([rng.uniform(-0.6, 0.6, n), rng.uniform(-0.45, 0.45, n),
+                      rng.uniform(1.5, 3.0, n)], 1)
+    scales = np.stack([rng.uniform(0.0005, 0.002, n), rng.uniform(0.2, 0.8, n),
+                       rng.uniform(0.0005, 0.002, n)], 1)
+    scene = GaussianScene(means, rng.normal(size=(n, 4)), scales, rng.uniform(0.3, 0.99, n))
+    v = CameraView(0, 320, 240, 300.0, 300.0, 160.0, 120.0, np.eye(4))
+    lab = (np.arange(320)[None, :] // 40 % 3 + np.zeros((240, 1))).astype(np.uint16)
+    pairs = [(v, LabelMask(0, lab))]
+    A = accumulate_contributions(scene, pairs, 3, blend).values
+    np.testing.assert_allclose(A, _oracle_A(scene, pairs, 3, blend), rtol=1e-6, atol=1e-9)
