@@ -63,9 +63,9 @@ typedef struct {
     int64_t label_error_view; /* first view with a label >= num_objects, or -1 */
     double gpu_ms;            /* CUDA-event time of the view loop on the device */
     /* per-stage CUDA-event times summed over views; only with fs_set_timing(ctx, 1) */
-    double prep_ms;           /* projection + depth radix sort */
-    double bin_ms;            /* instance emission + tile radix sort + tile ranges */
-    double raster_ms;         /* raster-accumulate kernel */
+    double prep_ms;           /* projection */
+    double bin_ms;            /* tile histograms, bucket offsets, instance emission */
+    double raster_ms;         /* raster kernel (in-kernel bucket sort + walk + atomics) */
 } fs_accumulate_stats;
 
 const char *fs_last_error(void);
