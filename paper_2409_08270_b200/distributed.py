@@ -60,7 +60,8 @@ def accumulate_shard_checked(ctx, views: Sequence, mine: Sequence, num_objects: 
                             blend.alpha_floor, blend.transmittance_floor, acc_ptr)
     except _native.LabelRangeError as err:
         bad = int(mine[err.view])
-    t = torch.tensor([bad], dtype=torch.int64, device=f"cuda:{device}")
+    on = "cpu" if dist.get_backend(group) == "gloo" else f"cuda:{device}"
+    t = torch.tensor([bad], dtype=torch.int64, device=on)
     dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
     first = int(t.item())
     if first != _NO_ERROR:
