@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(kThreads) tile_sort_kernel(TileSortArgs t) {
     const unsigned int begin = t.tile_start[tile], end = t.tile_start[tile + 1];
     if (begin >= end) return;
     sort_tile_list(t.inst + begin, sorted_view(t.inst, begin), t.scratch64 + 2ull * begin, end - begin,
-                   t.keys, smem_raw, t.cap);
+                   t.keys, smem_raw, t.cap,
+                   8 * ((size_t)t.cap + 2) + sizeof(unsigned int) * (2048 + 64) + 2 * (size_t)t.cap);
 }
 
 __device__ __forceinline__ void block_or_and(unsigned long long o, unsigned long long a,

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         // prologue: the tile's bucket -> gids in the reference (depth, id) order
         unsigned int* sorted = sorted_view(a.sort.inst, begin);
         sort_tile_list(a.sort.inst + begin, sorted, a.sort.scratch64 + 2ull * begin, n_list,
-                       a.sort.keys, SH.sort, a.sort.cap);
+                       a.sort.keys, SH.sort, a.sort.cap, kRasterSmem);
         list = sorted;
     }
     WarpSmem& W = S.w[warp];

@@ -5,6 +5,7 @@
 // A bucket holds the gids whose tile rectangle covers the tile, in arbitrary
 // order.  The reference order is np.lexsort((index, depth)) with float64 depth
 // (rasterizer.py:91).  Per tile:
+//   0. the bucket comes into shared memory by one TMA bulk copy;
 //   1. single-pass counting sort (shared memory, 2048 buckets) of
 //      (primary << 32 | gid) by an 11-bit digit that is monotone in the 32-bit
 //      primary key (= the 32 highest bits in which the view's float64 depth
@@ -13,8 +14,10 @@
 //      order (primary key, full 64-bit depth key, tie id) -- tie id = gid for
 //      scenes, the splat's gaussian_index for explicit splat lists -- each
 //      thread ranking its own entries, so runs cost no serial passes.
-// Buckets longer than `cap` are sorted in chunks and merged through global
-// memory before step 2.  The result is exactly the reference's tile list.
+// Buckets longer than `cap` keep only their primary keys in shared memory
+// (up to ~7 300 entries in the raster kernel's 52 KB); longer ones are sorted
+// in chunks and merged through global memory.  The result is exactly the
+// reference's tile list.
 #pragma once
 
 #include "fs_common.cuh"
@@ -122,22 +125,16 @@ static __device__ __forceinline__ unsigned int digit_of(unsigned int pk, DigitMa
     return (pk - m.lo) >> m.shift;
 }
 
-static __device__ __forceinline__ bool full_less(unsigned long long x, unsigned long long y,
-                                                 const TileSortKeys K) {
-    const unsigned int px = pk_of(x), py = pk_of(y);
-    if (px != py) return px < py;
-    return entry_less(x, y, K);
-}
 
 // a[0, n) -> b[0, n): indices into a, grouped by digit (unordered within a
 // digit); hist[d] is left at the end offset of digit d.
-static __device__ void smem_count_sort(const unsigned long long* a, unsigned short* b,
-                                       unsigned int n, unsigned int* hist, unsigned int* s_misc,
-                                       DigitMap* map) {
+template <class PK>
+static __device__ void smem_count_sort(PK pk, unsigned short* b, unsigned int n,
+                                       unsigned int* hist, unsigned int* s_misc, DigitMap* map) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned int lo = 0xFFFFFFFFu, hi = 0;
     for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
-        const unsigned int k = pk_of(a[i]);
+        const unsigned int k = pk(i);
         lo = min(lo, k);
         hi = max(hi, k);
     }
@@ -158,7 +155,7 @@ static __device__ void smem_count_sort(const unsigned long long* a, unsigned sho
     const int bits = range ? 32 - __clz(range) : 0;
     const DigitMap m{lo, bits > 11 ? (unsigned int)(bits - 11) : 0u};
     *map = m;
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&hist[digit_of(pk_of(a[i]), m)], 1u);
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) atomicAdd(&hist[digit_of(pk(i), m)], 1u);
     __syncthreads();
     unsigned int c[8], sum = 0;
 #pragma unroll
@@ -174,7 +171,7 @@ static __device__ void smem_count_sort(const unsigned long long* a, unsigned sho
     }
     __syncthreads();
     for (unsigned int i = threadIdx.x; i < n; i += kThreads)
-        b[atomicAdd(&hist[digit_of(pk_of(a[i]), m)], 1u)] = (unsigned short)i;
+        b[atomicAdd(&hist[digit_of(pk(i), m)], 1u)] = (unsigned short)i;
     __syncthreads();
 }
 
@@ -183,22 +180,27 @@ static __device__ void smem_count_sort(const unsigned long long* a, unsigned sho
 // ranked within the run by the full order (r comparisons each, all threads in
 // parallel).  hist[d] = end offset of digit d (as left by smem_count_sort).
 // store(pos, entry) receives every entry exactly once.
-template <class Store>
-static __device__ __forceinline__ void place_digit_runs(const unsigned long long* a,
-                                                        const unsigned short* idx, unsigned int n,
-                                                        const unsigned int* hist, DigitMap m,
-                                                        const TileSortKeys K, Store store) {
+template <class PK, class Entry, class Store>
+static __device__ __forceinline__ void place_digit_runs(PK pk, Entry entry, const unsigned short* idx,
+                                                        unsigned int n, const unsigned int* hist,
+                                                        DigitMap m, const TileSortKeys K,
+                                                        Store store) {
     for (unsigned int p = threadIdx.x; p < n; p += kThreads) {
-        const unsigned long long v = a[idx[p]];
-        const unsigned int d = digit_of(pk_of(v), m);
+        const unsigned int i = idx[p];
+        const unsigned int key = pk(i);
+        const unsigned int d = digit_of(key, m);
         const unsigned int s = d ? hist[d - 1] : 0u, t = hist[d];
         unsigned int pos = p;
         if (t - s > 1u) {
             pos = s;
-            for (unsigned int q = s; q < t; ++q)  // (skipping itself: equal keys take the slow path)
-                pos += (q != p && full_less(a[idx[q]], v, K)) ? 1u : 0u;
+            for (unsigned int q = s; q < t; ++q) {
+                if (q == p) continue;  // (itself: equal keys would take the slow path)
+                const unsigned int j = idx[q], kj = pk(j);
+                // primary key first; only equal primaries consult the full entries
+                pos += (kj != key ? kj < key : entry_less(entry(j), entry(i), K)) ? 1u : 0u;
+            }
         }
-        store(pos, v);
+        store(pos, i);
     }
 }
 
@@ -251,7 +253,7 @@ static __device__ unsigned long long* bulk_load_bucket(const unsigned long long*
 static __device__ __noinline__ void sort_tile_list(const unsigned long long* in, unsigned int* out,
                                                    unsigned long long* scratch64, unsigned int n,
                                                    const TileSortKeys K, unsigned char* smem,
-                                                   unsigned int cap) {
+                                                   unsigned int cap, size_t smem_bytes) {
     unsigned long long* region = reinterpret_cast<unsigned long long*>(smem);  // cap + 2 entries
     unsigned long long* a = region;
     unsigned int* whist = reinterpret_cast<unsigned int*>(region + cap + 2);
@@ -260,10 +262,36 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(misc + 62);
     if (n <= cap) {
         a = bulk_load_bucket(in, n, region, bar);  // TMA: global bucket -> shared memory
+        const unsigned long long* sa = a;
+        auto pk = [sa](unsigned int i) { return pk_of(sa[i]); };
+        auto entry = [sa](unsigned int i) { return sa[i]; };
         DigitMap m;
-        smem_count_sort(a, b, n, whist, misc, &m);
-        place_digit_runs(a, b, n, whist, m, K,
-                         [&](unsigned int pos, unsigned long long v) { out[pos] = (unsigned int)v; });
+        smem_count_sort(pk, b, n, whist, misc, &m);
+        place_digit_runs(pk, entry, b, n, whist, m, K,
+                         [&](unsigned int pos, unsigned int i) { out[pos] = (unsigned int)sa[i]; });
+        __syncthreads();
+        return;
+    }
+    // medium bucket: only the 32-bit primary keys (+ 16-bit indices) in shared
+    // memory, which holds up to `cap2` entries; gids come from the global bucket,
+    // the ordered gids pass through the (global) scratch
+    const unsigned int cap2 = (unsigned int)((smem_bytes - 4u * (2048 + 64)) / 6u);
+    if (n <= cap2) {
+        unsigned int* hist2 = reinterpret_cast<unsigned int*>(smem);
+        unsigned int* misc2 = hist2 + 2048;
+        unsigned int* pks = misc2 + 64;
+        unsigned short* idx2 = reinterpret_cast<unsigned short*>(pks + cap2);
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) pks[i] = pk_of(in[i]);
+        __syncthreads();
+        auto pk = [pks](unsigned int i) { return pks[i]; };
+        auto entry = [in](unsigned int i) { return in[i]; };
+        unsigned int* tmp = reinterpret_cast<unsigned int*>(scratch64);
+        DigitMap m;
+        smem_count_sort(pk, idx2, n, hist2, misc2, &m);
+        place_digit_runs(pk, entry, idx2, n, hist2, m, K,
+                         [&](unsigned int pos, unsigned int i) { tmp[pos] = (unsigned int)in[i]; });
+        __syncthreads();  // every read of `in` is done before `out` (aliasing it) is written
+        for (unsigned int i = threadIdx.x; i < n; i += kThreads) out[i] = tmp[i];
         __syncthreads();
         return;
     }
@@ -274,10 +302,14 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
         const unsigned int m = min(cap, n - c0);
         for (unsigned int i = threadIdx.x; i < m; i += kThreads) a[i] = in[c0 + i];
         __syncthreads();
+        const unsigned long long* sa = a;
+        auto pk = [sa](unsigned int i) { return pk_of(sa[i]); };
+        auto entry = [sa](unsigned int i) { return sa[i]; };
         DigitMap dm;
-        smem_count_sort(a, b, m, whist, misc, &dm);
+        smem_count_sort(pk, b, m, whist, misc, &dm);
         unsigned long long* dst = g0 + c0;  // chunk fully ordered
-        place_digit_runs(a, b, m, whist, dm, K, [&](unsigned int pos, unsigned long long v) { dst[pos] = v; });
+        place_digit_runs(pk, entry, b, m, whist, dm, K,
+                         [&](unsigned int pos, unsigned int i) { dst[pos] = sa[i]; });
         __syncthreads();
     }
     unsigned long long* src = g0;

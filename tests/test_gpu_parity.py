@@ -325,12 +325,13 @@ def test_label_solver_resident_matrix():
     assert np.array_equal(asn.labels, oracle.assign_binary(M2.values, 0.2))
 
 
-def test_long_tile_buckets_merge_path():
-    # ~10k splats on a 64x48 image: every tile bucket exceeds the 4096-entry
-    # shared-memory sort, exercising the chunk sort + global merge path
+@pytest.mark.parametrize("n", [5000, 10000], ids=["medium", "merge"])
+def test_long_tile_buckets_merge_path(n):
+    # n splats on a 64x48 image with 50 distinct depths (many primary-key ties):
+    # every tile bucket exceeds the 3584-entry in-smem sort; 5000 takes the
+    # primary-keys-only shared-memory path, 10000 the chunk sort + global merge
     from paper_2409_08270_b200 import CameraView
     rng = np.random.default_rng(17)
-    n = 10000
     means = np.stack([rng.uniform(-0.3, 0.3, n), rng.uniform(-0.2, 0.2, n),
                       rng.choice(np.linspace(3.0, 4.0, 50), size=n)], axis=1)
     scene = GaussianScene(means, rng.normal(size=(n, 4)), rng.uniform(0.05, 0.4, (n, 3)),
@@ -343,7 +344,7 @@ def test_long_tile_buckets_merge_path():
     alive, mean2d, _, depth, radius, _ = oracle.project(scene.means, scene.rotations, scene.scales,
                                                        oracle.camera_of(view))
     o_offs, o_items = oracle.bin_tiles(alive, mean2d, depth, radius, view.width, view.height)
-    assert np.diff(o_offs).max() > 4096
+    assert np.diff(o_offs).max() > (7296 if n == 10000 else 3584)
     assert np.array_equal(offs, o_offs)
     assert np.array_equal(items, o_items)
     m = LabelMask(0, rng.integers(0, 3, (48, 64), dtype=np.uint16))
