@@ -98,7 +98,7 @@ void launch_splat_keys(int k, const double* mean2d, const long long* radius, con
                        ViewCounters* vc, int num_sms, cudaStream_t st);
 
 // ---- fs_raster.cu ----
-constexpr unsigned int kTileSortCap = 3584;  // bucket entries sorted in shared memory
+constexpr unsigned int kTileSortCap = 4368;  // bucket entries sorted in shared memory
 // Novel-view compositing outputs (render_property, rasterizer.py:133-203).
 struct RenderArgs {
     double* alpha;                 // H x W accumulated alpha (rho)
