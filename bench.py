@@ -43,7 +43,7 @@ BYTES_PER_ATOMIC = 8         # float64 accumulator add
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -85,7 +85,7 @@ CONFIG_TEXT = {
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -94,13 +94,13 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines: list = []
+        self.lines: list = []  # (arrival time, csv line)
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -110,7 +110,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, begin: bool):
+        """Bracket the timed region (samples outside it are dropped when enough lie inside)."""
+        if begin:
+            self.t_begin = time.perf_counter()
+        else:
+            self.t_end = time.perf_counter()
 
     def __exit__(self, *exc):
         if self.proc:
@@ -123,7 +130,17 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo, hi = getattr(self, "t_begin", None), getattr(self, "t_end", None)
+        lines = [ln for t, ln in self.lines]
+        if lo is not None and hi is not None:
+            inside = [ln for t, ln in self.lines if lo <= t <= hi + 0.25]
+            window = "timed region"
+            if len(inside) < 3:  # short region: include the warm-up steps (also under load)
+                inside, window = lines, "warm-up + timed region"
+            lines = inside
+        else:
+            window = "run"
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -138,7 +155,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": window}
 
 
 def measured_peaks():
@@ -147,6 +164,17 @@ def measured_peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def atomic_peak(acc_bytes):
+    """R_atom measured by tools/atomic_peak.cu for the accumulator's size class."""
+    p = ROOT / "profiles" / "r1_atomic_peak.json"
+    if not p.exists():
+        return None, None
+    res = json.loads(p.read_text())["results"]
+    key = "16MB_C2" if acc_bytes <= (64 << 20) else ("256MB_C3" if acc_bytes <= (768 << 20)
+                                                      else "1536MB_C4")
+    return res[key]["f64_rand16"] * 1e9, key
 
 
 def cpu_baseline(wl, views_override=None):
@@ -250,22 +278,24 @@ def main():
                        out_ptr=out.data_ptr())
         return st
 
-    for _ in range(args.warmup):
-        step()
-    ctx.set_timing(True)
-    torch.cuda.synchronize()
-    if group is not None:
-        dist.barrier()
     stats = []
     with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.warmup):
+            step()
+        ctx.set_timing(True)
+        torch.cuda.synchronize()
+        if group is not None:
+            dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        clk.mark(True)
         t0.record()
         for _ in range(args.steps):
             stats.append(step())
         t1.record()
         torch.cuda.synchronize()
+        clk.mark(False)
     ctx.set_timing(False)
     elapsed = t0.elapsed_time(t1) / 1e3
     if group is not None:
@@ -279,13 +309,16 @@ def main():
     # ---- end to end through the public API (host inputs, host outputs) ----
     e2e = None
     if not args.no_e2e:
-        pairs = wl.pairs()
+        from paper_2409_08270_b200 import pin_inputs
+        # inputs staged once in page-locked host memory (the serving setup);
+        # every timed solve still copies them host -> device
+        scene_h, pairs = pin_inputs(wl.scene, wl.pairs(), device=local)
         h2d = int(wl.masks[mine].nbytes + wl.scene.means.nbytes + wl.scene.rotations.nbytes
                   + wl.scene.scales.nbytes + wl.scene.opacities.nbytes)
         d2h = int(E * N * 4 + (N if E == 2 else E * N))
         reps = max(1, min(args.steps, 3))
-        solve(wl.scene, [pairs[i] for i in mine] if group is None else pairs, E,
-              0.0, "binary" if E == 2 else "scene", process_group=group)  # warm
+        solve(scene_h, pairs, E, 0.0, "binary" if E == 2 else "scene",
+              process_group=group)  # warm
         torch.cuda.synchronize()
         if group is not None:
             dist.barrier()
@@ -295,17 +328,30 @@ def main():
         for _ in range(reps):
             ctx_cached = _native.context(local)
             ctx_cached._scene_key = None  # re-upload the scene every step
-            solve(wl.scene, pairs, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
+            solve(scene_h, pairs, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
         b.record()
         torch.cuda.synchronize()
         e_s = a.elapsed_time(b) / 1e3
+        # one more (warm) solve from the plain pageable numpy inputs, for reference
+        pairs_pg = wl.pairs()
+        solve(wl.scene, pairs_pg, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
+        ctx_cached._scene_key = None
+        torch.cuda.synchronize()
+        c = torch.cuda.Event(enable_timing=True)
+        c.record()
+        solve(wl.scene, pairs_pg, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
+        d = torch.cuda.Event(enable_timing=True)
+        d.record()
+        torch.cuda.synchronize()
+        pageable_s = c.elapsed_time(d) / 1e3
         if group is not None:
             t = torch.tensor([e_s], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
             e_s = float(t.item())
         e2e = {"value": total_px / (e_s / reps), "unit": "view-px/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "s_per_scene": e_s / reps}
+               "s_per_scene": e_s / reps, "inputs": "page-locked host arrays (pin_inputs)",
+               "s_per_scene_pageable_inputs": pageable_s}
 
     if rank != 0:
         if group is not None:
@@ -335,6 +381,7 @@ def main():
     achieved = alg_bytes / raster_avg_s / 1e9 if raster_avg_s > 0 else None
     traffic = None
     instr = None
+    rec = {}
     tp = ROOT / "profiles" / "raster_traffic.json"
     if tp.exists():
         try:
@@ -343,6 +390,8 @@ def main():
             instr = rec.get("warp_instructions_per_launch")
         except Exception:
             traffic = None
+    atom_rate = iso["atomics"] / views_n / raster_avg_s if raster_avg_s > 0 else None
+    atom_peak, atom_key = atomic_peak(E * N * 8)
     clk_summary = clk.summary()
     sm_hz = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
     issue_peak = 148 * 4 * sm_hz  # warp-instructions / s (one issue slot per scheduler per clock)
@@ -373,7 +422,21 @@ def main():
                          "achieved_winst_per_s": (instr / raster_avg_s) if instr else None,
                          "peak_winst_per_s": issue_peak,
                          "frac": (instr / raster_avg_s / issue_peak) if instr else None,
-                         "instructions_source": "profiles/raster_traffic.json (ncu --set full)"}},
+                         "instructions_source": "profiles/raster_traffic.json (ncu --set full)"},
+                     "atomics": {
+                         "per_launch": iso["atomics"] / views_n,
+                         "achieved_per_s": atom_rate,
+                         "peak_per_s": atom_peak,
+                         "frac": (atom_rate / atom_peak) if (atom_rate and atom_peak) else None,
+                         "peak_source": f"profiles/r1_atomic_peak.json {atom_key} "
+                                        "(tools/atomic_peak.cu: float64 RED, 16 random lanes "
+                                        "per warp instruction, accumulator-sized buffer)",
+                         "l2_atomic_alu_pct_of_peak_ncu": rec.get("l2_atomic_alu_pct_of_peak")},
+                     "warp_efficiency": {
+                         "threads_per_inst": rec.get("warp_efficiency_threads_per_inst"),
+                         "pred_on_threads_per_inst":
+                             rec.get("warp_efficiency_pred_on_threads_per_inst"),
+                         "source": "ncu smsp__thread_inst_executed[_pred_on]_per_inst_executed"}},
         "stages_ms_per_step": {"prep": st["prep_ms"], "bin": st["bin_ms"],
                                "raster": st["raster_ms"], "sum": stage_sum},
         "counters_per_step": {k: st[k] for k in ("emitted", "instances", "tile_steps",

@@ -89,6 +89,10 @@ int fs_synchronize(fs_context *ctx);
  * caller hands back to numpy -- the contribution matrix and the labels. */
 int fs_host_alloc(fs_context *ctx, uint64_t bytes, void **out);
 int fs_host_free(fs_context *ctx, void *ptr);
+/* 1 if [ptr, ptr + bytes) is page-locked host memory (fs_host_alloc or
+ * cudaHostRegister): fs_set_scene and fs_accumulate DMA such inputs directly
+ * instead of staging them through the library's pinned buffers. */
+int fs_host_pinned(const void *ptr, uint64_t bytes);
 
 /* Per-stage CUDA-event timing inside fs_accumulate (events on each view's
  * stream around its stages; adds ~3 event records per view). */

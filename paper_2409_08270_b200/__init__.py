@@ -54,7 +54,7 @@ from .scene import (
     project_scene,
     save_cameras,
 )
-from .solve import LabelSolver, solve
+from .solve import LabelSolver, pin_inputs, solve
 from .solver import Assignment, assign_binary, assign_scene
 
 __version__ = "0.1.0"
@@ -62,7 +62,7 @@ __version__ = "0.1.0"
 __all__ = [
     "Assignment", "BlendConfig", "CameraView", "ContributionMatrix", "DEFAULT_BLEND",
     "DEFAULT_TAU", "EXACT_BLEND", "Gaussian", "GaussianScene", "LabelMask", "LabelSolver",
-    "ProjectedGaussian", "ProjectionStats", "RenderOutput", "RenderedMask", "SceneDataError",
+    "ProjectedGaussian", "ProjectionStats", "pin_inputs", "RenderOutput", "RenderedMask", "SceneDataError",
     "accumulate_mask_files", "load_mask_png", "read_masks", "save_mask_png", "export_ply",
     "load_scene_ply",
     "SceneFormatError", "TILE_SIZE", "TileBinning", "accumulate_contributions", "assign_binary",

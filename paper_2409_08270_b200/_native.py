@@ -25,7 +25,7 @@ MODE_BINARY, MODE_SCENE = 0, 1
 EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
-    "fs_copy_to_host", "fs_synchronize", "fs_host_alloc", "fs_host_free", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_copy_to_host", "fs_synchronize", "fs_host_alloc", "fs_host_free", "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
     "fs_accumulate", "fs_finalize", "fs_assign", "fs_render", "fs_render_splats", "fs_render_mask",
     "fs_decode_mask_png",
 )
@@ -98,6 +98,7 @@ def load() -> ctypes.CDLL:
             "fs_synchronize": ([P], I),
             "fs_host_alloc": ([P, ctypes.c_uint64, ctypes.POINTER(P)], I),
             "fs_host_free": ([P, P], I),
+            "fs_host_pinned": ([P, ctypes.c_uint64], I),
             "fs_set_timing": ([P, I], I),
             "fs_set_scene": ([P, I64, P, P, P, P], I),
             "fs_project": ([P, P, P, P, P, P, P, P], I),

@@ -178,9 +178,30 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& t : th) t.join();
 }
 
-// Pageable host -> device copy through the context's two pinned chunks, so the
-// host memcpy of chunk i overlaps the DMA of chunk i-1.
+// Page-locked (cudaMallocHost / cudaHostRegister) host range: the DMA engine
+// reads it directly, no staging copy.
+bool host_pinned(const void* p, size_t bytes) {
+    if (!p || !bytes) return false;
+    const void* ends[2] = {p, static_cast<const char*>(p) + bytes - 1};
+    for (const void* q : ends) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (at.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
+}
+
+// Host -> device copy.  Pinned sources are copied directly; pageable ones go
+// through the context's two pinned chunks, so the host memcpy of chunk i
+// overlaps the DMA of chunk i-1.
 int upload(fs_context* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (host_pinned(src, bytes)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return FS_OK;
+    }
     if (!ctx->pinned_up[0]) {
         for (int k = 0; k < 2; ++k) {
             CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->pinned_up[k]), kUploadChunk));
@@ -508,6 +529,8 @@ int fs_host_free(fs_context* ctx, void* ptr) {
     return FS_OK;
 }
 
+int fs_host_pinned(const void* ptr, uint64_t bytes) { return host_pinned(ptr, bytes) ? 1 : 0; }
+
 int fs_synchronize(fs_context* ctx) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
@@ -750,11 +773,17 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
         const uint16_t* mask = masks[v];
         if (!masks_on_device) {
             const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
-            if (w.h2d_pending) CK(cudaEventSynchronize(w.h2d_done));
-            parallel_memcpy(w.pinned, masks[v], bytes);
-            CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
-            CK(cudaEventRecord(w.h2d_done, w.stream));
-            w.h2d_pending = true;
+            if (host_pinned(masks[v], bytes)) {
+                // page-locked input: DMA straight into the stream's mask buffer
+                // (stream order keeps it behind the previous view's raster)
+                CK(cudaMemcpyAsync(w.mask_dev, masks[v], bytes, cudaMemcpyHostToDevice, w.stream));
+            } else {
+                if (w.h2d_pending) CK(cudaEventSynchronize(w.h2d_done));
+                parallel_memcpy(w.pinned, masks[v], bytes);
+                CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
+                CK(cudaEventRecord(w.h2d_done, w.stream));
+                w.h2d_pending = true;
+            }
             mask = w.mask_dev;
         }
         enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,

@@ -487,3 +487,21 @@ def test_needle_splats_screen_is_conservative(blend):
     pairs = [(v, LabelMask(0, lab))]
     A = accumulate_contributions(scene, pairs, 3, blend).values
     np.testing.assert_allclose(A, _oracle_A(scene, pairs, 3, blend), rtol=1e-6, atol=1e-9)
+
+
+def test_pinned_inputs_identical_to_pageable():
+    """pin_inputs: page-locked scene + masks take the direct-DMA path (no staging);
+    the solve must be byte-identical to the pageable-input solve."""
+    from paper_2409_08270_b200 import pin_inputs, solve
+    wl = synth.make_workload(seed=5, n_gaussians=6000, n_views=5, width=120, height=72,
+                             num_objects=4)
+    pairs = wl.pairs()
+    m0, a0 = solve(wl.scene, pairs, 4, 0.1, "scene")
+    scene_p, pairs_p = pin_inputs(wl.scene, pairs)
+    for _, m in pairs_p:
+        assert _native.load().fs_host_pinned(m.labels.ctypes.data, m.labels.nbytes) == 1
+    m1, a1 = solve(scene_p, pairs_p, 4, 0.1, "scene")
+    assert np.array_equal(m0.values, m1.values)
+    assert np.array_equal(a0.membership, a1.membership)
+    for (_, m), (_, mp) in zip(pairs, pairs_p):
+        assert np.array_equal(m.labels, mp.labels)

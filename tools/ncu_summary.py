@@ -15,6 +15,17 @@ KEYS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    # warp efficiency of the compositing loop (active / predicated-on threads per warp instruction)
+    "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "smsp__thread_inst_executed_pred_on_per_inst_executed.ratio",
+    # L2 atomic traffic of the float64 accumulator adds
+    "lts__t_requests_srcunit_tex_op_atom_dot_alu.sum",
+    "lts__t_sectors_srcunit_tex_op_atom_dot_alu.sum",
+    "lts__t_sectors_srcunit_tex_op_atom_dot_alu.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_requests_srcunit_tex_op_red.sum",
+    "lts__t_sectors_srcunit_tex_op_red.sum",
+    "lts__t_sectors_srcunit_tex_op_red.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
