@@ -109,6 +109,32 @@ __device__ __forceinline__ Rec32 screen_record(double mx, double my, double ia, 
     return s;
 }
 
+// Tiles of the reference rectangle rc (rasterizer.py:106-113) that can hold a
+// sample with alpha >= floor.  The raster's strip test rejects a splat for the
+// pixel-centre strip [u_lo, u_hi] x [v_lo, v_hi] when u_hi < mx - hx,
+// u_lo > mx + hx (same in v) -- float32, these exact expressions; tile t holds
+// centres 16t + 0.5 ... 16t + 15.5, so every strip of a tile outside
+//   16t + 15.5 >= mx - hx  and  16t + 0.5 <= mx + hx
+// is rejected and its instance is dropped here instead (the reference gives
+// such samples no weight and no transmittance update, contributions.py:148).
+// Exact blend (hx = +inf) keeps the rectangle.  C2: 22% fewer instances.
+__device__ __forceinline__ unsigned long long floor_box_rect(unsigned long long rc, const Rec32& s) {
+    if (rc == ~0ull || !(s.hx < INFINITY) || !(s.hy < INFINITY)) return rc;
+    const float lx = s.mx - s.hx, hx = s.mx + s.hx, ly = s.my - s.hy, hy = s.my + s.hy;
+    // exact in float64: float + half-integer, then a power-of-two divide
+    const double bx0 = ceil(((double)lx - 15.5) / 16.0), bx1 = floor(((double)hx - 0.5) / 16.0);
+    const double by0 = ceil(((double)ly - 15.5) / 16.0), by1 = floor(((double)hy - 0.5) / 16.0);
+    double tx0 = (double)(rc & 0xFFFF), tx1 = (double)((rc >> 16) & 0xFFFF);
+    double ty0 = (double)((rc >> 32) & 0xFFFF), ty1 = (double)((rc >> 48) & 0xFFFF);
+    tx0 = fmax(tx0, bx0);
+    tx1 = fmin(tx1, bx1);
+    ty0 = fmax(ty0, by0);
+    ty1 = fmin(ty1, by1);
+    if (!(tx0 <= tx1) || !(ty0 <= ty1)) return ~0ull;
+    return (unsigned long long)tx0 | ((unsigned long long)tx1 << 16) |
+           ((unsigned long long)ty0 << 32) | ((unsigned long long)ty1 << 48);
+}
+
 // K1: one thread per Gaussian.  Mirrors _project_arrays (scene.py:252-312)
 // and tile_range (rasterizer.py:106-113); emits the depth sort key, the tile
 // rectangle and the walk records.  cull_floor > 0 additionally drops (from
@@ -211,7 +237,6 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
                 if (!transparent) rc = tile_rect(mxp, myp, rad, tx_n, ty_n);
             }
             keys[i] = key;
-            rect[i] = rc;
             // walk records (float64 exact, float32 screen)
             Rec64 q;
             q.mx = mxp;
@@ -223,6 +248,9 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
             r64[i] = q;
             const Rec32 s = screen_record(mxp, myp, ia, ib, ic, a, c, o, alpha_floor, alive);
             r32[i] = s;
+            // binning for a floored walk: only tiles the raster's strip test can accept
+            if (cull_floor && alpha_floor > 0.0) rc = floor_box_rect(rc, s);
+            rect[i] = rc;
             if (ex.alive) {
                 ex.alive[i] = alive ? 1 : 0;
                 ex.mean2d[2 * i] = mxp;

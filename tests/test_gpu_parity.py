@@ -263,17 +263,19 @@ def test_edge_cases():
 
 def test_instance_overflow_retry():
     # 1500 Gaussians covering a 4K image: 1500 x 8160 tiles > initial capacity
+    # (opaque enough that the alpha-floor box keeps the whole radius box)
     from paper_2409_08270_b200 import CameraView
     n = 1500
     rng = np.random.default_rng(0)
     scene = GaussianScene(np.c_[rng.uniform(-0.1, 0.1, (n, 2)), rng.uniform(2, 3, n)],
                           np.tile([1.0, 0, 0, 0], (n, 1)), np.full((n, 3), 2.0),
-                          rng.uniform(0.01, 0.02, n))
+                          rng.uniform(0.8, 0.95, n))
     v = CameraView(0, 1920, 1088, 1000.0, 1000.0, 960.0, 544.0, np.eye(4))
     m = LabelMask(0, rng.integers(0, 2, (1088, 1920), dtype=np.uint16))
     st = {}
     A = accumulate_contributions(scene, [(v, m)], 2, stats=st).values
     assert st["instances"] > 4 * n
+    assert st["retried_views"] == 1
     cams = [oracle.camera_of(v)]
     ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities, cams,
                             [m.labels], 2, threads=8)
