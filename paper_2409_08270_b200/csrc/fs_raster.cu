@@ -81,10 +81,6 @@ __device__ __forceinline__ void red_add(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
 // 32 x 32 bit-matrix transpose across the warp: lane i holds row i (bit j =
 // M[i][j]); on return lane j holds column j (bit i = M[i][j]).  Five
 // shuffle stages swap the off-diagonal blocks of halving size.
