@@ -507,3 +507,33 @@ def test_pinned_inputs_identical_to_pageable():
     assert np.array_equal(a0.membership, a1.membership)
     for (_, m), (_, mp) in zip(pairs, pairs_p):
         assert np.array_equal(m.labels, mp.labels)
+
+
+def test_floor_box_binning_drops_only_dead_instances():
+    """Floored walks bin a splat only into tiles its alpha-floor box reaches: fewer
+    instances than the reference's radius boxes (TileBinning), identical matrix; the
+    exact blend keeps every reference instance."""
+    wl = synth.make_workload(seed=33, n_gaussians=30000, n_views=2, width=256, height=192,
+                             num_objects=3)
+    # low opacities shrink the alpha-floor ellipse well inside the 3-sigma radius box
+    scene = GaussianScene(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                          np.random.default_rng(3).uniform(0.005, 0.05, len(wl.scene)))
+    pairs = wl.pairs()
+    ref_inst = 0
+    for v in wl.views:
+        alive, m2, _, depth, rad, _ = oracle.project(scene.means, scene.rotations, scene.scales,
+                                                     oracle.camera_of(v))
+        offs, _ = oracle.bin_tiles(alive, m2, depth, rad, v.width, v.height)
+        ref_inst += int(offs[-1])
+    cams = [oracle.camera_of(v) for v in wl.views]
+    for blend in (DEFAULT_BLEND, EXACT_BLEND):
+        st = {}
+        A = accumulate_contributions(scene, pairs, 3, blend, stats=st).values
+        ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities,
+                                cams, list(wl.masks), 3, blend.alpha_floor,
+                                blend.transmittance_floor, threads=8, as_float32=False)
+        np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+        if blend is EXACT_BLEND:
+            assert st["instances"] == ref_inst
+        else:
+            assert 0 < st["instances"] < 0.8 * ref_inst
