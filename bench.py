@@ -50,13 +50,15 @@ def parse():
     ap.add_argument("--views", type=int, default=None, help="override the view count")
     ap.add_argument("--gaussians", type=int, default=None, help="override the Gaussian count")
     ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--iid", action="store_true",
+                    help="worst case: iid uniform labels per pixel instead of object silhouettes")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=None)
     return ap.parse_args()
 
 
-def load_workload(name, views=None, gaussians=None):
+def load_workload(name, views=None, gaussians=None, iid=False):
     from paper_2409_08270_b200 import synth
     from paper_2409_08270_b200.scene import CameraView, GaussianScene
     if name == "C1":
@@ -72,6 +74,8 @@ def load_workload(name, views=None, gaussians=None):
         over["n_views"] = views
     if gaussians:
         over["n_gaussians"] = gaussians
+    if iid:
+        over["iid_masks"] = True
     return synth.config_workload(name, **over)
 
 
@@ -167,14 +171,16 @@ def measured_peaks():
 
 
 def atomic_peak(acc_bytes):
-    """R_atom measured by tools/atomic_peak.cu for the accumulator's size class."""
+    """R_atom (tools/atomic_peak.cu): the L2 float64 RED ceiling -- random lanes into an
+    L2-resident buffer -- plus, for context, the uniform-random rate into a buffer of the
+    accumulator's size (a floor: real scatters have far more locality)."""
     p = ROOT / "profiles" / "r1_atomic_peak.json"
     if not p.exists():
-        return None, None
+        return None, None, None
     res = json.loads(p.read_text())["results"]
     key = "16MB_C2" if acc_bytes <= (64 << 20) else ("256MB_C3" if acc_bytes <= (768 << 20)
                                                       else "1536MB_C4")
-    return res[key]["f64_rand16"] * 1e9, key
+    return res["16MB_C2"]["f64_rand16"] * 1e9, key, res[key]["f64_rand16"] * 1e9
 
 
 def cpu_baseline(wl, views_override=None):
@@ -200,7 +206,7 @@ def cpu_baseline(wl, views_override=None):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    wl = load_workload(args.config, args.views, args.gaussians)
+    wl = load_workload(args.config, args.views, args.gaussians, args.iid)
     import oracle
     oracle.build()
     cores = os.cpu_count() or 1
@@ -248,7 +254,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
 
-    wl = load_workload(args.config, args.views, args.gaussians)
+    wl = load_workload(args.config, args.views, args.gaussians, args.iid)
     E, N = wl.num_objects, len(wl.scene)
     mine = shard_views(len(wl.views), rank, world)
     views = [wl.views[i] for i in mine]
@@ -273,7 +279,7 @@ def main():
                             masks_on_device=True)
         if group is not None:
             dist.all_reduce(acc, group=group)
-        ctx.finalize(acc.data_ptr(), E * N, out_ptr=A32.data_ptr())
+        ctx.finalize(acc.data_ptr(), N, E, out_ptr=A32.data_ptr())
         _native.assign(None, 0.0, mode, ctx=ctx, on_device_ptr=A32.data_ptr(), n=N, e=E,
                        out_ptr=out.data_ptr())
         return st
@@ -391,7 +397,7 @@ def main():
         except Exception:
             traffic = None
     atom_rate = iso["atomics"] / views_n / raster_avg_s if raster_avg_s > 0 else None
-    atom_peak, atom_key = atomic_peak(E * N * 8)
+    atom_peak, atom_key, atom_sized = atomic_peak(E * N * 8)
     clk_summary = clk.summary()
     sm_hz = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
     issue_peak = 148 * 4 * sm_hz  # warp-instructions / s (one issue slot per scheduler per clock)
@@ -401,7 +407,8 @@ def main():
         "value": value, "unit": "view-px/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": s_per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_TEXT[args.config], "name": args.config,
+        "config": {"workload": CONFIG_TEXT[args.config] + (" (iid labels)" if args.iid else ""),
+                   "name": args.config + ("-iid" if args.iid else ""),
                    "gaussians": N, "views": len(wl.views),
                    "image": f"{wl.views[0].width}x{wl.views[0].height}", "num_objects": E,
                    "parallelism": f"views sharded over {world} GPU(s)",
@@ -428,9 +435,11 @@ def main():
                          "achieved_per_s": atom_rate,
                          "peak_per_s": atom_peak,
                          "frac": (atom_rate / atom_peak) if (atom_rate and atom_peak) else None,
-                         "peak_source": f"profiles/r1_atomic_peak.json {atom_key} "
+                         "peak_source": "profiles/r1_atomic_peak.json 16MB_C2 f64_rand16 "
                                         "(tools/atomic_peak.cu: float64 RED, 16 random lanes "
-                                        "per warp instruction, accumulator-sized buffer)",
+                                        "per warp instruction, L2-resident buffer)",
+                         "uniform_random_per_s_at_accumulator_size": atom_sized,
+                         "accumulator_size_class": atom_key,
                          "l2_atomic_alu_pct_of_peak_ncu": rec.get("l2_atomic_alu_pct_of_peak")},
                      "warp_efficiency": {
                          "threads_per_inst": rec.get("warp_efficiency_threads_per_inst"),

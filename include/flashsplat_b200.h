@@ -126,7 +126,8 @@ int fs_bin_splats(fs_context *ctx, int64_t k, const double *mean2d, const double
 
 /* accumulate_contributions (contributions.py:90-116) / _accumulate_view
  * (contributions.py:119-160) for n_views views: adds every view's alpha*T
- * mass into acc (E x N float64, DEVICE pointer, caller-zeroed).  masks[v] is
+ * mass into acc (N x E float64 -- Gaussian-major, so one splat's labels share
+ * cache lines -- DEVICE pointer, caller-zeroed).  masks[v] is
  * an H x W uint16 label grid, host or device (masks_on_device).  Labels must
  * be < num_objects (validated by the caller, contributions.py:104-114). */
 int fs_accumulate(fs_context *ctx, int n_views, const fs_camera *cams,
@@ -134,10 +135,11 @@ int fs_accumulate(fs_context *ctx, int n_views, const fs_camera *cams,
                   double alpha_floor, double transmittance_floor, double *acc,
                   fs_accumulate_stats *stats);
 
-/* ContributionMatrix(total.astype(float32)) (contributions.py:116): float64
- * device accumulator -> float32, written to host (out_on_device = 0) or
- * device memory. */
-int fs_finalize(fs_context *ctx, const double *acc, int64_t count, float *out, int out_on_device);
+/* ContributionMatrix(total.astype(float32)) (contributions.py:116): the N x E
+ * float64 device accumulator -> E x N float32 (the reference's layout), written
+ * to host (out_on_device = 0) or device memory. */
+int fs_finalize(fs_context *ctx, const double *acc, int64_t n, int num_objects, float *out,
+                int out_on_device);
 
 /* _one_vs_rest_wins + assign_binary / assign_scene (solver.py:118-172).
  * A is E x N float32; out is N (binary) or E x N (scene) uint8.  Host or

@@ -105,7 +105,7 @@ def load() -> ctypes.CDLL:
             "fs_bin": ([P, P, P, P, I64, ctypes.POINTER(I64)], I),
             "fs_bin_splats": ([P, I64, P, P, P, P, I, I, P, P, I64, ctypes.POINTER(I64)], I),
             "fs_accumulate": ([P, I, P, P, I, I, D, D, P, P], I),
-            "fs_finalize": ([P, P, I64, P, I], I),
+            "fs_finalize": ([P, P, I64, I, P, I], I),
             "fs_assign": ([P, P, I64, I, F, I, P, I], I),
             "fs_render": ([P, P, P, D, D, P, I, P, P, P], I),
             "fs_render_splats": ([P, I, I, I64, P, P, P, P, P, P, D, D, P, I, P, P, P], I),
@@ -306,7 +306,7 @@ class Context:
 
     def accumulate(self, views, masks, num_objects: int, alpha_floor: float, t_floor: float,
                    acc_ptr: int, masks_on_device: bool = False) -> dict:
-        """Add every view's alpha*T mass into the E x N float64 device buffer acc_ptr."""
+        """Add every view's alpha*T mass into the N x E (Gaussian-major) float64 device buffer acc_ptr."""
         nv = len(views)
         cams = (FsCamera * max(nv, 1))(*[camera_struct(v) for v in views])
         if masks_on_device:
@@ -335,11 +335,13 @@ class Context:
             self._buffers[role] = buf
         return buf
 
-    def finalize(self, acc_ptr: int, count: int, out_ptr: int = None, out: np.ndarray = None):
+    def finalize(self, acc_ptr: int, n: int, e: int, out_ptr: int = None,
+                 out: np.ndarray = None):
+        """N x E float64 accumulator -> E x N float32 (host ``out`` or device ``out_ptr``)."""
         if out is not None:
-            _check(load().fs_finalize(self.handle, acc_ptr, count, _p(out), 0))
+            _check(load().fs_finalize(self.handle, acc_ptr, n, e, _p(out), 0))
             return out
-        _check(load().fs_finalize(self.handle, acc_ptr, count, out_ptr, 1))
+        _check(load().fs_finalize(self.handle, acc_ptr, n, e, out_ptr, 1))
         return None
 
     def alloc(self, nbytes: int) -> DeviceBuffer:

@@ -169,7 +169,7 @@ def accumulate_contributions(
         acc = ctx.buffer("acc64", 8 * num_objects * n).zero()
         st = run_device_accumulate(ctx, views, num_objects, blend, acc.ptr)
         out = np.empty((num_objects, n), dtype=np.float32)
-        ctx.finalize(acc.ptr, out.size, out=out)
+        ctx.finalize(acc.ptr, n, num_objects, out=out)
     if stats is not None:
         stats.update(st)
     return ContributionMatrix(values=out)

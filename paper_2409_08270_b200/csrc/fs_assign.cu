@@ -17,18 +17,34 @@ namespace fs {
 
 namespace {
 
-__global__ void finalize_kernel(const double* __restrict__ acc, float* __restrict__ out,
-                                long long count) {
+// N x E float64 (Gaussian-major) -> E x N float32 (the API layout), the
+// contributions.py:116 cast.  Small E: one thread per Gaussian (its E
+// doubles are contiguous; the E stores are coalesced across the warp).
+__global__ void finalize_small_kernel(const double* __restrict__ acc, float* __restrict__ out,
+                                      long long n, int e) {
     const long long stride = (long long)gridDim.x * blockDim.x;
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long n2 = count / 2;
-    const double2* a2 = reinterpret_cast<const double2*>(acc);
-    float2* o2 = reinterpret_cast<float2*>(out);
-    for (long long k = i; k < n2; k += stride) {
-        double2 v = a2[k];
-        o2[k] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+    for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += stride)
+        for (int l = 0; l < e; ++l) out[(long long)l * n + g] = __double2float_rn(acc[g * e + l]);
+}
+
+// Larger E: 32 x 32 tiles transposed through shared memory.
+__global__ void __launch_bounds__(256) finalize_tile_kernel(const double* __restrict__ acc,
+                                                            float* __restrict__ out, long long n,
+                                                            int e) {
+    __shared__ float t[32][33];
+    const long long g0 = (long long)blockIdx.x * 32;
+    const int l0 = blockIdx.y * 32, tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) {
+        const long long g = g0 + r;
+        const int l = l0 + tx;
+        if (g < n && l < e) t[tx][r] = __double2float_rn(acc[g * e + l]);
     }
-    if (i == 0 && (count & 1)) out[count - 1] = __double2float_rn(acc[count - 1]);
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int l = l0 + r;
+        const long long g = g0 + tx;
+        if (l < e && g < n) out[(long long)l * n + g] = t[r][tx];
+    }
 }
 
 // mode 0 = binary (E == 2, N labels), mode 1 = scene (E x N membership)
@@ -60,12 +76,16 @@ __global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ A
 
 }  // namespace
 
-void launch_finalize(const double* acc, float* out, long long count, cudaStream_t st) {
-    if (count <= 0) return;
-    long long blocks = (count / 2 + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    if (blocks < 1) blocks = 1;
-    finalize_kernel<<<(int)blocks, 256, 0, st>>>(acc, out, count);
+void launch_finalize(const double* acc, float* out, long long n, int e, cudaStream_t st) {
+    if (n <= 0 || e <= 0) return;
+    if (e <= 8) {
+        long long blocks = (n + 255) / 256;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        finalize_small_kernel<<<(int)blocks, 256, 0, st>>>(acc, out, n, e);
+    } else {
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((e + 31) / 32));
+        finalize_tile_kernel<<<grid, 256, 0, st>>>(acc, out, n, e);
+    }
 }
 
 void launch_assign(const float* A, long long n, int e, float gamma, int mode, uint8_t* out,

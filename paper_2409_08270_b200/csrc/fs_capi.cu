@@ -872,26 +872,26 @@ int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uin
     return FS_OK;
 }
 
-int fs_finalize(fs_context* ctx, const double* acc, int64_t count, float* out, int out_on_device) {
-    if (!ctx || (!acc && count) || (!out && count)) return fail(FS_EINVAL, "fs_finalize: NULL argument");
+int fs_finalize(fs_context* ctx, const double* acc, int64_t n, int num_objects, float* out,
+                int out_on_device) {
+    if (!ctx) return fail(FS_EINVAL, "fs_finalize: NULL context");
+    if (n < 0 || num_objects < 0) return fail(FS_EINVAL, "fs_finalize: bad shape");
+    const size_t count = (size_t)n * (size_t)num_objects;
+    if ((!acc || !out) && count) return fail(FS_EINVAL, "fs_finalize: NULL argument");
     if (count == 0) return FS_OK;
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());  // acc may come from another stream (e.g. an NCCL all-reduce)
     cudaStream_t st = ctx->work[0].stream;
     float* dst = out;
     if (!out_on_device) {
-        int rc = grow(&ctx->tmp_f32, &ctx->tmp_f32_cap, (size_t)count);
+        int rc = grow(&ctx->tmp_f32, &ctx->tmp_f32_cap, count);
         if (rc) return rc;
         dst = ctx->tmp_f32;
     }
-    fs::launch_finalize(acc, dst, count, st);
+    fs::launch_finalize(acc, dst, n, num_objects, st);
     CK(cudaGetLastError());
-    if (!out_on_device) {
-        CK(cudaMemcpyAsync(out, dst, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-    } else {
-        CK(cudaStreamSynchronize(st));
-    }
+    if (!out_on_device) CK(cudaMemcpyAsync(out, dst, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return FS_OK;
 }
 

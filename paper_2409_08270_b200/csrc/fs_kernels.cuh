@@ -120,7 +120,7 @@ struct RasterArgs {
     TileSortArgs sort;             // bucket -> depth-ordered gid list (prologue)
     const Rec32* r32;
     const Rec64* r64;
-    double* acc;                   // E x N float64 accumulator
+    double* acc;                   // N x E float64 accumulator (Gaussian-major)
     ViewCounters* vc;
     const unsigned int* tile_order;  // ntiles: launch order (tile_start_kernel)
     RenderArgs render;             // launch_raster_render only
@@ -130,7 +130,7 @@ void launch_raster(const RasterArgs& a, cudaStream_t st);
 void launch_raster_render(const RasterArgs& a, cudaStream_t st);
 
 // ---- fs_assign.cu ----
-void launch_finalize(const double* acc, float* out, long long count, cudaStream_t st);
+void launch_finalize(const double* acc, float* out, long long n, int e, cudaStream_t st);
 void launch_assign(const float* A, long long n, int e, float gamma, int mode, uint8_t* out,
                    cudaStream_t st);
 

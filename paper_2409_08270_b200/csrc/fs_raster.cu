@@ -1,5 +1,5 @@
 // fs_raster.cu -- K3: per-tile front-to-back compositing that scatters alpha*T
-// into the E x N float64 contribution accumulator (reference
+// into the N x E (Gaussian-major) float64 contribution accumulator (reference
 // contributions.py:119-160, the `_accumulate_view` walk), and -- instantiated
 // with kRender -- the per-pixel compositing of render_property
 // (rasterizer.py:133-203).
@@ -29,7 +29,8 @@
 //   C  warps with at most 4 distinct labels reduce w per (splat, label) with a
 //      padded transpose in shared memory + a shuffle and issue one float64
 //      atomic each; warps with more labels issue one atomic per contributing
-//      pixel.
+//      pixel.  The accumulator is Gaussian-major (N x E): the labels of one
+//      splat share its cache lines.
 // A warp stops when none of its pixels is active (contributions.py:158-159:
 // pixels are independent, the reference's tile-level break is an
 // optimisation of the same rule).  The label range check of
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const bool lbl_ok = label < (unsigned)a.num_objects;
 
     const double af_eff = a.af_eff, tf_eff = a.tf_eff;
-    const long long n_g = a.n_gaussians;
+    const unsigned int n_obj = (unsigned)a.num_objects;  // accumulator row length (N x E)
     double* __restrict__ acc = a.acc;
     double* __restrict__ myval = W.val;
 
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                         const bool fire = lane < kMini && k < nm && v > 0.0 && gl < (unsigned)a.num_objects;
                         if (fire) {
-                            red_add(acc + (size_t)gl * n_g + W.gid[(head + k) & (kRing - 1)], v);
+                            red_add(acc + (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + gl, v);
                             ++atom;
                         }
                     }
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         mm &= mm - 1u;
                         const double w = myval[k * kRowStride + lane];
                         if (w > 0.0) {
-                            red_add(acc + (size_t)label * n_g + W.gid[(head + k) & (kRing - 1)], w);
+                            red_add(acc + (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label, w);
                             ++atom;
                         }
                     }

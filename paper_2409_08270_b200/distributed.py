@@ -90,7 +90,7 @@ def _device_partial_path(scene, views, mine, num_objects, blend, group, device, 
     out32 = torch.empty(num_objects * max(n, 1), dtype=torch.float32, device=acc.device)
     torch.cuda.synchronize(device)
     with ctx.lock:
-        ctx.finalize(acc.data_ptr(), num_objects * n, out_ptr=out32.data_ptr())
+        ctx.finalize(acc.data_ptr(), n, num_objects, out_ptr=out32.data_ptr())
     if stats is not None:
         stats.update(st)
     return out32[: num_objects * n].cpu().numpy().reshape(num_objects, n)

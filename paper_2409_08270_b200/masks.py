@@ -142,7 +142,7 @@ def accumulate_mask_files(scene, view_paths: Sequence, num_objects: int,
                         totals[k] = totals.get(k, 0) + v
             out = np.empty((num_objects, n), dtype=np.float32)
             if out.size:
-                ctx.finalize(acc.ptr, out.size, out=out)
+                ctx.finalize(acc.ptr, n, num_objects, out=out)
     if stats is not None:
         stats.update(totals)
     return ContributionMatrix(values=out)

@@ -92,7 +92,7 @@ class LabelSolver:
             A, out = self._buffers(e, n)
             self._A_cur, self._out_cur = A, out
             if n:
-                ctx.finalize(acc_ptr, e * n, out_ptr=A.ptr)
+                ctx.finalize(acc_ptr, n, e, out_ptr=A.ptr)
         self.num_objects = e
         if not download:
             return None

@@ -31,7 +31,7 @@ for rep in range(3):
     t["accumulate_gpu_ms"] = st["gpu_ms"] / 1e3
     out = np.empty((E, N), np.float32)
     t0 = time.perf_counter()
-    ctx.finalize(acc.ptr, E * N, out=out)
+    ctx.finalize(acc.ptr, N, E, out=out)
     t["finalize_d2h"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     _native.assign(out, 0.0, _native.MODE_BINARY if E == 2 else _native.MODE_SCENE)
