@@ -268,13 +268,14 @@ class Context:
     def render(self, view, member, alpha_floor: float, t_floor: float, channel=None):
         """fs_render over the resident scene: (value | None, alpha, depth)."""
         h, w = view.height, view.width
-        alpha = np.zeros((h, w))
-        depth = np.zeros((h, w))
+        # every pixel is written by the D2H copies: page-locked, uninitialised
+        alpha = self.pinned_empty((h, w), np.float64)
+        depth = self.pinned_empty((h, w), np.float64)
         channels, value, ch = 0, None, None
         if channel is not None:
             ch = np.ascontiguousarray(channel, dtype=np.float64)
             channels = 1 if ch.ndim == 1 else ch.shape[1]
-            value = np.zeros((h, w) if channels == 1 else (h, w, channels))
+            value = self.pinned_empty((h, w) if channels == 1 else (h, w, channels), np.float64)
         mem = None if member is None else np.ascontiguousarray(member, dtype=np.uint8)
         cam = camera_struct(view)
         _check(load().fs_render(self.handle, ctypes.byref(cam), _p(mem), float(alpha_floor),
@@ -285,7 +286,7 @@ class Context:
     def render_mask(self, view, membership, tau: float, alpha_floor: float, t_floor: float):
         """fs_render_mask: H x W uint16 labels (membership: E x N)."""
         membership = np.ascontiguousarray(membership, dtype=np.uint8)
-        labels = np.zeros((view.height, view.width), np.uint16)
+        labels = self.pinned_empty((view.height, view.width), np.uint16)
         cam = camera_struct(view)
         _check(load().fs_render_mask(self.handle, ctypes.byref(cam), _p(membership),
                                      int(membership.shape[0]), float(tau), float(alpha_floor),

@@ -120,6 +120,8 @@ struct fs_context {
     size_t rn_u32_cap = 0;
     uint16_t* rn_labels = nullptr;
     size_t rn_labels_cap = 0;
+    unsigned long long* rn_rect = nullptr;  // fs_render_mask: the full scene's tile rectangles
+    size_t rn_rect_cap = 0;
 };
 
 
@@ -464,7 +466,7 @@ void fs_destroy(fs_context* ctx) {
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
                     (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out,
                     (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
-                    (void*)ctx->rn_u32, (void*)ctx->rn_labels})
+                    (void*)ctx->rn_u32, (void*)ctx->rn_labels, (void*)ctx->rn_rect})
         if (p) cudaFree(p);
     for (int k = 0; k < 2; ++k) {
         if (ctx->pinned_up[k]) cudaFreeHost(ctx->pinned_up[k]);
@@ -1018,6 +1020,16 @@ __global__ void mask_combine_kernel(const double* __restrict__ alpha,
     }
 }
 
+// Tile rectangles of one object's members (the others are never binned, like
+// project_scene(member_mask=...), scene.py:346-350).
+__global__ void member_rect_kernel(const unsigned long long* __restrict__ all,
+                                   const uint8_t* __restrict__ member, long long n,
+                                   unsigned long long* __restrict__ rect) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        rect[i] = member[i] ? all[i] : ~0ull;
+}
+
 int check_render_cam(const fs_camera* cam) { return check_cam(*cam, 0); }
 
 }  // namespace
@@ -1155,27 +1167,58 @@ int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* members
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
     fs::Work& w = ctx->work[0];
+    cudaStream_t st = w.stream;
     const size_t px = (size_t)cam->width * cam->height, n = (size_t)std::max<long long>(ctx->n, 0);
+    const int tx = fs::tiles_x_of(cam->width), ntiles = tx * fs::tiles_y_of(cam->height);
     if ((rc = grow(&ctx->rn_f64, &ctx->rn_f64_cap, 3 * px))) return rc;  // alpha | depth | best
     if ((rc = grow(&ctx->rn_labels, &ctx->rn_labels_cap, px))) return rc;
-    if ((rc = grow(&ctx->rn_member, &ctx->rn_member_cap, std::max<size_t>(n, 1)))) return rc;
-    CK(cudaMemsetAsync(ctx->rn_labels, 0, sizeof(uint16_t) * px, w.stream));
-    double* best = ctx->rn_f64 + 2 * px;
-    int grid = (int)std::min<size_t>((px + 255) / 256, (size_t)ctx->num_sms * 8);
+    CK(cudaMemsetAsync(ctx->rn_labels, 0, sizeof(uint16_t) * px, st));
+    // maskrender.py:82-83: empty objects are skipped (early-exit scan per row)
+    std::vector<int> objs;
     for (int obj = 1; obj < num_objects; ++obj) {
         const uint8_t* row = membership + (size_t)obj * n;
-        bool any = false;  // maskrender.py:82-83: empty objects are skipped
+        bool any = false;
         for (size_t i = 0; i < n && !any; ++i) any = row[i] != 0;
-        if (!any) continue;
-        if ((rc = upload(ctx, ctx->rn_member, row, n, w.stream))) return rc;
-        if ((rc = render_scene_device(ctx, cam, ctx->rn_member, alpha_floor, transmittance_floor,
-                                      nullptr, 0, ctx->rn_f64)))
-            return rc;
-        mask_combine_kernel<<<std::max(grid, 1), 256, 0, w.stream>>>(
-            ctx->rn_f64, ctx->rn_f64 + px, (long long)px, tau, (unsigned int)obj, ctx->rn_labels, best);
-        CK(cudaGetLastError());
+        if (any) objs.push_back(obj);
     }
-    CK(cudaStreamSynchronize(w.stream));
+    if (!objs.empty()) {
+        if ((rc = grow(&ctx->rn_member, &ctx->rn_member_cap, (size_t)num_objects * n))) return rc;
+        if ((rc = grow(&ctx->rn_rect, &ctx->rn_rect_cap, n))) return rc;
+        if ((rc = upload(ctx, ctx->rn_member, membership, (size_t)num_objects * n, st))) return rc;
+        // Project once and bin the whole scene once: its instance count bounds
+        // every object's, so the per-object loop below runs without host syncs.
+        unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
+        fs::ViewCounters vc{};
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if ((rc = ensure_work(ctx, w, (long long)n, ntiles, cap, 1))) return rc;
+            enqueue_bin(ctx, w, to_cam(*cam), alpha_floor, 1, fs::ProjectExport{});
+            CK(cudaMemcpyAsync(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (!vc.overflow) break;
+            cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull,
+                                                             (unsigned long long)vc.n_instances + 1024);
+        }
+        if (vc.overflow) return fail(FS_ENOMEM, "fs_render_mask: instance buffer overflow");
+        CK(cudaMemcpyAsync(ctx->rn_rect, w.rect, sizeof(unsigned long long) * n,
+                           cudaMemcpyDeviceToDevice, st));
+        double* best = ctx->rn_f64 + 2 * px;
+        const int grid = (int)std::min<size_t>((px + 255) / 256, (size_t)ctx->num_sms * 8);
+        const int ngrid = (int)std::min<size_t>((n + 255) / 256, (size_t)ctx->num_sms * 8);
+        const fs::RasterArgs ra = render_args(w, cam->width, cam->height, alpha_floor,
+                                              transmittance_floor, ctx->rn_f64, 0, nullptr);
+        for (int obj : objs) {
+            member_rect_kernel<<<std::max(ngrid, 1), 256, 0, st>>>(
+                ctx->rn_rect, ctx->rn_member + (size_t)obj * n, (long long)n, w.rect);
+            fs::launch_bin(ntiles, tx, bin_buffers(w, (int)n, w.vc), w.vc, ctx->num_sms, st);
+            CK(cudaMemsetAsync(ctx->rn_f64, 0, sizeof(double) * 2 * px, st));
+            fs::launch_raster_render(ra, st);
+            mask_combine_kernel<<<std::max(grid, 1), 256, 0, st>>>(
+                ctx->rn_f64, ctx->rn_f64 + px, (long long)px, tau, (unsigned int)obj,
+                ctx->rn_labels, best);
+            CK(cudaGetLastError());
+        }
+    }
+    CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(labels, ctx->rn_labels, sizeof(uint16_t) * px, cudaMemcpyDeviceToHost));
     return FS_OK;
 }
