@@ -148,6 +148,11 @@ int fs_finalize(fs_context *ctx, const double *acc, int64_t n, int num_objects, 
 int fs_assign(fs_context *ctx, const float *A, int64_t n, int num_objects, float gamma, int mode,
               uint8_t *out, int on_device);
 
+/* Assignment.member_counts (solver.py:73-77): nonzero bytes per row of a
+ * rows x n uint8 DEVICE matrix (the labels or the membership fs_assign left
+ * on the device) -> counts[rows] on the host. */
+int fs_member_counts(fs_context *ctx, const uint8_t *m, int64_t n, int rows, int64_t *counts);
+
 /* ---- novel-view rendering ---- */
 
 /* render_view / render_subset_alpha_depth (rasterizer.py:206-234) over the

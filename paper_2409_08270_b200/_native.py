@@ -26,7 +26,7 @@ EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
     "fs_copy_to_host", "fs_synchronize", "fs_host_alloc", "fs_host_free", "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
-    "fs_accumulate", "fs_finalize", "fs_assign", "fs_render", "fs_render_splats", "fs_render_mask",
+    "fs_accumulate", "fs_finalize", "fs_assign", "fs_member_counts", "fs_render", "fs_render_splats", "fs_render_mask",
     "fs_decode_mask_png",
 )
 
@@ -106,6 +106,7 @@ def load() -> ctypes.CDLL:
             "fs_bin_splats": ([P, I64, P, P, P, P, I, I, P, P, I64, ctypes.POINTER(I64)], I),
             "fs_accumulate": ([P, I, P, P, I, I, D, D, P, P], I),
             "fs_finalize": ([P, P, I64, I, P, I], I),
+            "fs_member_counts": ([P, P, I64, I, P], I),
             "fs_assign": ([P, P, I64, I, F, I, P, I], I),
             "fs_render": ([P, P, P, D, D, P, I, P, P, P], I),
             "fs_render_splats": ([P, I, I, I64, P, P, P, P, P, P, D, D, P, I, P, P, P], I),
@@ -344,6 +345,12 @@ class Context:
             return out
         _check(load().fs_finalize(self.handle, acc_ptr, n, e, out_ptr, 1))
         return None
+
+    def member_counts(self, dev_ptr: int, n: int, rows: int) -> list:
+        """Nonzero bytes per row of a rows x n uint8 device matrix (fs_member_counts)."""
+        out = np.zeros(max(rows, 1), np.int64)
+        _check(load().fs_member_counts(self.handle, dev_ptr, int(n), int(rows), _p(out)))
+        return [int(x) for x in out[:rows]]
 
     def alloc(self, nbytes: int) -> DeviceBuffer:
         return DeviceBuffer(self, nbytes)

@@ -74,7 +74,48 @@ __global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ A
     }
 }
 
+// Nonzero bytes per row of a rows x n uint8 matrix (Assignment.member_counts,
+// solver.py:73-77): 16-byte loads, per-byte compare, block sum, one atomic per
+// block and row.
+__global__ void __launch_bounds__(256) row_count_kernel(const uint8_t* __restrict__ m, long long n,
+                                                        unsigned long long* __restrict__ counts) {
+    __shared__ unsigned int s_w[8];
+    const uint8_t* row = m + (long long)blockIdx.y * n;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    unsigned int c = 0;
+    const long long head = (16 - (long long)(reinterpret_cast<uintptr_t>(row) & 15)) & 15;
+    const long long h = head < n ? head : n;
+    const long long nv = (n - h) / 16;
+    const uint4* v = reinterpret_cast<const uint4*>(row + h);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 q = v[i];
+        c += __popc(__vcmpne4(q.x, 0u) & 0x01010101u) + __popc(__vcmpne4(q.y, 0u) & 0x01010101u) +
+             __popc(__vcmpne4(q.z, 0u) & 0x01010101u) + __popc(__vcmpne4(q.w, 0u) & 0x01010101u);
+    }
+    if (blockIdx.x == 0) {  // unaligned head and the tail
+        for (long long i = threadIdx.x; i < h; i += blockDim.x) c += row[i] != 0;
+        for (long long i = h + nv * 16 + threadIdx.x; i < n; i += blockDim.x) c += row[i] != 0;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < 8; ++w) t += s_w[w];
+        if (t) atomicAdd(counts + blockIdx.y, t);
+    }
+}
+
 }  // namespace
+
+void launch_row_counts(const uint8_t* m, long long n, int rows, unsigned long long* counts,
+                       cudaStream_t st) {
+    if (n <= 0 || rows <= 0) return;
+    long long bx = (n / 16 + 255) / 256;
+    if (bx > 148 * 4) bx = 148 * 4;
+    if (bx < 1) bx = 1;
+    row_count_kernel<<<dim3((unsigned)bx, (unsigned)rows), 256, 0, st>>>(m, n, counts);
+}
 
 void launch_finalize(const double* acc, float* out, long long n, int e, cudaStream_t st) {
     if (n <= 0 || e <= 0) return;

@@ -122,6 +122,8 @@ struct fs_context {
     size_t rn_labels_cap = 0;
     unsigned long long* rn_rect = nullptr;  // fs_render_mask: the full scene's tile rectangles
     size_t rn_rect_cap = 0;
+    unsigned long long* cnt = nullptr;      // fs_member_counts
+    size_t cnt_cap = 0;
 };
 
 
@@ -466,7 +468,8 @@ void fs_destroy(fs_context* ctx) {
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
                     (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out,
                     (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
-                    (void*)ctx->rn_u32, (void*)ctx->rn_labels, (void*)ctx->rn_rect})
+                    (void*)ctx->rn_u32, (void*)ctx->rn_labels, (void*)ctx->rn_rect,
+                    (void*)ctx->cnt})
         if (p) cudaFree(p);
     for (int k = 0; k < 2; ++k) {
         if (ctx->pinned_up[k]) cudaFreeHost(ctx->pinned_up[k]);
@@ -938,6 +941,22 @@ int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float
         if (tmpA) CK(cudaFreeAsync(tmpA, st));
         if (tmpO) CK(cudaFreeAsync(tmpO, st));
     }
+    CK(cudaStreamSynchronize(st));
+    return FS_OK;
+}
+
+int fs_member_counts(fs_context* ctx, const uint8_t* m, int64_t n, int rows, int64_t* counts) {
+    if (!ctx || !counts || (!m && n > 0 && rows > 0)) return fail(FS_EINVAL, "fs_member_counts: NULL argument");
+    if (n < 0 || rows < 0) return fail(FS_EINVAL, "fs_member_counts: bad shape");
+    if (rows == 0) return FS_OK;
+    CK(cudaSetDevice(ctx->device));
+    int rc = grow(&ctx->cnt, &ctx->cnt_cap, (size_t)rows);
+    if (rc) return rc;
+    cudaStream_t st = cudaStreamPerThread;
+    CK(cudaMemsetAsync(ctx->cnt, 0, sizeof(unsigned long long) * rows, st));
+    fs::launch_row_counts(m, n, rows, ctx->cnt, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(counts, ctx->cnt, sizeof(int64_t) * rows, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return FS_OK;
 }

@@ -133,5 +133,7 @@ void launch_raster_render(const RasterArgs& a, cudaStream_t st);
 void launch_finalize(const double* acc, float* out, long long n, int e, cudaStream_t st);
 void launch_assign(const float* A, long long n, int e, float gamma, int mode, uint8_t* out,
                    cudaStream_t st);
+void launch_row_counts(const uint8_t* m, long long n, int rows, unsigned long long* counts,
+                       cudaStream_t st);
 
 }  // namespace fs

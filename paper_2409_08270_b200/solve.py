@@ -114,7 +114,10 @@ class LabelSolver:
                        n=n, e=e, out_ptr=self._out_cur.ptr)
             labels = self.ctx.pinned_empty((n,), np.uint8)
             self._out_cur.to_host(labels)
-            return Assignment(mode="binary", gamma=gamma, labels=labels)
+            asn = Assignment(mode="binary", gamma=gamma, labels=labels)
+            fg = self.ctx.member_counts(self._out_cur.ptr, n, 1)[0]
+            asn._device_counts = [n - fg, fg]  # member_counts() without a host pass
+            return asn
         if mode == "scene":
             if e < 2:
                 raise ValueError(f"scene assignment requires E>=2, got E={e}")
@@ -122,7 +125,9 @@ class LabelSolver:
                        n=n, e=e, out_ptr=self._out_cur.ptr)
             member = self.ctx.pinned_empty((e, n), np.uint8)
             self._out_cur.to_host(member)
-            return Assignment(mode="scene", gamma=gamma, membership=member)
+            asn = Assignment(mode="scene", gamma=gamma, membership=member)
+            asn._device_counts = self.ctx.member_counts(self._out_cur.ptr, n, e)
+            return asn
         raise ValueError(f"unknown assignment mode {mode!r}")
 
 

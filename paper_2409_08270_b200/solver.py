@@ -60,6 +60,9 @@ class Assignment:
         return self.membership[object_id].astype(bool)
 
     def member_counts(self) -> list:
+        cached = getattr(self, "_device_counts", None)  # counted on the GPU by LabelSolver.assign
+        if cached is not None:
+            return list(cached)
         if self.mode == "binary":
             fg = int(np.count_nonzero(self.labels))
             return [self.num_gaussians - fg, fg]

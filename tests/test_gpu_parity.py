@@ -320,11 +320,33 @@ def test_label_solver_resident_matrix():
     s = LabelSolver(wl.scene)
     M = s.accumulate(wl.pairs(), 4)
     for g in (-0.4, 0.0, 0.5):
-        assert np.array_equal(s.assign(g, "scene").membership, oracle.assign_scene(M.values, g))
+        asn = s.assign(g, "scene")
+        assert np.array_equal(asn.membership, oracle.assign_scene(M.values, g))
+        # member counts taken on the device match the reference's host sum (solver.py:73-77)
+        assert asn.member_counts() == asn.membership.sum(axis=1, dtype=np.int64).tolist()
     wl2 = synth.make_workload(seed=8, n_gaussians=5000, n_views=2, width=96, height=64,
                               num_objects=2)
     M2, asn = fs.solve(wl2.scene, wl2.pairs(), 2, gamma=0.2)
     assert np.array_equal(asn.labels, oracle.assign_binary(M2.values, 0.2))
+    fg = int(np.count_nonzero(asn.labels))
+    assert asn.member_counts() == [len(asn.labels) - fg, fg]
+
+
+def test_member_counts_kernel_odd_shapes():
+    """fs_member_counts on unaligned, ragged rows with arbitrary nonzero bytes."""
+    ctx = _native.context(0)
+    rng = np.random.default_rng(9)
+    for rows, n in ((1, 1), (3, 17), (5, 1000003), (2, 64)):
+        m = (rng.random((rows, n)) < 0.3).astype(np.uint8) * rng.integers(1, 256, (rows, n),
+                                                                          dtype=np.uint8)
+        buf = ctx.alloc(m.nbytes + 1)
+        # +1 byte offset: rows start unaligned
+        raw = np.zeros(m.nbytes + 1, np.uint8)
+        raw[1:] = m.ravel()
+        buf.from_host(raw)
+        got = ctx.member_counts(buf.ptr + 1, n, rows)
+        assert got == np.count_nonzero(m, axis=1).tolist()
+        buf.release()
 
 
 @pytest.mark.parametrize("n", [5000, 10000], ids=["medium", "merge"])
