@@ -168,7 +168,7 @@ def accumulate_contributions(
         ctx.set_scene(scene)
         acc = ctx.buffer("acc64", 8 * num_objects * n).zero()
         st = run_device_accumulate(ctx, views, num_objects, blend, acc.ptr)
-        out = np.empty((num_objects, n), dtype=np.float32)
+        out = ctx.pinned_empty((num_objects, n), np.float32)  # full-speed D2H (768 MB at C4)
         ctx.finalize(acc.ptr, n, num_objects, out=out)
     if stats is not None:
         stats.update(st)

@@ -87,13 +87,14 @@ def _device_partial_path(scene, views, mine, num_objects, blend, group, device, 
         st = accumulate_shard_checked(ctx, views, mine, num_objects, blend, acc.data_ptr(), group,
                                       device)
     dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-    out32 = torch.empty(num_objects * max(n, 1), dtype=torch.float32, device=acc.device)
     torch.cuda.synchronize(device)
-    with ctx.lock:
-        ctx.finalize(acc.data_ptr(), n, num_objects, out_ptr=out32.data_ptr())
+    host = ctx.pinned_empty((num_objects, n), np.float32)  # finalize D2H straight into it
+    if host.size:
+        with ctx.lock:
+            ctx.finalize(acc.data_ptr(), n, num_objects, out=host)
     if stats is not None:
         stats.update(st)
-    return out32[: num_objects * n].cpu().numpy().reshape(num_objects, n)
+    return host
 
 
 def _gpu_partial_host(scene, views, num_objects, blend) -> np.ndarray:

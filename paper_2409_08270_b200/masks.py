@@ -140,7 +140,7 @@ def accumulate_mask_files(scene, view_paths: Sequence, num_objects: int,
                 for k, v in st.items():
                     if isinstance(v, (int, float)):
                         totals[k] = totals.get(k, 0) + v
-            out = np.empty((num_objects, n), dtype=np.float32)
+            out = ctx.pinned_empty((num_objects, n), np.float32)
             if out.size:
                 ctx.finalize(acc.ptr, n, num_objects, out=out)
     if stats is not None:
