@@ -16,10 +16,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -160,26 +162,68 @@ int dev_alloc(T** p, size_t count) {
     return FS_OK;
 }
 
-constexpr size_t kUploadChunk = 8u << 20;  // pinned staging chunk (bytes)
+constexpr size_t kUploadChunk = 8u << 20;  // pinned staging chunk (bytes; 32 MB measured slower)
 
-// Host memcpy into pinned staging, split over a few threads: one core copies
-// ~10 GB/s, well below the DMA rate, so the scene upload was memcpy-bound.
+// Host memcpy into pinned staging, split over a persistent pool of threads:
+// one core copies ~10 GB/s, well below the DMA rate, so pageable uploads were
+// memcpy-bound (and spawning threads per 8 MB chunk cost ~0.2 ms a chunk).
+class CopyPool {
+public:
+    // 8 threads: 16 on the GPU hosts measured slower (host memory bandwidth)
+    CopyPool() : parts_(std::max(1u, std::min(8u, std::thread::hardware_concurrency()))) {
+        for (unsigned i = 1; i < parts_; ++i) std::thread([this, i] { worker(i); }).detach();
+    }
+    void copy(void* dst, const void* src, size_t bytes) {
+        if (parts_ == 1 || bytes < (2u << 20)) {
+            memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> caller(call_);  // one job at a time
+        {
+            std::lock_guard<std::mutex> g(m_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            pending_ = parts_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> g(m_);
+        done_.wait(g, [this] { return pending_ == 0; });
+    }
+
+private:
+    void part(unsigned i) {
+        const size_t per = (bytes_ + parts_ - 1) / parts_;
+        const size_t off = std::min(bytes_, per * i), n = std::min(bytes_ - off, per);
+        if (n) memcpy(dst_ + off, src_ + off, n);
+    }
+    void worker(unsigned i) {
+        unsigned seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            part(i);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    const unsigned parts_;
+    std::mutex call_, m_;
+    std::condition_variable cv_, done_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+    unsigned pending_ = 0, gen_ = 0;
+};
+
 void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-    static const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-    const unsigned parts = bytes < (2u << 20) ? 1u : hw;
-    if (parts == 1) {
-        memcpy(dst, src, bytes);
-        return;
-    }
-    const size_t per = (bytes + parts - 1) / parts;
-    std::vector<std::thread> th;
-    th.reserve(parts - 1);
-    for (unsigned p = 1; p < parts; ++p) {
-        const size_t off = std::min(bytes, per * p), m = std::min(bytes - off, per);
-        th.emplace_back([=] { memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, m); });
-    }
-    memcpy(dst, src, std::min(bytes, per));
-    for (auto& t : th) t.join();
+    static CopyPool* pool = new CopyPool();  // never destroyed: its threads are detached
+    pool->copy(dst, src, bytes);
 }
 
 // Page-locked (cudaMallocHost / cudaHostRegister) host range: the DMA engine
