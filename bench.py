@@ -453,8 +453,10 @@ def main():
         "clocks": clk_summary,
     }
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = {k: v for k, v in cpu_baseline(wl, args.cpu_views).items()
-                                if k != "seconds"}
+        # ~10 s of wall time on the host: three views per core (one per core per step in
+        # the --impl reference arm, which repeats it warmup + steps times)
+        k = args.cpu_views or 3 * (os.cpu_count() or 1)
+        line["cpu_baseline"] = {k2: v for k2, v in cpu_baseline(wl, k).items() if k2 != "seconds"}
     print(json.dumps(line), flush=True)
     if group is not None:
         dist.destroy_process_group()
