@@ -259,6 +259,11 @@ def test_edge_cases():
     A = accumulate_contributions(g, [(one, LabelMask(0, np.full((1, 1), 299, np.uint16)))], 300)
     assert A.values.shape == (300, 1) and A.values[299, 0] > 0 and A.values[:299].sum() == 0
     assert accumulate_contributions(g, [], 2).values.sum() == 0
+    # E = 1 (background only) and E = 9 (first count on the tiled transpose of K5)
+    for E in (1, 9):
+        lab = np.full((1, 1), E - 1, np.uint16)
+        A = accumulate_contributions(g, [(one, LabelMask(0, lab))], E).values
+        assert A.shape == (E, 1) and A[E - 1, 0] > 0 and A[:E - 1].sum() == 0
 
 
 def test_instance_overflow_retry():
