@@ -12,8 +12,9 @@
  *     thread-local message for the last failing call on this thread;
  *   - float64 host arrays are C-contiguous numpy layouts (N x 3 means,
  *     N x 4 unit quaternions (w, x, y, z), N x 3 scales, N opacities);
- *   - matrices are E x N row-major (ContributionMatrix.values layout,
- *     contributions.py:52-55);
+ *   - float32 matrices are E x N row-major (ContributionMatrix.values layout,
+ *     contributions.py:52-55); the float64 accumulator of fs_accumulate is
+ *     N x E (Gaussian-major) and fs_finalize converts between the two;
  *   - "device" pointers are CUDA device addresses on the context's device.
  */
 #ifndef FLASHSPLAT_B200_H

@@ -130,7 +130,7 @@ __device__ __forceinline__ double depth_of_key(unsigned long long k) {
     return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
 }
 
-// kRender = false: accumulate alpha*T into the E x N matrix (contributions.py:119-160).
+// kRender = false: accumulate alpha*T into the N x E float64 accumulator (contributions.py:119-160).
 // kRender = true:  composite alpha, depth and an optional channel per pixel
 //                  (render_property, rasterizer.py:133-203); no mask, no atomics.
 template <bool kRender>
