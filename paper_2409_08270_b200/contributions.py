@@ -19,13 +19,12 @@ from __future__ import annotations
 
 import struct
 from dataclasses import dataclass
-from pathlib import Path
 from typing import Optional, Sequence
 
 import numpy as np
 
 from .rasterizer import DEFAULT_BLEND, BlendConfig
-from .scene import CameraView, GaussianScene
+from .scene import GaussianScene
 
 MATRIX_MAGIC = b"FSA1"  # reference contributions.py:26
 
