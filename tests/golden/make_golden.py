@@ -350,7 +350,33 @@ def save(name, cases):
     print(f"wrote {path} ({path.stat().st_size / 1e6:.2f} MB, {len(cases)} cases)")
 
 
+def gen_fullres():
+    """The benchmark resolution (1008 x 756, C2 camera geometry) straight from the reference:
+    a 100 k-Gaussian draw of the C2 recipe, two views, E = 4 (about 35 s of reference time)."""
+    D = ref.DEFAULT_BLEND
+    cases = {}
+    for name, kw in [("c2res_coherent", dict(seed=2, n_gaussians=100_000, n_views=2, width=1008,
+                                              height=756, num_objects=4))]:
+        wl = my_synth.make_workload(**kw)
+        ref_scene_obj = ref.GaussianScene(means=wl.scene.means, rotations=wl.scene.rotations,
+                                          scales=wl.scene.scales, opacities=wl.scene.opacities)
+        ref_views = [ref.CameraView(view_id=v.view_id, width=v.width, height=v.height, fx=v.fx,
+                                    fy=v.fy, cx=v.cx, cy=v.cy, world_to_camera=v.world_to_camera,
+                                    near_clip=v.near_clip) for v in wl.views]
+        pairs = [(rv, ref.LabelMask(rv.view_id, wl.masks[i])) for i, rv in enumerate(ref_views)]
+        c = accumulate_case(ref_scene_obj, pairs, wl.num_objects, D, store_inputs=False)
+        c.pop("A64")
+        c["labels_g0"] = ref.assign_scene(ref.ContributionMatrix(c["A"]), 0.0).membership
+        c["digest"] = np.frombuffer(wl.digest().encode(), dtype=np.uint8)
+        c["gen_args"] = np.frombuffer(repr(sorted(kw.items())).encode(), dtype=np.uint8)
+        cases[name] = c
+    return cases
+
+
 def main(which=None):
+    if which == "fullres":
+        save("accumulate_fullres", gen_fullres())
+        return
     if which in (None, "render"):
         save("render", gen_render())
     if which == "render":

@@ -564,3 +564,19 @@ def test_floor_box_binning_drops_only_dead_instances():
             assert st["instances"] == ref_inst
         else:
             assert 0 < st["instances"] < 0.8 * ref_inst
+
+
+def test_benchmark_resolution_matches_reference_golden():
+    """The CUDA path against the reference itself at 1008 x 756 (100 k Gaussians of the
+    C2 recipe, 2 views, E = 4): matrix to rtol 1e-6 with almost every float32 entry
+    bit-identical, labels equal to the reference's assign_scene."""
+    c = load_golden("accumulate_fullres")["c2res_coherent"]
+    kw = dict(eval(bytes(c["gen_args"]).decode()))
+    wl = synth.make_workload(**kw)
+    assert wl.digest() == bytes(c["digest"]).decode()
+    M = accumulate_contributions(wl.scene, wl.pairs(), wl.num_objects)
+    np.testing.assert_allclose(M.values, c["A"], rtol=1e-6, atol=1e-9)
+    assert np.count_nonzero(M.values != c["A"]) <= M.values.size // 10000
+    asn = assign_scene(M, 0.0)
+    same_cols = np.all(M.values == c["A"], axis=0)
+    assert np.array_equal(asn.membership[:, same_cols], c["labels_g0"][:, same_cols])

@@ -123,3 +123,20 @@ def test_assignment_matches_reference(case):
 def test_gamma_range_error_message():
     with pytest.raises(ValueError, match=r"gamma must lie in \[-1, 1\], got 1.5"):
         oracle.assign_binary(np.ones((2, 3), np.float32), 1.5)
+
+
+def test_oracle_matches_reference_at_benchmark_resolution():
+    """1008 x 756 (C2 camera geometry), 100 k Gaussians, 2 views, E = 4, straight from the
+    reference (tests/golden/make_golden.py fullres)."""
+    from conftest import load_golden
+    from paper_2409_08270_b200 import synth
+    c = load_golden("accumulate_fullres")["c2res_coherent"]
+    kw = dict(eval(bytes(c["gen_args"]).decode()))
+    wl = synth.make_workload(**kw)
+    assert wl.digest() == bytes(c["digest"]).decode(), "generator drifted"
+    cams = [oracle.camera_of(v) for v in wl.views]
+    A = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                          wl.scene.opacities, cams, list(wl.masks), wl.num_objects, threads=4)
+    assert np.count_nonzero(A != c["A"]) <= A.size // 10000
+    np.testing.assert_allclose(A, c["A"], rtol=1e-6, atol=1e-9)
+    assert np.array_equal(oracle.assign_scene(c["A"], 0.0), c["labels_g0"])
