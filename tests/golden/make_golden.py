@@ -370,6 +370,21 @@ def gen_fullres():
         c["digest"] = np.frombuffer(wl.digest().encode(), dtype=np.uint8)
         c["gen_args"] = np.frombuffer(repr(sorted(kw.items())).encode(), dtype=np.uint8)
         cases[name] = c
+        # novel-view rendering at the same resolution: render_view with a
+        # scalar channel on view 0 (20 000 sampled pixels + whole-image sums), and
+        # render_scene_mask of the reference's own labels on view 1 (all pixels)
+        t0 = time.perf_counter()
+        ch = np.random.default_rng(5).random(len(wl.scene))
+        out = ref.render_view(ref_scene_obj, ref_views[0], ch, D)
+        idx = np.sort(np.random.default_rng(6).choice(out.alpha.size, 20_000, replace=False))
+        cases[name + "_render"] = dict(  # channel = default_rng(5).random(N), not stored
+            idx=idx, alpha=out.alpha.ravel()[idx], depth=out.depth.ravel()[idx],
+            value=out.value.ravel()[idx],
+            sums=np.array([out.alpha.sum(), out.depth.sum(), out.value.sum()]))
+        asn = ref.Assignment(mode="scene", gamma=0.0, membership=c["labels_g0"])
+        m = ref.render_scene_mask(ref_scene_obj, asn, ref_views[1], 0.5)
+        cases[name + "_mask"] = dict(labels=m.labels, tau=np.float64(0.5))
+        print(f"  render + scene mask 1008x756: {time.perf_counter() - t0:.1f}s", flush=True)
     return cases
 
 

@@ -184,3 +184,24 @@ def test_tau_monotone_and_single_object_equals_binary():
                     membership=np.stack([~member, member]).astype(np.uint8))
     assert np.array_equal(render_scene_mask(scene, sc, view).labels,
                           render_binary_mask(scene, asn, view).labels)
+
+
+def test_render_at_benchmark_resolution_matches_reference():
+    """GPU render_view / render_scene_mask against the reference at 1008 x 756 (100 k
+    Gaussians of the C2 recipe; golden accumulate_fullres)."""
+    G = load_golden("accumulate_fullres")
+    c = G["c2res_coherent"]
+    wl = synth.make_workload(**dict(eval(bytes(c["gen_args"]).decode())))
+    assert wl.digest() == bytes(c["digest"]).decode()
+    r = G["c2res_coherent_render"]
+    ch = np.random.default_rng(5).random(len(wl.scene))
+    out = render_view(wl.scene, wl.views[0], ch)
+    for got, key in ((out.alpha, "alpha"), (out.depth, "depth"), (out.value, "value")):
+        np.testing.assert_allclose(np.asarray(got).ravel()[r["idx"]], r[key], rtol=1e-11,
+                                   atol=1e-14)
+    np.testing.assert_allclose([out.alpha.sum(), out.depth.sum(), out.value.sum()], r["sums"],
+                               rtol=1e-11)
+    m = G["c2res_coherent_mask"]
+    asn = Assignment(mode="scene", gamma=0.0, membership=c["labels_g0"])
+    got = render_scene_mask(wl.scene, asn, wl.views[1], float(m["tau"]))
+    assert np.array_equal(got.labels, m["labels"])

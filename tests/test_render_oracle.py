@@ -55,3 +55,24 @@ def test_render_known_answers():
     assert REN["subset_local"]["alpha"][8, 8] == pytest.approx(0.7, abs=1e-12)
     assert not REN["subset_empty"]["alpha"].any()
     assert REN["scene_tie"]["labels"][8, 8] == 1
+
+
+def test_oracle_render_at_benchmark_resolution():
+    """render_view (sampled pixels + whole-image sums) and render_scene_mask (all pixels)
+    of the reference at 1008 x 756, 100 k Gaussians (golden accumulate_fullres)."""
+    from paper_2409_08270_b200 import synth
+    G = load_golden("accumulate_fullres")
+    c = G["c2res_coherent"]
+    wl = synth.make_workload(**dict(eval(bytes(c["gen_args"]).decode())))
+    assert wl.digest() == bytes(c["digest"]).decode()
+    sc = (wl.scene.means, wl.scene.rotations, wl.scene.scales, wl.scene.opacities)
+    r = G["c2res_coherent_render"]
+    ch = np.random.default_rng(5).random(len(wl.scene))
+    value, alpha, depth = oracle.render_view(*sc, oracle.camera_of(wl.views[0]), ch)
+    for got, key in ((alpha, "alpha"), (depth, "depth"), (value, "value")):
+        np.testing.assert_allclose(got.ravel()[r["idx"]], r[key], rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose([alpha.sum(), depth.sum(), value.sum()], r["sums"], rtol=1e-12)
+    m = G["c2res_coherent_mask"]
+    labels = oracle.render_mask(*sc, oracle.camera_of(wl.views[1]), c["labels_g0"],
+                                float(m["tau"]))
+    assert np.array_equal(labels, m["labels"])
