@@ -580,3 +580,34 @@ def test_benchmark_resolution_matches_reference_golden():
     asn = assign_scene(M, 0.0)
     same_cols = np.all(M.values == c["A"], axis=0)
     assert np.array_equal(asn.membership[:, same_cols], c["labels_g0"][:, same_cols])
+
+
+def test_concurrent_calls_from_threads():
+    """The service calls assign from a thread pool (service.py:53-66): concurrent
+    assign_* and accumulate_contributions calls on one device give the same results
+    as serial ones."""
+    from concurrent.futures import ThreadPoolExecutor
+    rng = np.random.default_rng(17)
+    mats = [rng.random((2 if i % 2 == 0 else 5, 20_000), dtype=np.float32) for i in range(16)]
+    gammas = [(-0.5 + i / 16) for i in range(16)]
+
+    def one(i):
+        M = ContributionMatrix(mats[i])
+        if mats[i].shape[0] == 2:
+            return assign_binary(M, gammas[i]).labels
+        return assign_scene(M, gammas[i]).membership
+
+    with ThreadPoolExecutor(8) as ex:
+        got = list(ex.map(one, range(16)))
+    for i, g in enumerate(got):
+        ref = (oracle.assign_binary(mats[i], gammas[i]) if mats[i].shape[0] == 2
+               else oracle.assign_scene(mats[i], gammas[i]))
+        assert np.array_equal(g, ref), i
+    wl = synth.make_workload(seed=19, n_gaussians=5000, n_views=2, width=96, height=64,
+                             num_objects=3)
+    serial = accumulate_contributions(wl.scene, wl.pairs(), 3).values
+    with ThreadPoolExecutor(4) as ex:
+        outs = list(ex.map(lambda _: accumulate_contributions(wl.scene, wl.pairs(), 3).values,
+                           range(4)))
+    for o in outs:
+        np.testing.assert_allclose(o, serial, rtol=1e-6, atol=1e-9)
