@@ -78,3 +78,25 @@ def test_install_rebinds_mask_loading(splatlift):
     finally:
         splatlift_compat.uninstall()
     assert masks.load_mask_png is before
+
+
+def test_file_formats_byte_identical_to_reference(splatlift, tmp_path):
+    """FSA1 matrices and assignment files written by either package are byte-identical
+    and load in the other (contributions.py:70-87, solver.py:79-108)."""
+    import numpy as np
+    from paper_2409_08270_b200 import Assignment, ContributionMatrix
+    rng = np.random.default_rng(4)
+    A = rng.random((3, 11)).astype(np.float32)
+    ContributionMatrix(A).save(tmp_path / "ours.fsa")
+    splatlift.ContributionMatrix(A).save(tmp_path / "ref.fsa")
+    assert (tmp_path / "ours.fsa").read_bytes() == (tmp_path / "ref.fsa").read_bytes()
+    assert np.array_equal(splatlift.ContributionMatrix.load(tmp_path / "ours.fsa").values, A)
+    assert np.array_equal(ContributionMatrix.load(tmp_path / "ref.fsa").values, A)
+    for mode, kw in (("binary", dict(labels=rng.integers(0, 2, 13).astype(np.uint8))),
+                     ("scene", dict(membership=rng.integers(0, 2, (4, 13)).astype(np.uint8)))):
+        Assignment(mode, 0.25, **kw).save(tmp_path / f"ours_{mode}.bin")
+        splatlift.Assignment(mode=mode, gamma=0.25, **kw).save(tmp_path / f"ref_{mode}.bin")
+        assert ((tmp_path / f"ours_{mode}.bin").read_bytes()
+                == (tmp_path / f"ref_{mode}.bin").read_bytes())
+        back = splatlift.Assignment.load(tmp_path / f"ours_{mode}.bin")
+        assert back.mode == mode and back.member_counts() == Assignment(mode, 0.25, **kw).member_counts()
