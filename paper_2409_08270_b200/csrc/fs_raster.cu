@@ -100,6 +100,22 @@ __device__ __forceinline__ unsigned int warp_transpose32(unsigned int x, int lan
     return x;
 }
 
+// The same transpose when only rows 0..15 can be nonzero (a mini-batch has at
+// most 16 hits): the first stage (swap of the 16-bit halves with lane ^ 16) is
+// done by the caller's load -- lane l < 16 brings row l's low half, lane l >= 16
+// row (l - 16)'s high half -- so four shuffle stages remain.
+__device__ __forceinline__ unsigned int warp_transpose16x32(unsigned int x, int lane) {
+    const unsigned int masks[4] = {0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int b = 8 >> s;
+        const unsigned int m = masks[s];
+        const unsigned int y = __shfl_xor_sync(0xffffffffu, x, b);
+        x = (lane & b) ? ((x & ~m) | ((y & ~m) >> b)) : ((x & m) | ((y & m) << b));
+    }
+    return x;
+}
+
 // Candidate columns of one pixel row for one splat: the pixels whose float32
 // power clears the conservative cut, from the roots of the quadratic
 //   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
@@ -253,8 +269,12 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             Rec64 rq;
             if (lane < nm) rq = a.r64[W.gid[(head + lane) & (kRing - 1)]];
             // this lane's candidates of the mini-batch (bit k = k-th strip hit)
-            unsigned int mine = lane < nm ? W.cm[(head + lane) & (kRing - 1)] : 0u;
-            mine = warp_transpose32(mine, lane);
+            unsigned int mine = 0u;
+            if ((lane & 15) < nm) {
+                const unsigned int row = W.cm[(head + (lane & 15)) & (kRing - 1)];
+                mine = lane < 16 ? (row & 0xFFFFu) : (row >> 16);
+            }
+            mine = warp_transpose16x32(mine, lane);
             if (!active) mine = 0;
             // lane-major packing of the (splat, pixel) pairs: warp prefix sum
             const unsigned int n_mine = __popc(mine);
