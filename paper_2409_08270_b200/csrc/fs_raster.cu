@@ -85,25 +85,12 @@ __device__ __forceinline__ void red_add(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-// 32 x 32 bit-matrix transpose across the warp: lane i holds row i (bit j =
-// M[i][j]); on return lane j holds column j (bit i = M[i][j]).  Five
-// shuffle stages swap the off-diagonal blocks of halving size.
-__device__ __forceinline__ unsigned int warp_transpose32(unsigned int x, int lane) {
-    const unsigned int masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-        const int b = 16 >> s;
-        const unsigned int m = masks[s];
-        const unsigned int y = __shfl_xor_sync(0xffffffffu, x, b);
-        x = (lane & b) ? ((x & ~m) | ((y & ~m) >> b)) : ((x & m) | ((y & m) << b));
-    }
-    return x;
-}
-
-// The same transpose when only rows 0..15 can be nonzero (a mini-batch has at
-// most 16 hits): the first stage (swap of the 16-bit halves with lane ^ 16) is
-// done by the caller's load -- lane l < 16 brings row l's low half, lane l >= 16
-// row (l - 16)'s high half -- so four shuffle stages remain.
+// 32 x 32 bit-matrix transpose across the warp (lane i holds row i, bit j =
+// M[i][j]; on return lane j holds column j) when only rows 0..15 can be nonzero
+// (a mini-batch has at most 16 hits).  The full transpose swaps off-diagonal
+// blocks of halving size with five shuffles; its first stage (16-bit halves
+// between lane and lane ^ 16) is done by the caller's load -- lane l < 16 brings
+// row l's low half, lane l >= 16 row (l - 16)'s high half -- so four remain.
 __device__ __forceinline__ unsigned int warp_transpose16x32(unsigned int x, int lane) {
     const unsigned int masks[4] = {0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
