@@ -107,7 +107,8 @@ __device__ __forceinline__ unsigned int warp_transpose16x32(unsigned int x, int 
 // power clears the conservative cut, from the roots of the quadratic
 //   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
 // (widened by float32 rounding margins).  Returns a 16-bit column mask.
-__device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0) {
+__device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0,
+                                                       float inv_a) {
     if (!(s.cut > -INFINITY)) return 0xFFFFu;  // exact blend: no alpha floor
     const float dv = v_centre - s.my;
     const float Q = -2.0f * s.cut;
@@ -115,10 +116,9 @@ __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_c
     const float t1 = s.a * Q, t2 = detc * dv * dv;
     const float D = t1 - t2 + 1e-5f * (fabsf(t1) + fabsf(t2)) + 1e-20f;
     if (!(D >= 0.0f)) return 0u;
-    // approximate reciprocal / square root (MUFU): ~1e-7 relative, far inside the
-    // 0.03 px interval margin below
-    float inv_a, sq;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_a) : "f"(s.a));
+    // approximate square root (MUFU; inv_a likewise, once per splat by the caller):
+    // ~1e-7 relative, far inside the 0.03 px interval margin below
+    float sq;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));
     const float ctr = s.mx - 0.5f - s.b * dv * inv_a;
     const float half = sq * inv_a;
@@ -231,8 +231,11 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         if (idx + 64 < n_list) g_next2 = list[idx + 64];
         if (idx < n_list) {
             if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
-                  v_lo > s.my + s.hy))
-                cand = row_candidates(s, v_lo, x0) | (row_candidates(s, v_hi, x0) << 16);
+                  v_lo > s.my + s.hy)) {
+                float inv_a;  // shared by both rows (one MUFU instead of two)
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_a) : "f"(s.a));
+                cand = row_candidates(s, v_lo, x0, inv_a) | (row_candidates(s, v_hi, x0, inv_a) << 16);
+            }
         }
         steps += min(32u, n_list - c);
         const bool hit = cand != 0u;
