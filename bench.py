@@ -4,10 +4,16 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
 
 One step = one full label solve of the configuration's scene: for every view
-project -> depth sort -> bin -> raster-accumulate into the float64 E x N
-accumulator, (N>1: one NCCL all-reduce), float32 finalize, biased argmax.
-Views are sharded over ranks (strong scaling: the scene is fixed, more GPUs
-split its views).  ``value`` = view-pixels of the scene / device time per
+project -> depth sort -> bin -> raster-accumulate into the N x E accumulator
+(deterministic fixed-point by default, ``--acc f64`` for float64 atomics);
+N>1: reduce-scatter of the accumulator, float32 cast + biased argmax of the
+rank's Gaussian slice, all-gather of the matrix and labels; N=1: cast +
+argmax.  Views are sharded over ranks (strong scaling: the scene is fixed,
+more GPUs split its views).  ``--gpus N`` without torchrun re-launches itself
+under ``torch.distributed.run`` with N ranks (one per GPU).  After the timed
+region rank 0 re-solves the whole scene on its own GPU and compares: with the
+fixed-point accumulator the sharded matrix must be bit-identical
+(``shard_check``; at N=1 a 1-stream re-run checks schedule independence).  ``value`` = view-pixels of the scene / device time per
 step with inputs resident in HBM (CUDA events on the launching side, barrier
 + synchronize around the K steps, max over ranks).  ``e2e`` = the same
 metric through the public API ``solve()`` from host numpy inputs (scene +
@@ -37,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 # algorithmic bytes of one raster-accumulate launch
 BYTES_PER_PIXEL = 2          # uint16 label
 BYTES_PER_TILE_STEP = 36     # 4 B instance index + 32 B projected record
-BYTES_PER_ATOMIC = 8         # float64 accumulator add
+BYTES_PER_ATOMIC = {0: 8, 1: 16}  # accumulator add: float64 / fixed-point (hi, lo) words
 
 
 def parse():
@@ -55,7 +61,45 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-views", type=int, default=None)
+    ap.add_argument("--acc", default="fixed", choices=["fixed", "f64"],
+                    help="accumulator: deterministic fixed-point (default) or float64 atomics")
+    ap.add_argument("--no-check", action="store_true", help="skip the shard / rerun identity check")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="(tests) only report the rank layout; runs without a GPU (gloo)")
     return ap.parse_args()
+
+
+def self_launch(args) -> int:
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run, N ranks."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS setup in the log
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def launch_check(args, rank, world):
+    """Rank layout only (CPU test of the --gpus N launch path, gloo backend)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_08270_b200.distributed import shard_views
+    dist.init_process_group("gloo")
+    n_views = args.views or 200
+    mine = shard_views(n_views, rank, world)
+    t = torch.tensor([rank, len(mine), mine[0] if mine else -1], dtype=torch.int64)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "requested": args.gpus,
+                          "ranks": [[int(x) for x in o] for o in out]}), flush=True)
+    dist.destroy_process_group()
 
 
 def load_workload(name, views=None, gaussians=None, iid=False):
@@ -236,9 +280,13 @@ def run_reference(args, rank, world):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.launch_check:
+        return launch_check(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -246,7 +294,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2409_08270_b200 import _native, solve
-    from paper_2409_08270_b200.distributed import shard_views
+    from paper_2409_08270_b200.distributed import alloc_accumulator, padded_rows, shard_views
 
     torch.cuda.set_device(local)
     group = None
@@ -265,23 +313,43 @@ def main():
     # inputs resident in HBM before the timed region: this rank's masks
     masks_dev = torch.from_numpy(np.ascontiguousarray(wl.masks[mine]).view(np.int16)).cuda()
     mask_ptrs = [masks_dev[i].data_ptr() for i in range(len(mine))]
-    acc = torch.zeros(E * N, dtype=torch.float64, device="cuda")
+    kind = _native.ACC_FIXED if args.acc == "fixed" else _native.ACC_F64
+    acc = alloc_accumulator(N, E, world, kind, "cuda")
     A32 = torch.empty(E * N, dtype=torch.float32, device="cuda")
-    out = torch.empty(N, dtype=torch.uint8, device="cuda")
     mode = _native.MODE_BINARY if E == 2 else _native.MODE_SCENE
-    if mode == _native.MODE_SCENE:
-        out = torch.empty(E * N, dtype=torch.uint8, device="cuda")
+    rows = 1 if mode == _native.MODE_BINARY else E
+    out = torch.empty(rows * N, dtype=torch.uint8, device="cuda")
     floors = (1.0 / 255.0, 1e-4)
+    chunk = padded_rows(N, world) // world
+    g0, g1 = rank * chunk, min(N, rank * chunk + chunk)
+    part = torch.empty(acc.numel() // world, dtype=acc.dtype, device="cuda")
+    A_sl = torch.zeros((E, chunk), dtype=torch.float32, device="cuda")
+    L_sl = torch.zeros((rows, chunk), dtype=torch.uint8, device="cuda")
+    A_all = torch.empty((world, E, chunk), dtype=torch.float32, device="cuda")
+    L_all = torch.empty((world, rows, chunk), dtype=torch.uint8, device="cuda")
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 
     def step(timing=False):
         acc.zero_()
         st = ctx.accumulate(views, mask_ptrs, E, floors[0], floors[1], acc.data_ptr(),
-                            masks_on_device=True)
-        if group is not None:
-            dist.all_reduce(acc, group=group)
-        ctx.finalize(acc.data_ptr(), N, E, out_ptr=A32.data_ptr())
-        _native.assign(None, 0.0, mode, ctx=ctx, on_device_ptr=A32.data_ptr(), n=N, e=E,
-                       out_ptr=out.data_ptr())
+                            masks_on_device=True, acc_kind=kind)
+        if group is None:
+            ctx.finalize(acc.data_ptr(), N, E, out_ptr=A32.data_ptr(), acc_kind=kind)
+            _native.assign(None, 0.0, mode, ctx=ctx, on_device_ptr=A32.data_ptr(), n=N, e=E,
+                           out_ptr=out.data_ptr())
+            return st
+        # reduce-scatter by Gaussian slices -> cast + argmax of this rank's
+        # slice -> all-gather of matrix and labels -> the API's E x N layout
+        dist.reduce_scatter_tensor(part, acc, group=group)
+        if g1 > g0:
+            ctx.reduce_finalize([part.data_ptr()], g0, N, E, g0, g1, A_sl.data_ptr(), chunk,
+                                out_on_device=True, acc_kind=kind)
+        _native.assign(None, 0.0, mode, ctx=ctx, on_device_ptr=A_sl.data_ptr(), n=chunk, e=E,
+                       out_ptr=L_sl.data_ptr())
+        dist.all_gather_into_tensor(A_all, A_sl, group=group)
+        dist.all_gather_into_tensor(L_all, L_sl, group=group)
+        A32.view(E, N).copy_(A_all.permute(1, 0, 2).reshape(E, world * chunk)[:, :N])
+        out.view(rows, N).copy_(L_all.permute(1, 0, 2).reshape(rows, world * chunk)[:, :N])
         return st
 
     stats = []
@@ -314,6 +382,7 @@ def main():
 
     # ---- end to end through the public API (host inputs, host outputs) ----
     e2e = None
+    det = kind == _native.ACC_FIXED
     if not args.no_e2e:
         from paper_2409_08270_b200 import pin_inputs
         # inputs staged once in page-locked host memory (the serving setup);
@@ -324,7 +393,7 @@ def main():
         d2h = int(E * N * 4 + (N if E == 2 else E * N))
         reps = max(1, min(args.steps, 3))
         solve(scene_h, pairs, E, 0.0, "binary" if E == 2 else "scene",
-              process_group=group)  # warm
+              process_group=group, deterministic=det)  # warm
         torch.cuda.synchronize()
         if group is not None:
             dist.barrier()
@@ -334,18 +403,21 @@ def main():
         for _ in range(reps):
             ctx_cached = _native.context(local)
             ctx_cached._scene_key = None  # re-upload the scene every step
-            solve(scene_h, pairs, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
+            solve(scene_h, pairs, E, 0.0, "binary" if E == 2 else "scene", process_group=group,
+                  deterministic=det)
         b.record()
         torch.cuda.synchronize()
         e_s = a.elapsed_time(b) / 1e3
         # one more (warm) solve from the plain pageable numpy inputs, for reference
         pairs_pg = wl.pairs()
-        solve(wl.scene, pairs_pg, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
+        solve(wl.scene, pairs_pg, E, 0.0, "binary" if E == 2 else "scene", process_group=group,
+              deterministic=det)
         ctx_cached._scene_key = None
         torch.cuda.synchronize()
         c = torch.cuda.Event(enable_timing=True)
         c.record()
-        solve(wl.scene, pairs_pg, E, 0.0, "binary" if E == 2 else "scene", process_group=group)
+        solve(wl.scene, pairs_pg, E, 0.0, "binary" if E == 2 else "scene", process_group=group,
+              deterministic=det)
         d = torch.cuda.Event(enable_timing=True)
         d.record()
         torch.cuda.synchronize()
@@ -370,19 +442,48 @@ def main():
     # from one more (untimed for `value`) pass on a 1-stream context with CUDA
     # events around every raster launch on its stream.
     ctx1 = _native.Context(local, streams=1)
+    ctx1.set_stream(torch.cuda.current_stream().cuda_stream)
     ctx1.set_scene(wl.scene)
     ctx1.set_timing(True)
     iso = None
+    A_ts = A32.clone()  # the timed run's matrix and labels (all-gathered when sharded)
+    L_ts = out.clone()
     for _ in range(2):
         acc.zero_()
         iso = ctx1.accumulate(views, mask_ptrs, E, floors[0], floors[1], acc.data_ptr(),
-                              masks_on_device=True)
+                              masks_on_device=True, acc_kind=kind)
+    # ---- identity check: the whole scene re-solved on this GPU alone, on one
+    # stream (a different schedule), against the timed run's matrix / labels ----
+    check = None
+    if not args.no_check:
+        ctx1.set_timing(False)
+        if world > 1:
+            acc_c = alloc_accumulator(N, E, 1, kind, "cuda")
+            ctx1.accumulate(wl.views, list(wl.masks), E, floors[0], floors[1], acc_c.data_ptr(),
+                            acc_kind=kind)
+        else:
+            acc_c = acc  # the 1-stream pass above covered every view
+        A_c = torch.empty(E * N, dtype=torch.float32, device="cuda")
+        ctx1.finalize(acc_c.data_ptr(), N, E, out_ptr=A_c.data_ptr(), acc_kind=kind)
+        L_c = torch.empty_like(out)
+        _native.assign(None, 0.0, mode, ctx=ctx1, on_device_ptr=A_c.data_ptr(), n=N, e=E,
+                       out_ptr=L_c.data_ptr())
+        torch.cuda.synchronize()
+        diff = (A_c - A_ts).abs()
+        check = {"reference": "single-GPU 1-stream re-solve of all %d views" % len(wl.views),
+                 "timed_run": f"{world} GPU(s), {args.streams} streams",
+                 "accumulator": args.acc,
+                 "matrix_bit_identical": bool(torch.equal(A_c.view(torch.int32),
+                                                          A_ts.view(torch.int32))),
+                 "entries_differing": int((A_c != A_ts).sum().item()),
+                 "max_abs_diff": float(diff.max().item()) if diff.numel() else 0.0,
+                 "label_flips": int((L_c != L_ts).sum().item())}
     ctx1.close()
     st = stats[-1]
     views_n = max(iso["views"], 1)
     raster_avg_s = iso["raster_ms"] / views_n / 1e3
     alg_bytes = (BYTES_PER_PIXEL * iso["view_pixels"] + BYTES_PER_TILE_STEP * iso["tile_steps"]
-                 + BYTES_PER_ATOMIC * iso["atomics"]) / views_n
+                 + BYTES_PER_ATOMIC[kind] * iso["atomics"]) / views_n
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / raster_avg_s / 1e9 if raster_avg_s > 0 else None
     traffic = None
@@ -397,7 +498,7 @@ def main():
         except Exception:
             traffic = None
     atom_rate = iso["atomics"] / views_n / raster_avg_s if raster_avg_s > 0 else None
-    atom_peak, atom_key, atom_sized = atomic_peak(E * N * 8)
+    atom_peak, atom_key, atom_sized = atomic_peak(E * N * BYTES_PER_ATOMIC[kind])
     clk_summary = clk.summary()
     sm_hz = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
     issue_peak = 148 * 4 * sm_hz  # warp-instructions / s (one issue slot per scheduler per clock)
@@ -411,7 +512,10 @@ def main():
                    "name": args.config + ("-iid" if args.iid else ""),
                    "gaussians": N, "views": len(wl.views),
                    "image": f"{wl.views[0].width}x{wl.views[0].height}", "num_objects": E,
-                   "parallelism": f"views sharded over {world} GPU(s)",
+                   "parallelism": f"views sharded over {world} GPU(s)" + (
+                       ", reduce-scatter + sliced cast/argmax + all-gather (NCCL)" if world > 1 else ""),
+                   "accumulator": "fixed-point (deterministic)" if kind == _native.ACC_FIXED
+                   else "float64 atomics",
                    "l2": "inputs larger than L2 (masks %.0f MB + scene %.0f MB)" % (
                        wl.masks.nbytes / 1e6, N * 88 / 1e6)},
         "solve_s_per_scene": s_per_step,
@@ -451,6 +555,7 @@ def main():
         "counters_per_step": {k: st[k] for k in ("emitted", "instances", "tile_steps",
                                                  "exact_evals", "atomics", "retried_views")},
         "clocks": clk_summary,
+        "shard_check": check,
     }
     if world == 1 and not args.no_cpu:
         # ~10 s of wall time on the host: three views per core (one per core per step in

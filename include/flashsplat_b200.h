@@ -35,6 +35,18 @@ extern "C" {
 #define FS_MODE_BINARY 0
 #define FS_MODE_SCENE 1
 
+/* Accumulator kinds (N x E, Gaussian-major, device memory, caller-zeroed).
+ * FS_ACC_F64:   one float64 per entry; float64 atomics, so the low bits of
+ *               an entry depend on the order the adds land in.
+ * FS_ACC_FIXED: two uint64 words per entry, (hi, lo) = (sum q >> 32,
+ *               sum q & 0xffffffff) for q = round(w * 2^59) per add; the
+ *               value is (hi * 2^32 + lo) * 2^-59.  Integer adds commute, so
+ *               the result is bit-identical for any schedule, stream count or
+ *               split of the views over GPUs (
+ *               test_contributions.py:160-168).  16 B per entry. */
+#define FS_ACC_F64 0
+#define FS_ACC_FIXED 1
+
 typedef struct fs_context fs_context;
 
 /* Pinhole view, scene.py:164-203 (CameraView). */
@@ -86,6 +98,11 @@ int fs_copy_to_device(fs_context *ctx, void *dst, const void *src, uint64_t byte
 int fs_copy_to_host(fs_context *ctx, void *dst, const void *src, uint64_t bytes);
 int fs_synchronize(fs_context *ctx);
 
+/* Stream the context's entry points order themselves after (an event recorded
+ * on it at entry; default NULL = the legacy default stream, which also covers
+ * torch's default stream).  No entry point synchronises the whole device. */
+int fs_set_stream(fs_context *ctx, void *stream);
+
 /* Page-locked host memory (DMA at full PCIe/C2C speed) for result arrays the
  * caller hands back to numpy -- the contribution matrix and the labels. */
 int fs_host_alloc(fs_context *ctx, uint64_t bytes, void **out);
@@ -127,25 +144,62 @@ int fs_bin_splats(fs_context *ctx, int64_t k, const double *mean2d, const double
 
 /* accumulate_contributions (contributions.py:90-116) / _accumulate_view
  * (contributions.py:119-160) for n_views views: adds every view's alpha*T
- * mass into acc (N x E float64 -- Gaussian-major, so one splat's labels share
- * cache lines -- DEVICE pointer, caller-zeroed).  masks[v] is
- * an H x W uint16 label grid, host or device (masks_on_device).  Labels must
- * be < num_objects (validated by the caller, contributions.py:104-114). */
+ * mass into acc (N x E, Gaussian-major so one splat's labels share cache
+ * lines, of acc_kind, DEVICE pointer, caller-zeroed).  masks[v] is an H x W
+ * uint16 label grid, host or device (masks_on_device).  A label >= num_objects
+ * returns FS_ELABEL with stats->label_error_view = the first such view
+ * (contributions.py:108-114). */
 int fs_accumulate(fs_context *ctx, int n_views, const fs_camera *cams,
                   const uint16_t *const *masks, int masks_on_device, int num_objects,
-                  double alpha_floor, double transmittance_floor, double *acc,
+                  double alpha_floor, double transmittance_floor, int acc_kind, void *acc,
                   fs_accumulate_stats *stats);
 
+/* The same over several contexts (one per GPU, the same scene uploaded to
+ * each) from ONE process: one host thread per context pops views from a
+ * shared queue whenever one of its streams frees up (dynamic load balance;
+ * contributions.py:103-116 -- A is additive over views) and accumulates into
+ * accs[i] on context i's device.  Host masks only.  view_ctx (optional,
+ * n_views) receives the context that ran each view.  With FS_ACC_FIXED the
+ * summed result does not depend on which GPU ran which view. */
+int fs_accumulate_multi(fs_context *const *ctxs, int n_ctx, int n_views, const fs_camera *cams,
+                        const uint16_t *const *masks, int num_objects, double alpha_floor,
+                        double transmittance_floor, int acc_kind, void *const *accs,
+                        int32_t *view_ctx, fs_accumulate_stats *stats);
+
 /* ContributionMatrix(total.astype(float32)) (contributions.py:116): the N x E
- * float64 device accumulator -> E x N float32 (the reference's layout), written
- * to host (out_on_device = 0) or device memory. */
-int fs_finalize(fs_context *ctx, const double *acc, int64_t n, int num_objects, float *out,
-                int out_on_device);
+ * device accumulator -> E x N float32 (the reference's layout), written to
+ * host (out_on_device = 0) or device memory. */
+int fs_finalize(fs_context *ctx, int acc_kind, const void *acc, int64_t n, int num_objects,
+                float *out, int out_on_device);
+
+/* Reduce + cast of the Gaussian slice [g0, g1): the sum of n_parts N x E
+ * accumulators (device pointers -- other GPUs' through peer memory, see
+ * fs_enable_peer_access; part rows start at Gaussian part_g0, e.g. the output
+ * of a reduce-scatter) -> float32 E x (g1 - g0) at out with row stride ld
+ * (out = element (0, g0) of the caller's matrix; host or device). */
+int fs_reduce_finalize(fs_context *ctx, int acc_kind, const void *const *parts, int n_parts,
+                       int64_t part_g0, int64_t n, int num_objects, int64_t g0, int64_t g1,
+                       float *out, int64_t ld, int out_on_device);
+
+/* Peer access from ctx's device to peer_device (NVLink P2P loads). */
+int fs_enable_peer_access(fs_context *ctx, int peer_device);
+
+/* After fs_accumulate_multi: context i reduces column slice i of A over all
+ * contexts' accumulators (peer-memory loads -- the reduce half of a
+ * reduce-scatter fused into the cast; staged copies when P2P is unavailable),
+ * casts it, runs the biased argmax on it (mode FS_MODE_BINARY / FS_MODE_SCENE,
+ * or -1 for none; solver.py:118-172) and copies both straight into the host
+ * outputs: out E x N float32, labels N (binary) or E x N (scene) uint8. */
+int fs_finalize_multi(fs_context *const *ctxs, int n_ctx, int acc_kind, void *const *accs,
+                      int64_t n, int num_objects, float *out, float gamma, int mode,
+                      uint8_t *labels);
 
 /* _one_vs_rest_wins + assign_binary / assign_scene (solver.py:118-172).
  * A is E x N float32; out is N (binary) or E x N (scene) uint8.  Host or
  * device pointers (on_device).  Reentrant: runs on the calling thread's
- * default stream; ctx may be NULL (device 0 / current device). */
+ * default stream with stream-ordered scratch and touches no context state
+ * (ctx only selects the device; NULL = current device), so it can run from
+ * many threads, also while fs_accumulate runs on the same context. */
 int fs_assign(fs_context *ctx, const float *A, int64_t n, int num_objects, float gamma, int mode,
               uint8_t *out, int on_device);
 

@@ -20,14 +20,24 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libflashsplat_b200.so"
 
 FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ELABEL = 0, 1, 2, 3, 4
 MODE_BINARY, MODE_SCENE = 0, 1
+# accumulator kinds (include/flashsplat_b200.h): float64 entries, or the
+# deterministic fixed-point pair of uint64 words (schedule-independent sums)
+ACC_F64, ACC_FIXED = 0, 1
+ACC_DEFAULT = ACC_FIXED
+
+
+def acc_entry_bytes(kind: int) -> int:
+    return 16 if kind == ACC_FIXED else 8
 
 # Every symbol include/flashsplat_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
-    "fs_copy_to_host", "fs_synchronize", "fs_host_alloc", "fs_host_free", "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
-    "fs_accumulate", "fs_finalize", "fs_assign", "fs_member_counts", "fs_render", "fs_render_splats", "fs_render_mask",
-    "fs_decode_mask_png",
+    "fs_copy_to_host", "fs_synchronize", "fs_set_stream", "fs_host_alloc", "fs_host_free",
+    "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_accumulate", "fs_accumulate_multi", "fs_finalize", "fs_reduce_finalize",
+    "fs_enable_peer_access", "fs_finalize_multi", "fs_assign", "fs_member_counts", "fs_render",
+    "fs_render_splats", "fs_render_mask", "fs_decode_mask_png",
 )
 
 
@@ -96,6 +106,7 @@ def load() -> ctypes.CDLL:
             "fs_copy_to_device": ([P, P, P, ctypes.c_uint64], I),
             "fs_copy_to_host": ([P, P, P, ctypes.c_uint64], I),
             "fs_synchronize": ([P], I),
+            "fs_set_stream": ([P, P], I),
             "fs_host_alloc": ([P, ctypes.c_uint64, ctypes.POINTER(P)], I),
             "fs_host_free": ([P, P], I),
             "fs_host_pinned": ([P, ctypes.c_uint64], I),
@@ -104,8 +115,12 @@ def load() -> ctypes.CDLL:
             "fs_project": ([P, P, P, P, P, P, P, P], I),
             "fs_bin": ([P, P, P, P, I64, ctypes.POINTER(I64)], I),
             "fs_bin_splats": ([P, I64, P, P, P, P, I, I, P, P, I64, ctypes.POINTER(I64)], I),
-            "fs_accumulate": ([P, I, P, P, I, I, D, D, P, P], I),
-            "fs_finalize": ([P, P, I64, I, P, I], I),
+            "fs_accumulate": ([P, I, P, P, I, I, D, D, I, P, P], I),
+            "fs_accumulate_multi": ([P, I, I, P, P, I, D, D, I, P, P, P], I),
+            "fs_finalize": ([P, I, P, I64, I, P, I], I),
+            "fs_reduce_finalize": ([P, I, P, I, I64, I64, I, I64, I64, P, I64, I], I),
+            "fs_enable_peer_access": ([P, I], I),
+            "fs_finalize_multi": ([P, I, I, P, I64, I, P, F, I, P], I),
             "fs_member_counts": ([P, P, I64, I, P], I),
             "fs_assign": ([P, P, I64, I, F, I, P, I], I),
             "fs_render": ([P, P, P, D, D, P, I, P, P, P], I),
@@ -208,6 +223,10 @@ class Context:
     def set_timing(self, enable: bool) -> None:
         _check(load().fs_set_timing(self.handle, 1 if enable else 0))
 
+    def set_stream(self, stream_handle: int) -> None:
+        """Order the context's work after this CUDA stream (e.g. torch's current stream)."""
+        _check(load().fs_set_stream(self.handle, int(stream_handle) or None))
+
     def close(self) -> None:
         for buf in getattr(self, "_buffers", {}).values():
             buf.release()
@@ -307,8 +326,9 @@ class Context:
         return offs, items[:count.value]
 
     def accumulate(self, views, masks, num_objects: int, alpha_floor: float, t_floor: float,
-                   acc_ptr: int, masks_on_device: bool = False) -> dict:
-        """Add every view's alpha*T mass into the N x E (Gaussian-major) float64 device buffer acc_ptr."""
+                   acc_ptr: int, masks_on_device: bool = False, acc_kind: int = ACC_DEFAULT) -> dict:
+        """Add every view's alpha*T mass into the N x E (Gaussian-major) device accumulator
+        acc_ptr of kind ``acc_kind`` (ACC_F64 / ACC_FIXED)."""
         nv = len(views)
         cams = (FsCamera * max(nv, 1))(*[camera_struct(v) for v in views])
         if masks_on_device:
@@ -320,12 +340,17 @@ class Context:
         L = load()
         rc = L.fs_accumulate(self.handle, nv, ctypes.byref(cams), ctypes.byref(ptrs),
                              1 if masks_on_device else 0, int(num_objects), float(alpha_floor),
-                             float(t_floor), acc_ptr, ctypes.byref(st))
+                             float(t_floor), int(acc_kind), acc_ptr, ctypes.byref(st))
         if rc == FS_ELABEL:
             raise LabelRangeError(L.fs_last_error().decode(errors="replace"),
                                   int(st.label_error_view))
         _check(rc)
         return st.as_dict()
+
+    def acc_buffer(self, num_objects: int, n: int, acc_kind: int = ACC_DEFAULT,
+                   role: str = "acc") -> "DeviceBuffer":
+        """Grow-only N x E accumulator of kind ``acc_kind`` (not zeroed)."""
+        return self.buffer(role, acc_entry_bytes(acc_kind) * int(num_objects) * max(int(n), 1))
 
     def buffer(self, role: str, nbytes: int) -> "DeviceBuffer":
         """Grow-only device scratch owned by the context, keyed by role."""
@@ -338,13 +363,22 @@ class Context:
         return buf
 
     def finalize(self, acc_ptr: int, n: int, e: int, out_ptr: int = None,
-                 out: np.ndarray = None):
-        """N x E float64 accumulator -> E x N float32 (host ``out`` or device ``out_ptr``)."""
+                 out: np.ndarray = None, acc_kind: int = ACC_DEFAULT):
+        """N x E accumulator -> E x N float32 (host ``out`` or device ``out_ptr``)."""
         if out is not None:
-            _check(load().fs_finalize(self.handle, acc_ptr, n, e, _p(out), 0))
+            _check(load().fs_finalize(self.handle, int(acc_kind), acc_ptr, n, e, _p(out), 0))
             return out
-        _check(load().fs_finalize(self.handle, acc_ptr, n, e, out_ptr, 1))
+        _check(load().fs_finalize(self.handle, int(acc_kind), acc_ptr, n, e, out_ptr, 1))
         return None
+
+    def reduce_finalize(self, parts, part_g0: int, n: int, e: int, g0: int, g1: int,
+                        out_ptr: int, ld: int, out_on_device: bool = True,
+                        acc_kind: int = ACC_DEFAULT) -> None:
+        """Sum of accumulator parts over Gaussians [g0, g1) -> float32 E x (g1-g0) at out_ptr."""
+        arr = (ctypes.c_void_p * len(parts))(*[int(p) for p in parts])
+        _check(load().fs_reduce_finalize(self.handle, int(acc_kind), arr, len(parts), int(part_g0),
+                                         int(n), int(e), int(g0), int(g1), out_ptr, int(ld),
+                                         1 if out_on_device else 0))
 
     def member_counts(self, dev_ptr: int, n: int, rows: int) -> list:
         """Nonzero bytes per row of a rows x n uint8 device matrix (fs_member_counts)."""
@@ -393,17 +427,18 @@ def assign(values: np.ndarray, gamma: float, mode: int, ctx: Context = None,
     L = load()
     if ctx is None:
         ctx = context()
-    with ctx.lock:
-        if on_device_ptr is not None:
-            _check(L.fs_assign(ctx.handle, on_device_ptr, int(n), int(e), float(gamma), int(mode),
-                               out_ptr, 1))
-            return None
-        values = np.ascontiguousarray(values, dtype=np.float32)
-        e, n = values.shape
-        out = np.zeros(n if mode == MODE_BINARY else (e, n), np.uint8)
-        _check(L.fs_assign(ctx.handle, _p(values), int(n), int(e), float(gamma), int(mode),
-                           _p(out), 0))
-        return out
+    # fs_assign is reentrant (per-thread stream, stream-ordered scratch, no
+    # context state): no lock, so service threads never wait on an accumulation
+    if on_device_ptr is not None:
+        _check(L.fs_assign(ctx.handle, on_device_ptr, int(n), int(e), float(gamma), int(mode),
+                           out_ptr, 1))
+        return None
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    e, n = values.shape
+    out = np.zeros(n if mode == MODE_BINARY else (e, n), np.uint8)
+    _check(L.fs_assign(ctx.handle, _p(values), int(n), int(e), float(gamma), int(mode),
+                       _p(out), 0))
+    return out
 
 
 _contexts: dict = {}
@@ -417,16 +452,50 @@ def default_device() -> int:
     return 0
 
 
-def context(device: int = None) -> Context:
-    """Process-wide cached context per device."""
+def context(device: int = None, slot: int = 0) -> Context:
+    """Process-wide cached context per device (``slot`` > 0: further independent
+    contexts on the same device, e.g. a device listed twice in ``devices=``)."""
     if device is None:
         device = default_device()
+    key = (int(device), int(slot))
     with _ctx_lock:
-        ctx = _contexts.get(device)
+        ctx = _contexts.get(key)
         if ctx is None:
-            ctx = Context(device)
-            _contexts[device] = ctx
+            ctx = Context(key[0])
+            _contexts[key] = ctx
         return ctx
+
+
+def accumulate_multi(ctxs, views, masks, num_objects: int, alpha_floor: float, t_floor: float,
+                     acc_ptrs, acc_kind: int = ACC_DEFAULT):
+    """fs_accumulate_multi: one host thread per context, shared dynamic view queue.
+    Returns (stats dict, per-view context index)."""
+    nv = len(views)
+    cams = (FsCamera * max(nv, 1))(*[camera_struct(v) for v in views])
+    keep = [np.ascontiguousarray(m, dtype=np.uint16) for m in masks]
+    ptrs = (ctypes.c_void_p * max(nv, 1))(*[k.ctypes.data for k in keep])
+    handles = (ctypes.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+    accs = (ctypes.c_void_p * len(ctxs))(*[int(p) for p in acc_ptrs])
+    owner = np.full(max(nv, 1), -1, np.int32)
+    st = FsAccumulateStats()
+    L = load()
+    rc = L.fs_accumulate_multi(handles, len(ctxs), nv, ctypes.byref(cams), ctypes.byref(ptrs),
+                               int(num_objects), float(alpha_floor), float(t_floor), int(acc_kind),
+                               accs, _p(owner), ctypes.byref(st))
+    if rc == FS_ELABEL:
+        raise LabelRangeError(L.fs_last_error().decode(errors="replace"), int(st.label_error_view))
+    _check(rc)
+    return st.as_dict(), owner[:nv]
+
+
+def finalize_multi(ctxs, acc_ptrs, n: int, e: int, out: np.ndarray, gamma: float = 0.0,
+                   mode: int = -1, labels: np.ndarray = None, acc_kind: int = ACC_DEFAULT) -> None:
+    """fs_finalize_multi: slice i of A reduced over all contexts' accumulators on context i
+    (peer-memory loads), cast, optionally argmax'ed, copied into host ``out`` / ``labels``."""
+    handles = (ctypes.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+    accs = (ctypes.c_void_p * len(ctxs))(*[int(p) for p in acc_ptrs])
+    _check(load().fs_finalize_multi(handles, len(ctxs), int(acc_kind), accs, int(n), int(e),
+                                    _p(out), float(gamma), int(mode), _p(labels)))
 
 
 def bin_splats(mean2d, depth, radius, index, width: int, height: int, device: int = None):

@@ -9,10 +9,18 @@ float64 accumulation on the device, one float32 cast at the end --
 ``contributions.py:116``).
 
 Views are independent and A is additive over views
-(``contributions.py:103-116``), so with ``process_group`` set (a
-``torch.distributed`` group, one process per GPU) every rank accumulates a
-disjoint shard of the views and one all-reduce of the float64 accumulator
-joins them (``distributed.py``).
+(``contributions.py:103-116``), so the views can be split over GPUs:
+``devices=[...]`` runs one host thread per GPU in this process with a shared
+dynamic view queue and reduces the per-GPU accumulators over NVLink peer
+memory inside the finalize (``multidevice.py``); ``process_group`` (a
+``torch.distributed`` group, one process per GPU) shards the views over the
+ranks and joins them with a reduce-scatter + all-gather (``distributed.py``).
+
+The accumulator is deterministic by default: fixed-point integer sums
+(``FS_ACC_FIXED``), so the matrix is bit-identical for any schedule and any
+number of GPUs (test_contributions.py:160-168).
+``deterministic=False`` -- and blends without floors (``EXACT_BLEND``), whose
+weights can underflow below any fixed-point resolution -- use float64 atomics.
 """
 
 from __future__ import annotations
@@ -117,13 +125,37 @@ def check_shapes(views: Sequence, num_objects: int) -> None:
             validate_views(views[: i + 1], num_objects)
 
 
-def run_device_accumulate(ctx, views: Sequence, num_objects: int, blend, acc_ptr) -> dict:
+# The fixed-point accumulator resolves 2^-60 per add; every add carries at least
+# one weight w = alpha*T >= alpha_floor * T_floor (T is checked against its
+# floor before the update, contributions.py:148-157), so its relative error is
+# at most 2^-60 / (alpha_floor * T_floor) -- 2e-12 for the default blend, far
+# inside the float32 result.  Without floors (EXACT_BLEND) weights can underflow
+# towards 1e-300 and only float64 covers that range.
+FIXED_MIN_WEIGHT = 2.0 ** -26
+
+
+def acc_kind_of(deterministic: bool, blend=None) -> int:
+    """Accumulator kind: fixed-point when deterministic and the blend's floors
+    bound the weights from below, float64 atomics otherwise."""
+    from . import _native
+    if not deterministic:
+        return _native.ACC_F64
+    if blend is not None and blend.alpha_floor * blend.transmittance_floor < FIXED_MIN_WEIGHT:
+        return _native.ACC_F64
+    return _native.ACC_FIXED
+
+
+def run_device_accumulate(ctx, views: Sequence, num_objects: int, blend, acc_ptr,
+                          acc_kind: Optional[int] = None) -> dict:
     """ctx.accumulate with the reference's label error reproduced on failure."""
     from . import _native
 
+    if acc_kind is None:
+        acc_kind = _native.ACC_DEFAULT
     try:
         return ctx.accumulate([v for v, _ in views], [m.labels for _, m in views], num_objects,
-                              blend.alpha_floor, blend.transmittance_floor, acc_ptr)
+                              blend.alpha_floor, blend.transmittance_floor, acc_ptr,
+                              acc_kind=acc_kind)
     except _native.LabelRangeError as err:
         validate_views([views[err.view]], num_objects)  # raises the reference message
         raise
@@ -136,15 +168,20 @@ def accumulate_contributions(
     blend: BlendConfig = DEFAULT_BLEND,
     *,
     device: Optional[int] = None,
+    devices: Optional[Sequence[int]] = None,
     process_group=None,
     stats: Optional[dict] = None,
+    deterministic: bool = True,
 ) -> ContributionMatrix:
     """Scatter every pixel's surviving alpha*T samples into label rows, on the GPU.
 
-    ``device``: CUDA ordinal (default: ``LOCAL_RANK`` or 0).  ``process_group``:
-    shard the views over a ``torch.distributed`` group and all-reduce the
-    accumulator (every rank returns the full matrix).  ``stats``: filled with
-    the library's counters (instances, tile steps, exact evaluations, ...).
+    ``device``: CUDA ordinal (default: ``LOCAL_RANK`` or 0).  ``devices``: split
+    the views over these GPUs from this process (dynamic queue, peer-memory
+    reduction).  ``process_group``: shard the views over a ``torch.distributed``
+    group (every rank returns the full matrix).  ``stats``: filled with the
+    library's counters (instances, tile steps, exact evaluations, ...).
+    ``deterministic``: fixed-point accumulator (default), bit-identical for any
+    schedule and GPU count; False: float64 atomics.
     """
     views = list(views)
     num_objects = int(num_objects)
@@ -152,12 +189,17 @@ def accumulate_contributions(
     if len(scene) == 0:
         validate_views(views, num_objects)
         return ContributionMatrix(values=np.zeros((num_objects, 0), dtype=np.float32))
+    kind = acc_kind_of(deterministic, blend)
     if process_group is not None:
         # shapes were checked above on every rank; label ranges are checked per
         # shard and agreed on (distributed.accumulate_shard_checked)
         from .distributed import accumulate_sharded
         values = accumulate_sharded(scene, views, num_objects, blend, process_group,
-                                    device=device, stats=stats)
+                                    device=device, stats=stats, acc_kind=kind)
+        return ContributionMatrix(values=values)
+    if devices is not None:
+        from .multidevice import solve_multi
+        values, _ = solve_multi(scene, views, num_objects, blend, devices, kind, stats=stats)
         return ContributionMatrix(values=values)
     from . import _native
 
@@ -165,10 +207,10 @@ def accumulate_contributions(
     n = len(scene)
     with ctx.lock:
         ctx.set_scene(scene)
-        acc = ctx.buffer("acc64", 8 * num_objects * n).zero()
-        st = run_device_accumulate(ctx, views, num_objects, blend, acc.ptr)
+        acc = ctx.acc_buffer(num_objects, n, kind).zero()
+        st = run_device_accumulate(ctx, views, num_objects, blend, acc.ptr, kind)
         out = ctx.pinned_empty((num_objects, n), np.float32)  # full-speed D2H (768 MB at C4)
-        ctx.finalize(acc.ptr, n, num_objects, out=out)
+        ctx.finalize(acc.ptr, n, num_objects, out=out, acc_kind=kind)
     if stats is not None:
         stats.update(st)
     return ContributionMatrix(values=out)

@@ -16,12 +16,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <mutex>
+#include <set>
 #include <thread>
 #include <vector>
 
@@ -80,6 +82,7 @@ struct Work {
     cudaEvent_t h2d_done = nullptr;
     bool h2d_pending = false;
     cudaEvent_t done = nullptr;
+    cudaEvent_t view_done = nullptr;  // last view enqueued on this stream (dynamic queue)
 };
 
 }  // namespace fs
@@ -97,6 +100,16 @@ struct fs_context {
     int view_log_cap = 0;
     std::vector<fs::Work> work;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+    // entry points order their streams after the caller's stream (fs_set_stream;
+    // default: the legacy default stream) with this event -- no device-wide sync
+    cudaStream_t caller_stream = nullptr;
+    cudaEvent_t ev_caller = nullptr;
+    float* fin_tmp = nullptr;     // fs_reduce_finalize: E x slice float32 (host output)
+    size_t fin_tmp_cap = 0;
+    uint8_t* fin_lab = nullptr;   // fs_finalize_multi: the slice's labels
+    size_t fin_lab_cap = 0;
+    unsigned char* fin_stage = nullptr;  // peer parts staged when P2P access is unavailable
+    size_t fin_stage_cap = 0;
     bool timing = false;
     std::vector<cudaEvent_t> stage_events;  // 4 per view when timing
     // grow-only scratch reused across calls (no cudaMalloc/cudaFree per call)
@@ -106,11 +119,6 @@ struct fs_context {
     double* up_scales = nullptr;
     unsigned char* pinned_up[2] = {nullptr, nullptr};  // host->device staging ring
     cudaEvent_t pinned_free[2] = {nullptr, nullptr};
-    float* tmp_f32 = nullptr;     // fs_finalize to host
-    size_t tmp_f32_cap = 0;
-    float* asg_in = nullptr;      // fs_assign with host buffers
-    uint8_t* asg_out = nullptr;
-    size_t asg_in_cap = 0, asg_out_cap = 0;
     // novel-view rendering (fs_render*): outputs, inputs, mask combine
     double* rn_f64 = nullptr;     // alpha | depth | value (H*W*(2 + C))
     size_t rn_f64_cap = 0;
@@ -271,6 +279,15 @@ int upload(fs_context* ctx, void* dst, const void* src, size_t bytes, cudaStream
     return FS_OK;
 }
 
+// Blocking copy ordered on one of the context's (non-blocking) streams: unlike
+// cudaMemcpy on the legacy default stream it never waits for other threads'
+// work on the device (a concurrent fs_assign, an NCCL stream).
+cudaError_t sync_copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                      cudaStream_t st) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+    return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+}
+
 template <typename T>
 int grow(T** p, size_t* cap, size_t count) {
     if (count <= *cap && *p) return FS_OK;
@@ -295,6 +312,7 @@ void free_work(fs::Work& w) {
     if (w.pinned) cudaFreeHost(w.pinned);
     if (w.h2d_done) cudaEventDestroy(w.h2d_done);
     if (w.done) cudaEventDestroy(w.done);
+    if (w.view_done) cudaEventDestroy(w.view_done);
     if (w.stream) cudaStreamDestroy(w.stream);
     w = fs::Work{};
 }
@@ -413,7 +431,7 @@ int view_launches() { return 1 + 4 + 1; }
 
 // One view of fs_accumulate; its counters live in `log` (zeroed by the caller).
 void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uint16_t* mask,
-                  int num_objects, double alpha_floor, double t_floor, double* acc,
+                  int num_objects, double alpha_floor, double t_floor, int acc_kind, void* acc,
                   fs::ViewCounters* log, cudaEvent_t* ev = nullptr) {
     if (ev) cudaEventRecord(ev[0], w.stream);
     enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr, log);
@@ -432,16 +450,319 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.sort = tile_sort_args(w, nullptr, log);
     ra.r32 = w.r32;
     ra.r64 = w.r64;
-    ra.acc = acc;
+    if (acc_kind == FS_ACC_FIXED)
+        ra.acc_fixed = static_cast<unsigned long long*>(acc);
+    else
+        ra.acc = static_cast<double*>(acc);
     ra.vc = log;
     ra.tile_order = w.tile_order;
     fs::launch_raster(ra, w.stream);
     if (ev) cudaEventRecord(ev[3], w.stream);
 }
 
+// Orders the context's streams after the caller's stream (fs_set_stream; by
+// default the legacy default stream, which is where torch's default stream
+// and the synchronous CUDA calls of other libraries land): work enqueued before
+// the call -- zeroing an accumulator, an NCCL reduction the caller waited on --
+// completes before our kernels touch it.  Unlike cudaDeviceSynchronize this does
+// not wait for other threads' independent work (a concurrent fs_assign).
+int order_after_caller(fs_context* ctx) {
+    CK(cudaEventRecord(ctx->ev_caller, ctx->caller_stream));
+    for (auto& w : ctx->work) CK(cudaStreamWaitEvent(w.stream, ctx->ev_caller, 0));
+    return FS_OK;
+}
+
 unsigned int initial_inst_cap(long long n) {
     long long c = std::max<long long>(1 << 22, 4 * n);
     return (unsigned int)std::min<long long>(c, 0x7fffffffLL);
+}
+
+// ---- accumulation runtime (fs_accumulate / fs_accumulate_multi) ----
+
+// Validated view list: sizes for the workspaces.
+struct ViewPlan {
+    int n_views = 0;
+    int max_tiles = 1;
+    size_t max_px = 1;
+    long long view_px = 0;
+};
+
+int plan_views(int n_views, const fs_camera* cams, const uint16_t* const* masks, int num_objects,
+               int acc_kind, ViewPlan& p) {
+    if (n_views < 0 || (n_views > 0 && (!cams || !masks)))
+        return fail(FS_EINVAL, "fs_accumulate: bad view arguments");
+    if (num_objects < 1 || num_objects > 65536)
+        return fail(FS_EINVAL, "fs_accumulate: num_objects must be in [1, 65536], got %d", num_objects);
+    if (acc_kind != FS_ACC_F64 && acc_kind != FS_ACC_FIXED)
+        return fail(FS_EINVAL, "bad accumulator kind %d", acc_kind);
+    p.n_views = n_views;
+    int rc;
+    for (int v = 0; v < n_views; ++v) {
+        if ((rc = check_cam(cams[v], v))) return rc;
+        if (!masks[v]) return fail(FS_EINVAL, "view %d: NULL mask", v);
+        p.max_tiles = std::max(p.max_tiles, fs::tiles_x_of(cams[v].width) * fs::tiles_y_of(cams[v].height));
+        p.max_px = std::max(p.max_px, (size_t)cams[v].width * cams[v].height);
+        p.view_px += (long long)cams[v].width * cams[v].height;
+    }
+    return FS_OK;
+}
+
+// One context's share of an accumulation.
+struct CtxRun {
+    std::vector<int> views;             // global view indices run here, in enqueue order
+    std::vector<fs::ViewCounters> log;  // their counters, same order
+    double gpu_ms = 0, prep_ms = 0, bin_ms = 0, raster_ms = 0;
+    long long launches = 0, retried = 0;
+};
+
+// Host mask of one view -> the workspace's device mask buffer, on its stream
+// (stream order keeps it behind the previous view's raster).  Page-locked
+// sources are DMA'd directly; pageable ones go through the stream's pinned
+// buffer, whose previous copy must have finished first.
+int stage_mask(fs::Work& w, const fs_camera& cam, const uint16_t* src, const uint16_t** dev) {
+    const size_t bytes = (size_t)cam.width * cam.height * sizeof(uint16_t);
+    if (host_pinned(src, bytes)) {
+        CK(cudaMemcpyAsync(w.mask_dev, src, bytes, cudaMemcpyHostToDevice, w.stream));
+    } else {
+        if (w.h2d_pending) CK(cudaEventSynchronize(w.h2d_done));
+        parallel_memcpy(w.pinned, src, bytes);
+        CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
+        CK(cudaEventRecord(w.h2d_done, w.stream));
+        w.h2d_pending = true;
+    }
+    *dev = w.mask_dev;
+    return FS_OK;
+}
+
+// Accumulates views into acc on ctx's device.  queue == nullptr: views 0..n-1
+// round-robin over the context's streams, all enqueued at once.  Otherwise
+// views are popped from the shared queue, at most one in flight per stream, so
+// several contexts (GPUs) share the list dynamically.  Each view runs
+// project -> bin -> raster on one stream with its counters in a zeroed slot of
+// the view log; the log is read back once, and views whose instance count
+// overflowed the buffers (the raster skipped them, nothing was added) are
+// re-run after growing them.
+int accumulate_on(fs_context* ctx, const ViewPlan& plan, const fs_camera* cams,
+                  const uint16_t* const* masks, int masks_on_device, int num_objects,
+                  double alpha_floor, double t_floor, int acc_kind, void* acc,
+                  std::atomic<int>* queue, CtxRun& R) {
+    CK(cudaSetDevice(ctx->device));
+    int rc;
+    const int n_views = plan.n_views;
+    const size_t mask_px = masks_on_device ? 1 : plan.max_px;
+    for (auto& w : ctx->work) {
+        unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
+        if ((rc = ensure_work(ctx, w, ctx->n, plan.max_tiles, cap, mask_px))) return rc;
+    }
+    if (n_views > ctx->view_log_cap) {
+        if ((rc = dev_alloc(&ctx->view_log, (size_t)n_views))) return rc;
+        ctx->view_log_cap = n_views;
+    }
+    const int S = (int)ctx->work.size();
+    fs::Work& w0 = ctx->work[0];
+    if (ctx->timing) {
+        while ((int)ctx->stage_events.size() < 4 * n_views) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ctx->stage_events.push_back(e);
+        }
+    }
+    if ((rc = order_after_caller(ctx))) return rc;
+    CK(cudaMemsetAsync(ctx->view_log, 0, sizeof(fs::ViewCounters) * (size_t)n_views, w0.stream));
+    CK(cudaEventRecord(ctx->ev_start, w0.stream));
+    for (int s = 1; s < S; ++s) CK(cudaStreamWaitEvent(ctx->work[s].stream, ctx->ev_start, 0));
+    R.views.clear();
+    for (int i = 0;; ++i) {
+        fs::Work& w = ctx->work[i % S];
+        if (queue && i >= S) CK(cudaEventSynchronize(w.view_done));  // this stream's last view
+        const int v = queue ? queue->fetch_add(1) : i;
+        if (v >= n_views) break;
+        const uint16_t* mask = masks[v];
+        if (!masks_on_device && (rc = stage_mask(w, cams[v], masks[v], &mask))) return rc;
+        enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc_kind,
+                     acc, ctx->view_log + i, ctx->timing ? &ctx->stage_events[4 * i] : nullptr);
+        if (queue) CK(cudaEventRecord(w.view_done, w.stream));
+        R.views.push_back(v);
+        R.launches += view_launches();
+    }
+    CK(cudaGetLastError());
+    for (int s = 1; s < S; ++s) {
+        CK(cudaEventRecord(ctx->work[s].done, ctx->work[s].stream));
+        CK(cudaStreamWaitEvent(w0.stream, ctx->work[s].done, 0));
+    }
+    CK(cudaEventRecord(ctx->ev_stop, w0.stream));
+    CK(cudaEventSynchronize(ctx->ev_stop));
+    for (auto& w : ctx->work) w.h2d_pending = false;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_stop));
+    R.gpu_ms = ms;
+    const int k = (int)R.views.size();
+    if (ctx->timing) {
+        for (int i = 0; i < k; ++i) {
+            float a = 0, b = 0, c = 0;
+            cudaEvent_t* e = &ctx->stage_events[4 * i];
+            CK(cudaEventElapsedTime(&a, e[0], e[1]));
+            CK(cudaEventElapsedTime(&b, e[1], e[2]));
+            CK(cudaEventElapsedTime(&c, e[2], e[3]));
+            R.prep_ms += a;
+            R.bin_ms += b;
+            R.raster_ms += c;
+        }
+    }
+    R.log.resize(k);
+    if (k) CK(sync_copy(R.log.data(), ctx->view_log, sizeof(fs::ViewCounters) * k,
+                        cudaMemcpyDeviceToHost, w0.stream));
+    for (int j = 0; j < k; ++j) {
+        if (!R.log[j].overflow) continue;
+        const int v = R.views[j];
+        const unsigned int need = (unsigned int)std::min<unsigned long long>(
+            0x7fffffffull, (unsigned long long)R.log[j].n_instances + R.log[j].n_instances / 4 + 1024);
+        for (auto& o : ctx->work)  // later calls start with the grown capacity
+            if (o.inst_cap < need && (rc = ensure_work(ctx, o, ctx->n, plan.max_tiles, need, mask_px)))
+                return rc;
+        const uint16_t* mask = masks[v];
+        if (!masks_on_device && (rc = stage_mask(w0, cams[v], masks[v], &mask))) return rc;
+        CK(cudaMemsetAsync(ctx->view_log + j, 0, sizeof(fs::ViewCounters), w0.stream));
+        enqueue_view(ctx, w0, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc_kind,
+                     acc, ctx->view_log + j);
+        CK(cudaGetLastError());
+        CK(sync_copy(&R.log[j], ctx->view_log + j, sizeof(fs::ViewCounters), cudaMemcpyDeviceToHost,
+                     w0.stream));
+        w0.h2d_pending = false;
+        if (R.log[j].overflow) return fail(FS_ENOMEM, "view %d: instance buffer overflow after retry", v);
+        ++R.retried;
+        R.launches += view_launches();
+    }
+    return FS_OK;
+}
+
+// Totals over the contexts' runs; the label range error of the first offending
+// view in the caller's order (contributions.py:104-114).
+int finish_stats(const CtxRun* R, int n_ctx, const ViewPlan& plan, int num_objects,
+                 fs_accumulate_stats* stats) {
+    long long bad_view = -1;
+    unsigned int bad_label = 0;
+    for (int c = 0; c < n_ctx; ++c)
+        for (size_t j = 0; j < R[c].views.size(); ++j)
+            if (R[c].log[j].max_label >= (unsigned)num_objects &&
+                (bad_view < 0 || R[c].views[j] < bad_view)) {
+                bad_view = R[c].views[j];
+                bad_label = R[c].log[j].max_label;
+            }
+    if (stats) {
+        stats->label_error_view = bad_view;
+        stats->views = plan.n_views;
+        stats->view_pixels = plan.view_px;
+        for (int c = 0; c < n_ctx; ++c) {
+            for (const auto& l : R[c].log) {
+                stats->emitted += l.n_emitted;
+                stats->instances += l.n_instances;
+                stats->tile_steps += (int64_t)l.tile_steps;
+                stats->exact_evals += (int64_t)l.exact_evals;
+                stats->atomics += (int64_t)l.atomics;
+            }
+            stats->retried_views += R[c].retried;
+            stats->launches += R[c].launches;
+            stats->gpu_ms = std::max(stats->gpu_ms, R[c].gpu_ms);
+            stats->prep_ms += R[c].prep_ms;
+            stats->bin_ms += R[c].bin_ms;
+            stats->raster_ms += R[c].raster_ms;
+        }
+    }
+    if (bad_view >= 0)
+        return fail(FS_ELABEL, "view %lld: label %u exceeds object count %d", bad_view, bad_label,
+                    num_objects);
+    return FS_OK;
+}
+
+// ---- finalize (fs_finalize / fs_reduce_finalize / fs_finalize_multi) ----
+
+// Peer access dev -> peer (NVLink P2P loads from dev's kernels), enabled once.
+bool enable_peer(int dev, int peer) {
+    if (dev == peer) return true;
+    static std::mutex m;
+    static std::set<std::pair<int, int>> on;
+    std::lock_guard<std::mutex> g(m);
+    if (on.count({dev, peer})) return true;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return false;
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    cudaSetDevice(cur);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+    cudaGetLastError();
+    if (e != cudaSuccess) return false;
+    on.insert({dev, peer});
+    return true;
+}
+
+// Parts of slice [g0, g1) for ctx's finalize: the other contexts' accumulators
+// read in place over peer memory, or -- without P2P access -- their slice
+// copied into local staging first.
+int gather_parts(fs_context* ctx, fs_context* const* ctxs, int n_ctx, void* const* accs,
+                 int acc_kind, int num_objects, long long g0, long long g1, fs::AccParts& P) {
+    const size_t entry = acc_kind == FS_ACC_FIXED ? 16 : 8;
+    const size_t row = (size_t)num_objects * entry;
+    const size_t slice = (size_t)(g1 - g0) * row;
+    std::vector<int> staged;
+    for (int i = 0; i < n_ctx; ++i) {
+        if (!accs[i]) return fail(FS_EINVAL, "fs_finalize_multi: NULL accumulator %d", i);
+        if (ctxs[i]->device == ctx->device || enable_peer(ctx->device, ctxs[i]->device))
+            P.p[i] = accs[i];
+        else
+            staged.push_back(i);
+    }
+    if (!staged.empty()) {
+        int rc = grow(&ctx->fin_stage, &ctx->fin_stage_cap, staged.size() * slice);
+        if (rc) return rc;
+        for (size_t k = 0; k < staged.size(); ++k) {
+            const int i = staged[k];
+            unsigned char* dst = ctx->fin_stage + k * slice;
+            CK(cudaMemcpyPeerAsync(dst, ctx->device,
+                                   static_cast<const unsigned char*>(accs[i]) + (size_t)g0 * row,
+                                   ctxs[i]->device, slice, ctx->work[0].stream));
+            P.p[i] = dst - (size_t)g0 * row;  // indexed by absolute Gaussian id
+        }
+    }
+    return FS_OK;
+}
+
+// Reduce + cast (+ biased argmax when mode >= 0) of Gaussians [g0, g1) on
+// ctx's device.  out: element (0, g0) of an E-row float32 matrix with row
+// stride ld (device or host); labels (host, same stride; mode >= 0 only).
+int finalize_slice(fs_context* ctx, const fs::AccParts& P, int acc_kind, int num_objects,
+                   long long g0, long long g1, float* out, long long ld, int out_on_device,
+                   uint8_t* labels, float gamma, int mode) {
+    cudaStream_t st = ctx->work[0].stream;
+    const long long w = g1 - g0;
+    if (mode >= 0 && (out_on_device || !labels))
+        return fail(FS_EINVAL, "finalize_slice: labels need a host matrix and label buffer");
+    float* dst = out;
+    long long dld = ld;
+    int rc;
+    if (!out_on_device) {
+        if ((rc = grow(&ctx->fin_tmp, &ctx->fin_tmp_cap, (size_t)num_objects * w))) return rc;
+        dst = ctx->fin_tmp;
+        dld = w;
+    }
+    fs::launch_finalize(P, acc_kind == FS_ACC_FIXED, g0, g1, num_objects, dst, dld, st);
+    if (!out_on_device)
+        CK(cudaMemcpy2DAsync(out, sizeof(float) * ld, dst, sizeof(float) * w, sizeof(float) * w,
+                             num_objects, cudaMemcpyDeviceToHost, st));
+    if (mode >= 0) {
+        const int rows = mode == FS_MODE_BINARY ? 1 : num_objects;
+        if ((rc = grow(&ctx->fin_lab, &ctx->fin_lab_cap, (size_t)rows * w))) return rc;
+        fs::launch_assign(dst, w, dld, num_objects, gamma, mode, ctx->fin_lab, st);
+        CK(cudaMemcpy2DAsync(labels, ld, ctx->fin_lab, dld, w, rows, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return FS_OK;
 }
 
 }  // namespace
@@ -495,7 +816,9 @@ int fs_create(int device, int n_streams, fs_context** out) {
         CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&w.h2d_done, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&w.view_done, cudaEventDisableTiming));
     }
+    CK(cudaEventCreateWithFlags(&ctx->ev_caller, cudaEventDisableTiming));
     CK(cudaEventCreate(&ctx->ev_start));
     CK(cudaEventCreate(&ctx->ev_stop));
     *out = ctx;
@@ -505,12 +828,12 @@ int fs_create(int device, int n_streams, fs_context** out) {
 void fs_destroy(fs_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    cudaDeviceSynchronize();
+    for (auto& w : ctx->work)
+        if (w.stream) cudaStreamSynchronize(w.stream);
     for (auto& w : ctx->work) free_work(w);
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
                     (void*)ctx->opac, (void*)ctx->view_log,
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
-                    (void*)ctx->tmp_f32, (void*)ctx->asg_in, (void*)ctx->asg_out,
                     (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
                     (void*)ctx->rn_u32, (void*)ctx->rn_labels, (void*)ctx->rn_rect,
                     (void*)ctx->cnt})
@@ -522,6 +845,9 @@ void fs_destroy(fs_context* ctx) {
     for (cudaEvent_t e : ctx->stage_events) cudaEventDestroy(e);
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
     if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
+    if (ctx->ev_caller) cudaEventDestroy(ctx->ev_caller);
+    for (void* p : {(void*)ctx->fin_tmp, (void*)ctx->fin_lab, (void*)ctx->fin_stage})
+        if (p) cudaFree(p);
     delete ctx;
 }
 
@@ -545,19 +871,21 @@ int fs_device_free(fs_context* ctx, void* ptr) {
 
 int fs_memset_zero(fs_context* ctx, void* p, uint64_t bytes) {
     CK(cudaSetDevice(ctx->device));
-    CK(cudaMemset(p, 0, bytes));
+    cudaStream_t st = ctx->work[0].stream;
+    CK(cudaMemsetAsync(p, 0, bytes, st));
+    CK(cudaStreamSynchronize(st));
     return FS_OK;
 }
 
 int fs_copy_to_device(fs_context* ctx, void* dst, const void* src, uint64_t bytes) {
     CK(cudaSetDevice(ctx->device));
-    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    CK(sync_copy(dst, src, bytes, cudaMemcpyHostToDevice, ctx->work[0].stream));
     return FS_OK;
 }
 
 int fs_copy_to_host(fs_context* ctx, void* dst, const void* src, uint64_t bytes) {
     CK(cudaSetDevice(ctx->device));
-    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    CK(sync_copy(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->work[0].stream));
     return FS_OK;
 }
 
@@ -582,7 +910,13 @@ int fs_host_pinned(const void* ptr, uint64_t bytes) { return host_pinned(ptr, by
 
 int fs_synchronize(fs_context* ctx) {
     CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());
+    for (auto& w : ctx->work) CK(cudaStreamSynchronize(w.stream));
+    return FS_OK;
+}
+
+int fs_set_stream(fs_context* ctx, void* stream) {
+    if (!ctx) return fail(FS_EINVAL, "fs_set_stream: NULL context");
+    ctx->caller_stream = static_cast<cudaStream_t>(stream);
     return FS_OK;
 }
 
@@ -599,8 +933,8 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
     if (n > 0 && (!means || !quats || !scales || !opacities))
         return fail(FS_EINVAL, "fs_set_scene: NULL array");
     CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());
     int rc;
+    if ((rc = order_after_caller(ctx))) return rc;
     if (n > ctx->scene_cap) {
         if ((rc = dev_alloc(&ctx->mx, n)) || (rc = dev_alloc(&ctx->my, n)) ||
             (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
@@ -645,14 +979,14 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
                        ctx->num_sms, w.stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(w.stream));
-    CK(cudaMemcpy(alive, ex.alive, (size_t)n, cudaMemcpyDeviceToHost));
-    if (mean2d) CK(cudaMemcpy(mean2d, ex.mean2d, 16 * (size_t)n, cudaMemcpyDeviceToHost));
-    if (conic) CK(cudaMemcpy(conic, ex.conic, 24 * (size_t)n, cudaMemcpyDeviceToHost));
-    if (depth) CK(cudaMemcpy(depth, ex.depth, 8 * (size_t)n, cudaMemcpyDeviceToHost));
-    if (radius) CK(cudaMemcpy(radius, ex.radius, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    CK(sync_copy(alive, ex.alive, (size_t)n, cudaMemcpyDeviceToHost, w.stream));
+    if (mean2d) CK(sync_copy(mean2d, ex.mean2d, 16 * (size_t)n, cudaMemcpyDeviceToHost, w.stream));
+    if (conic) CK(sync_copy(conic, ex.conic, 24 * (size_t)n, cudaMemcpyDeviceToHost, w.stream));
+    if (depth) CK(sync_copy(depth, ex.depth, 8 * (size_t)n, cudaMemcpyDeviceToHost, w.stream));
+    if (radius) CK(sync_copy(radius, ex.radius, 8 * (size_t)n, cudaMemcpyDeviceToHost, w.stream));
     if (stats) {
         fs::ViewCounters vc;
-        CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
+        CK(sync_copy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost, w.stream));
         stats->n_input = n;
         stats->n_emitted = vc.n_emitted;
         stats->n_behind = vc.n_behind;
@@ -671,14 +1005,14 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
 static int copy_tile_lists(fs::Work& w, int ntiles, unsigned int n_valid, int64_t* tile_offsets,
                            int64_t* items, int64_t items_capacity, int64_t* n_items) {
     std::vector<unsigned int> starts(ntiles + 1);
-    CK(cudaMemcpy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost));
+    CK(sync_copy(starts.data(), w.tile_start, sizeof(unsigned int) * (ntiles + 1), cudaMemcpyDeviceToHost, w.stream));
     for (int t = 0; t <= ntiles; ++t) tile_offsets[t] = starts[t];
     *n_items = n_valid;
     if (items) {
         if (items_capacity < (int64_t)n_valid) return fail(FS_EINVAL, "fs_bin: items buffer too small");
         // bucket t's gids sit in the first half of its instance bytes (sorted_view)
         std::vector<unsigned long long> g(n_valid);
-        if (n_valid) CK(cudaMemcpy(g.data(), w.inst, sizeof(unsigned long long) * n_valid, cudaMemcpyDeviceToHost));
+        if (n_valid) CK(sync_copy(g.data(), w.inst, sizeof(unsigned long long) * n_valid, cudaMemcpyDeviceToHost, w.stream));
         for (int t = 0; t < ntiles; ++t) {
             const unsigned int* v = fs::sorted_view(g.data(), starts[t]);
             for (unsigned int i = starts[t]; i < starts[t + 1]; ++i) items[i] = v[i - starts[t]];
@@ -704,7 +1038,7 @@ int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t
         fs::launch_tile_sort(ntiles, tile_sort_args(w), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
-        CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
+        CK(sync_copy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost, w.stream));
         if (!vc.overflow) break;
         cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull, (unsigned long long)vc.n_instances + 1024);
     }
@@ -740,9 +1074,9 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
         (rc = dev_alloc(&d_rad, k1)))
         return rc;
     if (k > 0) {
-        CK(cudaMemcpy(d_mean, mean2d, 16 * (size_t)k, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_depth, depth, 8 * (size_t)k, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(d_rad, radius, 8 * (size_t)k, cudaMemcpyHostToDevice));
+        CK(sync_copy(d_mean, mean2d, 16 * (size_t)k, cudaMemcpyHostToDevice, w.stream));
+        CK(sync_copy(d_depth, depth, 8 * (size_t)k, cudaMemcpyHostToDevice, w.stream));
+        CK(sync_copy(d_rad, radius, 8 * (size_t)k, cudaMemcpyHostToDevice, w.stream));
     }
     fs::ViewCounters vc{};
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -757,7 +1091,7 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
         fs::launch_tile_sort(ntiles, tile_sort_args(w, w.tie), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
-        CK(cudaMemcpy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost));
+        CK(sync_copy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost, w.stream));
         if (!vc.overflow) break;
         cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull, (unsigned long long)vc.n_instances + 1024);
     }
@@ -770,177 +1104,160 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
 
 int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uint16_t* const* masks,
                   int masks_on_device, int num_objects, double alpha_floor, double t_floor,
-                  double* acc, fs_accumulate_stats* stats) {
+                  int acc_kind, void* acc, fs_accumulate_stats* stats) {
     if (!ctx) return fail(FS_EINVAL, "fs_accumulate: NULL context");
-    if (n_views < 0 || (n_views > 0 && (!cams || !masks)))
-        return fail(FS_EINVAL, "fs_accumulate: bad view arguments");
-    if (num_objects < 1 || num_objects > 65536)
-        return fail(FS_EINVAL, "fs_accumulate: num_objects must be in [1, 65536], got %d", num_objects);
-    if (!acc && ctx->n > 0) return fail(FS_EINVAL, "fs_accumulate: NULL accumulator");
     if (stats) {
         memset(stats, 0, sizeof(*stats));
         stats->label_error_view = -1;
     }
-    if (n_views == 0 || ctx->n == 0) return FS_OK;
     int rc;
-    int max_tiles = 1;
-    size_t max_px = 1;
-    long long view_px = 0;
-    for (int v = 0; v < n_views; ++v) {
-        if ((rc = check_cam(cams[v], v))) return rc;
-        if (!masks[v]) return fail(FS_EINVAL, "view %d: NULL mask", v);
-        max_tiles = std::max(max_tiles, fs::tiles_x_of(cams[v].width) * fs::tiles_y_of(cams[v].height));
-        max_px = std::max(max_px, (size_t)cams[v].width * cams[v].height);
-        view_px += (long long)cams[v].width * cams[v].height;
-    }
-    CK(cudaSetDevice(ctx->device));
-    // order after everything the caller enqueued on other streams (e.g. zeroing acc)
-    CK(cudaDeviceSynchronize());
-    for (auto& w : ctx->work) {
-        unsigned int cap = std::max(w.inst_cap, initial_inst_cap(ctx->n));
-        if ((rc = ensure_work(ctx, w, ctx->n, max_tiles, cap, masks_on_device ? 1 : max_px))) return rc;
-    }
-    if (n_views > ctx->view_log_cap) {
-        if ((rc = dev_alloc(&ctx->view_log, (size_t)n_views))) return rc;
-        ctx->view_log_cap = n_views;
-    }
-    const int S = (int)ctx->work.size();
-    fs::Work& w0 = ctx->work[0];
-    if (ctx->timing) {
-        while ((int)ctx->stage_events.size() < 4 * n_views) {
-            cudaEvent_t e;
-            CK(cudaEventCreate(&e));
-            ctx->stage_events.push_back(e);
-        }
-    }
-    long long launches = 0;  // our kernels (the log memset is a driver memset)
-    CK(cudaMemsetAsync(ctx->view_log, 0, sizeof(fs::ViewCounters) * (size_t)n_views, w0.stream));
-    CK(cudaEventRecord(ctx->ev_start, w0.stream));
-    for (int s = 1; s < S; ++s) CK(cudaStreamWaitEvent(ctx->work[s].stream, ctx->ev_start, 0));
-    for (int v = 0; v < n_views; ++v) {
-        fs::Work& w = ctx->work[v % S];
-        const uint16_t* mask = masks[v];
-        if (!masks_on_device) {
-            const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
-            if (host_pinned(masks[v], bytes)) {
-                // page-locked input: DMA straight into the stream's mask buffer
-                // (stream order keeps it behind the previous view's raster)
-                CK(cudaMemcpyAsync(w.mask_dev, masks[v], bytes, cudaMemcpyHostToDevice, w.stream));
-            } else {
-                if (w.h2d_pending) CK(cudaEventSynchronize(w.h2d_done));
-                parallel_memcpy(w.pinned, masks[v], bytes);
-                CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
-                CK(cudaEventRecord(w.h2d_done, w.stream));
-                w.h2d_pending = true;
-            }
-            mask = w.mask_dev;
-        }
-        enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
-                     ctx->view_log + v, ctx->timing ? &ctx->stage_events[4 * v] : nullptr);
-        launches += view_launches();
-    }
-    CK(cudaGetLastError());
-    for (int s = 1; s < S; ++s) {
-        CK(cudaEventRecord(ctx->work[s].done, ctx->work[s].stream));
-        CK(cudaStreamWaitEvent(w0.stream, ctx->work[s].done, 0));
-    }
-    CK(cudaEventRecord(ctx->ev_stop, w0.stream));
-    CK(cudaEventSynchronize(ctx->ev_stop));
-    for (auto& w : ctx->work) w.h2d_pending = false;
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_stop));
-
-    double prep_ms = 0, bin_ms = 0, raster_ms = 0;
-    if (ctx->timing) {
-        for (int v = 0; v < n_views; ++v) {
-            float a = 0, b = 0, c = 0;
-            cudaEvent_t* e = &ctx->stage_events[4 * v];
-            CK(cudaEventElapsedTime(&a, e[0], e[1]));
-            CK(cudaEventElapsedTime(&b, e[1], e[2]));
-            CK(cudaEventElapsedTime(&c, e[2], e[3]));
-            prep_ms += a;
-            bin_ms += b;
-            raster_ms += c;
-        }
-    }
-    std::vector<fs::ViewCounters> log(n_views);
-    CK(cudaMemcpy(log.data(), ctx->view_log, sizeof(fs::ViewCounters) * n_views, cudaMemcpyDeviceToHost));
-    // re-run views that overflowed the instance buffers (they contributed nothing)
-    long long retried = 0;
-    for (int v = 0; v < n_views; ++v) {
-        if (!log[v].overflow) continue;
-        fs::Work& w = w0;
-        unsigned int need = (unsigned int)std::min<unsigned long long>(
-            0x7fffffffull, (unsigned long long)log[v].n_instances + log[v].n_instances / 4 + 1024);
-        if ((rc = ensure_work(ctx, w, ctx->n, max_tiles, need, masks_on_device ? 1 : max_px))) return rc;
-        for (auto& o : ctx->work)  // later calls start with the grown capacity
-            if (o.inst_cap < need && (rc = ensure_work(ctx, o, ctx->n, max_tiles, need, 1))) return rc;
-        const uint16_t* mask = masks[v];
-        if (!masks_on_device) {
-            const size_t bytes = (size_t)cams[v].width * cams[v].height * sizeof(uint16_t);
-            parallel_memcpy(w.pinned, masks[v], bytes);
-            CK(cudaMemcpyAsync(w.mask_dev, w.pinned, bytes, cudaMemcpyHostToDevice, w.stream));
-            mask = w.mask_dev;
-        }
-        CK(cudaMemsetAsync(ctx->view_log + v, 0, sizeof(fs::ViewCounters), w.stream));
-        enqueue_view(ctx, w, to_cam(cams[v]), mask, num_objects, alpha_floor, t_floor, acc,
-                     ctx->view_log + v);
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(w.stream));
-        CK(cudaMemcpy(&log[v], ctx->view_log + v, sizeof(fs::ViewCounters), cudaMemcpyDeviceToHost));
-        if (log[v].overflow) return fail(FS_ENOMEM, "view %d: instance buffer overflow after retry", v);
-        ++retried;
-    }
-    long long bad_view = -1;
-    for (int v = 0; v < n_views; ++v)
-        if (log[v].max_label >= (unsigned)num_objects) {
-            bad_view = v;
-            break;
-        }
-    if (stats) {
-        stats->label_error_view = bad_view;
-        stats->views = n_views;
-        stats->view_pixels = view_px;
-        for (const auto& l : log) {
-            stats->emitted += l.n_emitted;
-            stats->instances += l.n_instances;
-            stats->tile_steps += (int64_t)l.tile_steps;
-            stats->exact_evals += (int64_t)l.exact_evals;
-            stats->atomics += (int64_t)l.atomics;
-        }
-        stats->retried_views = retried;
-        stats->launches = launches;
-        stats->gpu_ms = ms;
-        stats->prep_ms = prep_ms;
-        stats->bin_ms = bin_ms;
-        stats->raster_ms = raster_ms;
-    }
-    if (bad_view >= 0)
-        return fail(FS_ELABEL, "view %lld: label %u exceeds object count %d", bad_view,
-                    log[bad_view].max_label, num_objects);
-    return FS_OK;
+    ViewPlan plan;
+    if ((rc = plan_views(n_views, cams, masks, num_objects, acc_kind, plan))) return rc;
+    if (!acc && ctx->n > 0) return fail(FS_EINVAL, "fs_accumulate: NULL accumulator");
+    if (n_views == 0 || ctx->n == 0) return FS_OK;
+    CtxRun R;
+    if ((rc = accumulate_on(ctx, plan, cams, masks, masks_on_device, num_objects, alpha_floor,
+                            t_floor, acc_kind, acc, nullptr, R)))
+        return rc;
+    return finish_stats(&R, 1, plan, num_objects, stats);
 }
 
-int fs_finalize(fs_context* ctx, const double* acc, int64_t n, int num_objects, float* out,
-                int out_on_device) {
-    if (!ctx) return fail(FS_EINVAL, "fs_finalize: NULL context");
-    if (n < 0 || num_objects < 0) return fail(FS_EINVAL, "fs_finalize: bad shape");
-    const size_t count = (size_t)n * (size_t)num_objects;
-    if ((!acc || !out) && count) return fail(FS_EINVAL, "fs_finalize: NULL argument");
-    if (count == 0) return FS_OK;
-    CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());  // acc may come from another stream (e.g. an NCCL all-reduce)
-    cudaStream_t st = ctx->work[0].stream;
-    float* dst = out;
-    if (!out_on_device) {
-        int rc = grow(&ctx->tmp_f32, &ctx->tmp_f32_cap, count);
-        if (rc) return rc;
-        dst = ctx->tmp_f32;
+int fs_accumulate_multi(fs_context* const* ctxs, int n_ctx, int n_views, const fs_camera* cams,
+                        const uint16_t* const* masks, int num_objects, double alpha_floor,
+                        double t_floor, int acc_kind, void* const* accs, int32_t* view_ctx,
+                        fs_accumulate_stats* stats) {
+    if (!ctxs || n_ctx < 1 || n_ctx > fs::kMaxParts || !accs)
+        return fail(FS_EINVAL, "fs_accumulate_multi: need 1..%d contexts and accumulators",
+                    fs::kMaxParts);
+    if (stats) {
+        memset(stats, 0, sizeof(*stats));
+        stats->label_error_view = -1;
     }
-    fs::launch_finalize(acc, dst, n, num_objects, st);
-    CK(cudaGetLastError());
-    if (!out_on_device) CK(cudaMemcpyAsync(out, dst, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    int rc;
+    ViewPlan plan;
+    if ((rc = plan_views(n_views, cams, masks, num_objects, acc_kind, plan))) return rc;
+    const long long n = ctxs[0]->n;
+    for (int i = 0; i < n_ctx; ++i) {
+        if (!ctxs[i]) return fail(FS_EINVAL, "fs_accumulate_multi: NULL context %d", i);
+        if (ctxs[i]->n != n)
+            return fail(FS_EINVAL, "fs_accumulate_multi: context %d holds %lld Gaussians, context 0 "
+                                   "%lld (upload the same scene to every context)", i,
+                        (long long)ctxs[i]->n, n);
+        if (!accs[i] && n > 0) return fail(FS_EINVAL, "fs_accumulate_multi: NULL accumulator %d", i);
+    }
+    if (n_views == 0 || n == 0) return FS_OK;
+    // dynamic queue: every host thread pops the next view when one of its
+    // context's streams frees up, so faster GPUs take more views
+    std::atomic<int> next(0);
+    std::vector<CtxRun> R(n_ctx);
+    std::vector<int> codes(n_ctx, FS_OK);
+    std::vector<std::string> errs(n_ctx);
+    std::vector<std::thread> threads;
+    for (int i = 0; i < n_ctx; ++i)
+        threads.emplace_back([&, i] {
+            codes[i] = accumulate_on(ctxs[i], plan, cams, masks, 0, num_objects, alpha_floor,
+                                     t_floor, acc_kind, accs[i], &next, R[i]);
+            if (codes[i]) errs[i] = fs::g_error;
+        });
+    for (auto& t : threads) t.join();
+    for (int i = 0; i < n_ctx; ++i)
+        if (codes[i]) return fail(codes[i], "%s", errs[i].c_str());
+    if (view_ctx)
+        for (int i = 0; i < n_ctx; ++i)
+            for (int v : R[i].views) view_ctx[v] = i;
+    return finish_stats(R.data(), n_ctx, plan, num_objects, stats);
+}
+
+int fs_enable_peer_access(fs_context* ctx, int peer_device) {
+    if (!ctx) return fail(FS_EINVAL, "fs_enable_peer_access: NULL context");
+    return enable_peer(ctx->device, peer_device) ? FS_OK
+                                                 : fail(FS_ECUDA, "no peer access from device %d to %d",
+                                                        ctx->device, peer_device);
+}
+
+int fs_reduce_finalize(fs_context* ctx, int acc_kind, const void* const* parts, int n_parts,
+                       int64_t part_g0, int64_t n, int num_objects, int64_t g0, int64_t g1,
+                       float* out, int64_t ld, int out_on_device) {
+    if (!ctx) return fail(FS_EINVAL, "fs_reduce_finalize: NULL context");
+    if (acc_kind != FS_ACC_F64 && acc_kind != FS_ACC_FIXED)
+        return fail(FS_EINVAL, "bad accumulator kind %d", acc_kind);
+    if (n < 0 || num_objects < 0 || g0 < 0 || g1 > n || g0 > g1 || part_g0 > g0)
+        return fail(FS_EINVAL, "fs_reduce_finalize: bad range");
+    if (n_parts < 1 || n_parts > fs::kMaxParts || !parts)
+        return fail(FS_EINVAL, "fs_reduce_finalize: need 1..%d parts", fs::kMaxParts);
+    if (g1 == g0 || num_objects == 0) return FS_OK;
+    if (!out) return fail(FS_EINVAL, "fs_reduce_finalize: NULL output");
+    if (ld < g1 - g0) return fail(FS_EINVAL, "fs_reduce_finalize: row stride %lld < slice width %lld",
+                                  (long long)ld, (long long)(g1 - g0));
+    CK(cudaSetDevice(ctx->device));
+    int rc;
+    if ((rc = order_after_caller(ctx))) return rc;
+    fs::AccParts P{};
+    P.n = n_parts;
+    const size_t entry = acc_kind == FS_ACC_FIXED ? 16 : 8;
+    for (int i = 0; i < n_parts; ++i) {
+        if (!parts[i]) return fail(FS_EINVAL, "fs_reduce_finalize: NULL part %d", i);
+        // element (g, l) of a part lives at (g - part_g0) * E + l
+        P.p[i] = static_cast<const unsigned char*>(parts[i]) -
+                 (size_t)part_g0 * num_objects * entry;
+    }
+    return finalize_slice(ctx, P, acc_kind, num_objects, g0, g1, out, ld, out_on_device, nullptr,
+                          0.0f, -1);
+}
+
+int fs_finalize(fs_context* ctx, int acc_kind, const void* acc, int64_t n, int num_objects,
+                float* out, int out_on_device) {
+    return fs_reduce_finalize(ctx, acc_kind, &acc, 1, 0, n, num_objects, 0, n, out, n,
+                              out_on_device);
+}
+
+int fs_finalize_multi(fs_context* const* ctxs, int n_ctx, int acc_kind, void* const* accs,
+                      int64_t n, int num_objects, float* out, float gamma, int mode,
+                      uint8_t* labels) {
+    if (!ctxs || n_ctx < 1 || n_ctx > fs::kMaxParts || !accs)
+        return fail(FS_EINVAL, "fs_finalize_multi: need 1..%d contexts and accumulators",
+                    fs::kMaxParts);
+    if (acc_kind != FS_ACC_F64 && acc_kind != FS_ACC_FIXED)
+        return fail(FS_EINVAL, "bad accumulator kind %d", acc_kind);
+    if (mode != -1 && mode != FS_MODE_BINARY && mode != FS_MODE_SCENE)
+        return fail(FS_EINVAL, "fs_finalize_multi: bad mode %d", mode);
+    if (mode == FS_MODE_BINARY && num_objects != 2)
+        return fail(FS_EINVAL, "binary assignment requires E=2, got E=%d", num_objects);
+    if (mode == FS_MODE_SCENE && num_objects < 2)
+        return fail(FS_EINVAL, "scene assignment requires E>=2, got E=%d", num_objects);
+    if (mode != -1 && !(gamma >= -1.0f && gamma <= 1.0f))
+        return fail(FS_EINVAL, "gamma must lie in [-1, 1], got %g", (double)gamma);
+    if (n <= 0 || num_objects <= 0) return FS_OK;
+    if (!out || (mode != -1 && !labels)) return fail(FS_EINVAL, "fs_finalize_multi: NULL output");
+    // Column slice i of A is reduced, cast and argmax'ed on context i, reading
+    // the other contexts' accumulators over NVLink peer memory: a reduce-scatter
+    // fused into the finalize, then one D2H per slice straight into the host
+    // matrix (no gather: the host is the destination).
+    std::vector<int> codes(n_ctx, FS_OK);
+    std::vector<std::string> errs(n_ctx);
+    std::vector<std::thread> threads;
+    for (int i = 0; i < n_ctx; ++i)
+        threads.emplace_back([&, i] {
+            fs_context* ctx = ctxs[i];
+            const long long base = n / n_ctx, extra = n % n_ctx;
+            const long long g0 = i * base + std::min<long long>(i, extra);
+            const long long g1 = g0 + base + (i < extra ? 1 : 0);
+            int rc = cudaSetDevice(ctx->device) == cudaSuccess ? FS_OK : FS_ECUDA;
+            if (!rc) rc = order_after_caller(ctx);
+            if (!rc && g1 > g0) {
+                fs::AccParts P{};
+                P.n = n_ctx;
+                rc = gather_parts(ctx, ctxs, n_ctx, accs, acc_kind, num_objects, g0, g1, P);
+                if (!rc)
+                    rc = finalize_slice(ctx, P, acc_kind, num_objects, g0, g1, out + g0, n, 0,
+                                        labels ? labels + g0 : nullptr, gamma, mode);
+            }
+            codes[i] = rc;
+            if (rc) errs[i] = fs::g_error.empty() ? "CUDA error in fs_finalize_multi" : fs::g_error;
+        });
+    for (auto& t : threads) t.join();
+    for (int i = 0; i < n_ctx; ++i)
+        if (codes[i]) return fail(codes[i], "%s", errs[i].c_str());
     return FS_OK;
 }
 
@@ -955,6 +1272,9 @@ int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float
     if (!(gamma >= -1.0f && gamma <= 1.0f)) return fail(FS_EINVAL, "gamma must lie in [-1, 1], got %g", (double)gamma);
     if (n <= 0) return FS_OK;
     if (ctx) CK(cudaSetDevice(ctx->device));
+    // Reentrant: the calling thread's default stream and stream-ordered
+    // scratch (cudaMallocAsync pools), no context state -- the service's
+    // thread pool calls this concurrently, also while an accumulation runs.
     cudaStream_t st = cudaStreamPerThread;
     const size_t in_bytes = sizeof(float) * (size_t)num_objects * n;
     const size_t out_bytes = (mode == FS_MODE_BINARY ? 1 : (size_t)num_objects) * n;
@@ -962,28 +1282,18 @@ int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float
     uint8_t* dout = out;
     void *tmpA = nullptr, *tmpO = nullptr;
     if (!on_device) {
-        if (ctx) {  // context-owned scratch (the context is single-threaded by contract)
-            int rc;
-            if ((rc = grow(&ctx->asg_in, &ctx->asg_in_cap, in_bytes / sizeof(float))) ||
-                (rc = grow(&ctx->asg_out, &ctx->asg_out_cap, out_bytes)))
-                return rc;
-            dA = ctx->asg_in;
-            dout = ctx->asg_out;
-            CK(cudaMemcpyAsync(ctx->asg_in, A, in_bytes, cudaMemcpyHostToDevice, st));
-        } else {
-            CK(cudaMallocAsync(&tmpA, in_bytes, st));
-            CK(cudaMallocAsync(&tmpO, out_bytes, st));
-            CK(cudaMemcpyAsync(tmpA, A, in_bytes, cudaMemcpyHostToDevice, st));
-            dA = static_cast<const float*>(tmpA);
-            dout = static_cast<uint8_t*>(tmpO);
-        }
+        CK(cudaMallocAsync(&tmpA, in_bytes, st));
+        CK(cudaMallocAsync(&tmpO, out_bytes, st));
+        CK(cudaMemcpyAsync(tmpA, A, in_bytes, cudaMemcpyHostToDevice, st));
+        dA = static_cast<const float*>(tmpA);
+        dout = static_cast<uint8_t*>(tmpO);
     }
-    fs::launch_assign(dA, n, num_objects, gamma, mode, dout, st);
+    fs::launch_assign(dA, n, n, num_objects, gamma, mode, dout, st);
     CK(cudaGetLastError());
     if (!on_device) {
         CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
-        if (tmpA) CK(cudaFreeAsync(tmpA, st));
-        if (tmpO) CK(cudaFreeAsync(tmpO, st));
+        CK(cudaFreeAsync(tmpA, st));
+        CK(cudaFreeAsync(tmpO, st));
     }
     CK(cudaStreamSynchronize(st));
     return FS_OK;
@@ -1109,7 +1419,7 @@ int fs_render(fs_context* ctx, const fs_camera* cam, const uint8_t* member, doub
     int rc = check_render_cam(cam);
     if (rc) return rc;
     CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());
+    if ((rc = order_after_caller(ctx))) return rc;
     fs::Work& w = ctx->work[0];
     const size_t px = (size_t)cam->width * cam->height, n = (size_t)std::max<long long>(ctx->n, 0);
     if ((rc = grow(&ctx->rn_f64, &ctx->rn_f64_cap, px * (2 + (size_t)channels)))) return rc;
@@ -1128,11 +1438,11 @@ int fs_render(fs_context* ctx, const fs_camera* cam, const uint8_t* member, doub
     if ((rc = render_scene_device(ctx, cam, member_dev, alpha_floor, transmittance_floor, ch_dev,
                                   channels, ctx->rn_f64)))
         return rc;
-    CK(cudaMemcpy(alpha, ctx->rn_f64, sizeof(double) * px, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(depth, ctx->rn_f64 + px, sizeof(double) * px, cudaMemcpyDeviceToHost));
+    CK(sync_copy(alpha, ctx->rn_f64, sizeof(double) * px, cudaMemcpyDeviceToHost, w.stream));
+    CK(sync_copy(depth, ctx->rn_f64 + px, sizeof(double) * px, cudaMemcpyDeviceToHost, w.stream));
     if (channels)
-        CK(cudaMemcpy(value, ctx->rn_f64 + 2 * px, sizeof(double) * px * channels,
-                      cudaMemcpyDeviceToHost));
+        CK(sync_copy(value, ctx->rn_f64 + 2 * px, sizeof(double) * px * channels,
+                      cudaMemcpyDeviceToHost, w.stream));
     return FS_OK;
 }
 
@@ -1171,7 +1481,7 @@ int fs_render_splats(fs_context* ctx, int width, int height, int64_t k, const do
     }
     for (int t = 0; t < ntiles; ++t) order[t] = (unsigned int)t;
     CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());
+    if ((rc = order_after_caller(ctx))) return rc;
     fs::Work& w = ctx->work[0];
     const size_t px = (size_t)width * height, kk = (size_t)std::max<int64_t>(k, 1);
     if ((rc = ensure_work(ctx, w, (long long)kk, ntiles, std::max(w.inst_cap, 1u), 1))) return rc;
@@ -1208,11 +1518,11 @@ int fs_render_splats(fs_context* ctx, int width, int height, int64_t k, const do
     fs::launch_raster_render(ra, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
-    CK(cudaMemcpy(alpha, ctx->rn_f64, sizeof(double) * px, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(depth_out, ctx->rn_f64 + px, sizeof(double) * px, cudaMemcpyDeviceToHost));
+    CK(sync_copy(alpha, ctx->rn_f64, sizeof(double) * px, cudaMemcpyDeviceToHost, st));
+    CK(sync_copy(depth_out, ctx->rn_f64 + px, sizeof(double) * px, cudaMemcpyDeviceToHost, st));
     if (channels)
-        CK(cudaMemcpy(value, ctx->rn_f64 + 2 * px, sizeof(double) * px * channels,
-                      cudaMemcpyDeviceToHost));
+        CK(sync_copy(value, ctx->rn_f64 + 2 * px, sizeof(double) * px * channels,
+                      cudaMemcpyDeviceToHost, st));
     return FS_OK;
 }
 
@@ -1228,7 +1538,7 @@ int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* members
     int rc = check_render_cam(cam);
     if (rc) return rc;
     CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());
+    if ((rc = order_after_caller(ctx))) return rc;
     fs::Work& w = ctx->work[0];
     cudaStream_t st = w.stream;
     const size_t px = (size_t)cam->width * cam->height, n = (size_t)std::max<long long>(ctx->n, 0);
@@ -1282,7 +1592,7 @@ int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* members
         }
     }
     CK(cudaStreamSynchronize(st));
-    CK(cudaMemcpy(labels, ctx->rn_labels, sizeof(uint16_t) * px, cudaMemcpyDeviceToHost));
+    CK(sync_copy(labels, ctx->rn_labels, sizeof(uint16_t) * px, cudaMemcpyDeviceToHost, st));
     return FS_OK;
 }
 

@@ -120,7 +120,8 @@ struct RasterArgs {
     TileSortArgs sort;             // bucket -> depth-ordered gid list (prologue)
     const Rec32* r32;
     const Rec64* r64;
-    double* acc;                   // N x E float64 accumulator (Gaussian-major)
+    double* acc;                   // N x E float64 accumulator (Gaussian-major), or
+    unsigned long long* acc_fixed; // N x E x 2 uint64 fixed-point accumulator (FS_ACC_FIXED)
     ViewCounters* vc;
     const unsigned int* tile_order;  // ntiles: launch order (tile_start_kernel)
     RenderArgs render;             // launch_raster_render only
@@ -130,9 +131,16 @@ void launch_raster(const RasterArgs& a, cudaStream_t st);
 void launch_raster_render(const RasterArgs& a, cudaStream_t st);
 
 // ---- fs_assign.cu ----
-void launch_finalize(const double* acc, float* out, long long n, int e, cudaStream_t st);
-void launch_assign(const float* A, long long n, int e, float gamma, int mode, uint8_t* out,
-                   cudaStream_t st);
+// Accumulator parts summed by the finalize (local or NVLink peer pointers).
+constexpr int kMaxParts = 16;
+struct AccParts {
+    const void* p[kMaxParts];
+    int n;
+};
+void launch_finalize(const AccParts& parts, bool fixed, long long g0, long long g1, int e,
+                     float* out, long long ld, cudaStream_t st);
+void launch_assign(const float* A, long long n, long long ld, int e, float gamma, int mode,
+                   uint8_t* out, cudaStream_t st);
 void launch_row_counts(const uint8_t* m, long long n, int rows, unsigned long long* counts,
                        cudaStream_t st);
 

@@ -85,6 +85,27 @@ __device__ __forceinline__ void red_add(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// Deterministic accumulator (FS_ACC_FIXED): an entry is two uint64 words
+// (hi, lo) holding sum(q >> 32) and sum(q & 0xffffffff) for q = v * 2^59
+// rounded to an integer (v < 32: one RED carries at most 32 pixels' weights,
+// each < 1).  Integer adds commute, so the sum -- and the float32 matrix made
+// from it -- is independent of the order the REDs land in, of the stream
+// schedule and of how views are split over GPUs.  Resolution 2^-59 per RED.
+__device__ __forceinline__ void red_fixed(unsigned long long* p, double v) {
+    const unsigned long long q = __double2ull_rn(__dmul_rn(v, 0x1p59));
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(q >> 32) : "memory");
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p + 1), "l"(q & 0xffffffffull) : "memory");
+}
+
+template <bool kFixed>
+__device__ __forceinline__ void acc_add(double* acc, unsigned long long* acc_fx, size_t at,
+                                        double v) {
+    if (kFixed)
+        red_fixed(acc_fx + 2 * at, v);
+    else
+        red_add(acc + at, v);
+}
+
 // 32 x 32 bit-matrix transpose across the warp (lane i holds row i, bit j =
 // M[i][j]; on return lane j holds column j) when only rows 0..15 can be nonzero
 // (a mini-batch has at most 16 hits).  The full transpose swaps off-diagonal
@@ -139,7 +160,8 @@ __device__ __forceinline__ double depth_of_key(unsigned long long k) {
 // kRender = false: accumulate alpha*T into the N x E float64 accumulator (contributions.py:119-160).
 // kRender = true:  composite alpha, depth and an optional channel per pixel
 //                  (render_property, rasterizer.py:133-203); no mask, no atomics.
-template <bool kRender>
+// kFixed: the accumulator is FS_ACC_FIXED (two uint64 words per entry), else float64.
+template <bool kRender, bool kFixed>
 __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const ViewCounters* vc = a.vc;
     if (vc->overflow) return;
@@ -204,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     const double af_eff = a.af_eff, tf_eff = a.tf_eff;
     const unsigned int n_obj = (unsigned)a.num_objects;  // accumulator row length (N x E)
     double* __restrict__ acc = a.acc;
+    unsigned long long* __restrict__ acc_fx = a.acc_fixed;
     double* __restrict__ myval = W.val;
 
     double T = 1.0;
@@ -363,7 +386,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                         const bool fire = lane < kMini && k < nm && v > 0.0 && gl < (unsigned)a.num_objects;
                         if (fire) {
-                            red_add(acc + (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + gl, v);
+                            acc_add<kFixed>(acc, acc_fx,
+                                            (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + gl, v);
                             ++atom;
                         }
                     }
@@ -374,7 +398,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         mm &= mm - 1u;
                         const double w = myval[k * kRowStride + lane];
                         if (w > 0.0) {
-                            red_add(acc + (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label, w);
+                            acc_add<kFixed>(acc, acc_fx,
+                                            (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label, w);
                             ++atom;
                         }
                     }
@@ -418,21 +443,27 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
 cudaError_t raster_configure() {
     cudaError_t e = tile_sort_configure(kTileSortCap);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(raster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(raster_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)kRasterSmem);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(raster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(raster_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kRasterSmem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(raster_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kRasterSmem);
 }
 
 void launch_raster(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
-    raster_kernel<false><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
+    if (a.acc_fixed)
+        raster_kernel<false, true><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
+    else
+        raster_kernel<false, false><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
 }
 
 void launch_raster_render(const RasterArgs& a, cudaStream_t st) {
     if (a.ntiles <= 0) return;
-    raster_kernel<true><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
+    raster_kernel<true, false><<<a.ntiles, kThreads, kRasterSmem, st>>>(a);
 }
 
 }  // namespace fs

@@ -91,16 +91,17 @@ def read_masks(masks_dir, views: Sequence, workers: Optional[int] = None) -> lis
 def accumulate_mask_files(scene, view_paths: Sequence, num_objects: int,
                           blend: BlendConfig = DEFAULT_BLEND, *, chunk: int = 16,
                           lookahead: int = 2, workers: Optional[int] = None,
-                          device: Optional[int] = None, stats: Optional[dict] = None):
+                          device: Optional[int] = None, stats: Optional[dict] = None,
+                          deterministic: bool = True):
     """accumulate_contributions over ``[(view, png_path)]`` with decode overlapped.
 
     Equivalent to ``accumulate_contributions(scene, [(v, LabelMask(v.view_id,
     load_mask_png(p))) ...], num_objects, blend)``; the matrix differs only in
     float64 summation order (atomics), i.e. not at all after the float32 cast
-    in practice.
+    in practice (and not at all with the default deterministic accumulator).
     """
     from . import _native
-    from .contributions import (ContributionMatrix, LabelMask, check_shapes,
+    from .contributions import (ContributionMatrix, LabelMask, acc_kind_of, check_shapes,
                                 run_device_accumulate, validate_views)
 
     view_paths = list(view_paths)
@@ -111,6 +112,7 @@ def accumulate_mask_files(scene, view_paths: Sequence, num_objects: int,
     window = chunk * max(1, int(lookahead))  # views decoded ahead of the GPU
 
     ctx = _native.context(device)
+    kind = acc_kind_of(deterministic, blend)
     totals: dict = {}
     with ThreadPoolExecutor(_workers(workers)) as pool:
         # one decode task per view, at most `window` views ahead of the device
@@ -125,7 +127,7 @@ def accumulate_mask_files(scene, view_paths: Sequence, num_objects: int,
         submit_until(window)
         with ctx.lock:
             ctx.set_scene(scene)
-            acc = ctx.buffer("acc64", 8 * num_objects * max(n, 1)).zero()
+            acc = ctx.acc_buffer(num_objects, n, kind).zero()
             for s in starts:
                 e = min(s + chunk, len(view_paths))
                 pairs = [(view_paths[j][0], LabelMask(view_id=view_paths[j][0].view_id,
@@ -136,13 +138,13 @@ def accumulate_mask_files(scene, view_paths: Sequence, num_objects: int,
                 if n == 0:
                     validate_views(pairs, num_objects)
                     continue
-                st = run_device_accumulate(ctx, pairs, num_objects, blend, acc.ptr)
+                st = run_device_accumulate(ctx, pairs, num_objects, blend, acc.ptr, kind)
                 for k, v in st.items():
                     if isinstance(v, (int, float)):
                         totals[k] = totals.get(k, 0) + v
             out = ctx.pinned_empty((num_objects, n), np.float32)
             if out.size:
-                ctx.finalize(acc.ptr, n, num_objects, out=out)
+                ctx.finalize(acc.ptr, n, num_objects, out=out, acc_kind=kind)
     if stats is not None:
         stats.update(totals)
     return ContributionMatrix(values=out)

@@ -14,7 +14,8 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .contributions import ContributionMatrix, check_shapes, run_device_accumulate, validate_views
+from .contributions import (ContributionMatrix, acc_kind_of, check_shapes, run_device_accumulate,
+                            validate_views)
 from .rasterizer import DEFAULT_BLEND, BlendConfig
 from .solver import Assignment, _check_gamma
 
@@ -27,13 +28,16 @@ class LabelSolver:
     the solver's lifetime (the interactive-gamma service case).
     """
 
-    def __init__(self, scene, device: Optional[int] = None, own_buffers: bool = True):
+    def __init__(self, scene, device: Optional[int] = None, own_buffers: bool = True,
+                 deterministic: bool = True):
         from . import _native
 
         self._native = _native
         self.scene = scene
         self.ctx = _native.context(device)
         self.own = own_buffers
+        self.deterministic = deterministic
+        self._torch_A = None  # keeps a torch-owned matrix (sharded solves) alive
         self.num_objects = 0
         self._A = None  # device float32 E x N
         self._out = None
@@ -64,35 +68,27 @@ class LabelSolver:
         else:
             check_shapes(views, e)
         ctx = self.ctx
-        acc_t = None
-        mine = None
-        if process_group is not None:
-            import torch
-            import torch.distributed as dist
-
-            from .distributed import shard_views
-            rank = dist.get_rank(process_group)
-            world = dist.get_world_size(process_group)
-            mine = shard_views(len(views), rank, world)
-            acc_t = torch.zeros(e * max(n, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
-        with ctx.lock:
-            ctx.set_scene(self.scene)
-            if acc_t is None:
-                acc_ptr = ctx.buffer("acc64", 8 * e * max(n, 1)).zero().ptr
-                self.stats = run_device_accumulate(ctx, views, e, blend, acc_ptr) if n else {}
-            else:
-                from .distributed import accumulate_shard_checked
-                acc_ptr = acc_t.data_ptr()
-                self.stats = (accumulate_shard_checked(ctx, views, mine, e, blend, acc_ptr,
-                                                       process_group, ctx.device) if n else {})
-        if acc_t is not None:
-            import torch.distributed as dist
-            dist.all_reduce(acc_t, group=process_group)
-        with ctx.lock:
-            A, out = self._buffers(e, n)
-            self._A_cur, self._out_cur = A, out
-            if n:
-                ctx.finalize(acc_ptr, n, e, out_ptr=A.ptr)
+        kind = acc_kind_of(self.deterministic, blend)
+        if process_group is not None and n:
+            # reduce-scatter + sliced cast + all-gather (distributed.py); the
+            # gathered E x N matrix stays on this rank's device
+            from .distributed import sharded_matrix_device
+            A_t, self.stats = sharded_matrix_device(self.scene, views, e, blend, process_group,
+                                                    ctx.device, kind)
+            with ctx.lock:
+                A, out = self._buffers(e, n)
+                self._torch_A = A_t
+                self._A_cur, self._out_cur = _TorchView(A_t, ctx), out
+        else:
+            with ctx.lock:
+                ctx.set_scene(self.scene)
+                acc_ptr = ctx.acc_buffer(e, n, kind).zero().ptr
+                self.stats = run_device_accumulate(ctx, views, e, blend, acc_ptr, kind) if n else {}
+                A, out = self._buffers(e, n)
+                self._A_cur, self._out_cur = A, out
+                if n:
+                    ctx.finalize(acc_ptr, n, e, out_ptr=A.ptr, acc_kind=kind)
+        A = self._A_cur
         self.num_objects = e
         if not download:
             return None
@@ -129,6 +125,20 @@ class LabelSolver:
             asn._device_counts = self.ctx.member_counts(self._out_cur.ptr, n, e)
             return asn
         raise ValueError(f"unknown assignment mode {mode!r}")
+
+
+class _TorchView:
+    """A torch CUDA tensor seen through the DeviceBuffer interface (ptr, to_host)."""
+
+    def __init__(self, t, ctx):
+        self.t, self.ctx = t, ctx
+        self.ptr = t.data_ptr()
+        self.nbytes = t.numel() * t.element_size()
+
+    def to_host(self, out: np.ndarray) -> np.ndarray:
+        import torch
+        torch.from_numpy(out.reshape(-1)).copy_(self.t.reshape(-1)[:out.size])
+        return out
 
 
 def pin_inputs(scene, views: Sequence, device: Optional[int] = None):
@@ -170,12 +180,37 @@ def pin_inputs(scene, views: Sequence, device: Optional[int] = None):
 
 
 def solve(scene, views: Sequence, num_objects: int, gamma: float = 0.0, mode: str = "binary",
-          blend: BlendConfig = DEFAULT_BLEND, device: Optional[int] = None, process_group=None):
+          blend: BlendConfig = DEFAULT_BLEND, device: Optional[int] = None, process_group=None,
+          devices: Optional[Sequence[int]] = None, deterministic: bool = True,
+          stats: Optional[dict] = None):
     """(ContributionMatrix, Assignment) for one scene: the north-star entry point.
 
-    Host numpy inputs in, host results out; with ``process_group`` the views
-    are sharded over the group's GPUs and every rank returns the full result.
+    Host numpy inputs in, host results out.  ``devices``: split the views over
+    these GPUs from this process (multidevice.py); ``process_group``: shard them
+    over a torch.distributed group (every rank returns the full result).
     """
-    s = LabelSolver(scene, device, own_buffers=False)
+    if devices is not None:
+        from .multidevice import solve_multi
+        gamma = _check_gamma(gamma)
+        views = list(views)
+        e = int(num_objects)
+        if mode not in ("binary", "scene"):
+            raise ValueError(f"unknown assignment mode {mode!r}")
+        if mode == "binary" and e != 2:
+            raise ValueError(f"binary assignment requires E=2, got E={e}")
+        if mode == "scene" and e < 2:
+            raise ValueError(f"scene assignment requires E>=2, got E={e}")
+        check_shapes(views, e)
+        if len(scene) == 0:
+            validate_views(views, e)
+        values, labels = solve_multi(scene, views, e, blend, devices,
+                                     acc_kind_of(deterministic, blend),
+                                     gamma=gamma, mode=mode, stats=stats)
+        if mode == "binary":
+            return ContributionMatrix(values=values), Assignment(mode, gamma, labels=labels)
+        return ContributionMatrix(values=values), Assignment(mode, gamma, membership=labels)
+    s = LabelSolver(scene, device, own_buffers=False, deterministic=deterministic)
     matrix = s.accumulate(views, num_objects, blend, process_group=process_group)
+    if stats is not None:
+        stats.update(s.stats)
     return matrix, s.assign(gamma, mode)

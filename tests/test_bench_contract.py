@@ -3,8 +3,14 @@ lookup and the --impl reference JSON line (C1, oracle on the host)."""
 
 import argparse
 import json
+import os
+import subprocess
+import sys
+from pathlib import Path
 
 import bench
+
+ROOT = Path(__file__).resolve().parents[1]
 
 
 def test_clock_window_keeps_timed_region_samples():
@@ -43,3 +49,20 @@ def test_reference_arm_line(capsys):
     # other ranks print nothing
     bench.run_reference(args, rank=1, world=2)
     assert capsys.readouterr().out == ""
+
+
+def test_gpus_flag_launches_that_many_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (here on
+    gloo, --launch-check: rank layout only) and reports n_gpus = 2."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--launch-check",
+                        "--views", "7"], capture_output=True, text=True, timeout=300, env=env,
+                       cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["requested"] == 2
+    # contiguous balanced view shards: rank 0 views 0..3, rank 1 views 4..6
+    assert rec["ranks"] == [[0, 4, 0], [1, 3, 4]]

@@ -62,7 +62,7 @@ class _FakeCtx:
     def __init__(self, bad_local):
         self.bad_local = bad_local
 
-    def accumulate(self, views, masks, *args):
+    def accumulate(self, views, masks, *args, **kw):
         from paper_2409_08270_b200._native import LabelRangeError
         if self.bad_local is not None:
             raise LabelRangeError("label out of range", self.bad_local)

@@ -1,0 +1,207 @@
+"""GPU tests of the accumulator kinds, schedule independence, the multi-GPU
+reduction paths and stream ordering (no device-wide synchronisation).
+
+Only one GPU is available: the single-process multi-GPU path is exercised
+with ``devices=[0, 0]`` (two independent contexts -- host threads, streams,
+accumulators -- on one device; the peer-memory reduction then reads both
+accumulators in place), and the sharded reduction through
+``fs_reduce_finalize`` on explicit view shards.  Reference semantics:
+A is additive over views (contributions.py:103-116, test_contributions.py:79-95)
+and reruns are byte-identical (test_contributions.py:160-168).
+"""
+
+import threading
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+fs = pytest.importorskip("paper_2409_08270_b200")
+from paper_2409_08270_b200 import DEFAULT_BLEND, LabelMask, accumulate_contributions, solve  # noqa: E402
+from paper_2409_08270_b200 import _native, synth  # noqa: E402
+from paper_2409_08270_b200.multidevice import device_contexts  # noqa: E402
+
+
+def _workload(seed=21, n=30000, views=6, w=200, h=150, e=4, **kw):
+    return synth.make_workload(seed=seed, n_gaussians=n, n_views=views, width=w, height=h,
+                               num_objects=e, **kw)
+
+
+def _oracle_A(wl, views=None):
+    sel = range(len(wl.views)) if views is None else views
+    cams = [oracle.camera_of(wl.views[i]) for i in sel]
+    return oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                             wl.scene.opacities, cams, [wl.masks[i] for i in sel],
+                             wl.num_objects, threads=8)
+
+
+def _raw_acc(ctx, wl, views, kind, streams_ctx=None):
+    """Accumulate `views` into a fresh buffer; return its raw words (uint64 / float64)."""
+    c = streams_ctx or ctx
+    n, e = len(wl.scene), wl.num_objects
+    with c.lock:
+        c.set_scene(wl.scene)
+        buf = c.alloc(_native.acc_entry_bytes(kind) * e * n).zero()
+        c.accumulate([wl.views[i] for i in views], [wl.masks[i] for i in views], e, 1 / 255,
+                     1e-4, buf.ptr, acc_kind=kind)
+        raw = np.empty(_native.acc_entry_bytes(kind) * e * n // 8,
+                       np.uint64 if kind == _native.ACC_FIXED else np.float64)
+        buf.to_host(raw)
+    return buf, raw
+
+
+@pytest.mark.parametrize("iid", [False, True], ids=["objects", "iid"])
+def test_fixed_accumulator_matches_oracle_and_f64(iid):
+    wl = _workload(iid_masks=iid)
+    ref = _oracle_A(wl)
+    A_fx = accumulate_contributions(wl.scene, wl.pairs(), wl.num_objects, deterministic=True).values
+    A_64 = accumulate_contributions(wl.scene, wl.pairs(), wl.num_objects,
+                                    deterministic=False).values
+    np.testing.assert_allclose(A_fx, ref, rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(A_64, ref, rtol=1e-6, atol=1e-9)
+    # both are float32 casts of sums within ~1e-16 of each other: at most a
+    # handful of entries may sit on a float32 rounding boundary
+    assert np.count_nonzero(A_fx != A_64) <= max(1, A_fx.size // 1000)
+    assert np.count_nonzero(A_fx != ref) <= max(1, A_fx.size // 1000)
+
+
+def test_fixed_accumulator_is_schedule_independent():
+    """The raw accumulator words are identical for 1 vs 4 streams and for any
+    view order: integer adds commute."""
+    wl = _workload(seed=22, n=40000, views=8, e=3)
+    ctx4 = _native.context(0)
+    ctx1 = _native.Context(0, streams=1)
+    try:
+        order = list(range(len(wl.views)))
+        _, a = _raw_acc(ctx4, wl, order, _native.ACC_FIXED)
+        _, b = _raw_acc(ctx1, wl, order, _native.ACC_FIXED)
+        _, c = _raw_acc(ctx4, wl, order[::-1], _native.ACC_FIXED)
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+    finally:
+        ctx1.close()
+
+
+def test_fixed_accumulator_is_additive_over_view_shards():
+    """Shard accumulators summed as integers == the joint accumulator, word for
+    word (the property the multi-GPU reductions rely on)."""
+    wl = _workload(seed=23, n=20000, views=7, e=2)
+    ctx = _native.context(0)
+    _, full = _raw_acc(ctx, wl, range(7), _native.ACC_FIXED)
+    _, p0 = _raw_acc(ctx, wl, [0, 3, 5], _native.ACC_FIXED)
+    _, p1 = _raw_acc(ctx, wl, [1, 2, 4, 6], _native.ACC_FIXED)
+    assert np.array_equal(full, p0 + p1)
+
+
+@pytest.mark.parametrize("kind", [_native.ACC_FIXED, _native.ACC_F64], ids=["fixed", "f64"])
+def test_reduce_finalize_over_shards_and_slices(kind):
+    """fs_reduce_finalize: the sum of per-shard accumulators, slice by slice (the
+    reduce-scatter's reduction fused into the cast), equals the single-pass matrix."""
+    wl = _workload(seed=24, n=25001, views=6, e=5)
+    n, e = len(wl.scene), wl.num_objects
+    ctx = _native.context(0)
+    bufs = [_raw_acc(ctx, wl, s, kind)[0] for s in ([0, 1], [2, 3, 4], [5])]
+    full = accumulate_contributions(wl.scene, wl.pairs(), e,
+                                    deterministic=kind == _native.ACC_FIXED).values
+    out = np.zeros((e, n), np.float32)
+    cuts = [0, 7, 9000, 9001, n]
+    for g0, g1 in zip(cuts[:-1], cuts[1:]):
+        ctx.reduce_finalize([b.ptr for b in bufs], 0, n, e, g0, g1, out[:, g0:].ctypes.data, n,
+                            out_on_device=False, acc_kind=kind)
+    if kind == _native.ACC_FIXED:
+        assert np.array_equal(out, full)  # exact integer sums: bit-identical
+    else:
+        np.testing.assert_allclose(out, full, rtol=1e-6, atol=1e-12)
+    # a part holding only rows [g0, g1) (a reduce-scatter output) at part_g0 = g0
+    g0, g1 = 9000, 17000
+    entry = _native.acc_entry_bytes(kind)
+    tmp = ctx.alloc(entry * e * (g1 - g0))
+    raw = np.empty(entry * e * n, np.uint8)
+    bufs[0].to_host(raw)
+    tmp.from_host(raw[entry * e * g0: entry * e * g1])
+    sl = np.zeros((e, g1 - g0), np.float32)
+    ctx.reduce_finalize([tmp.ptr], g0, n, e, g0, g1, sl.ctypes.data, g1 - g0,
+                        out_on_device=False, acc_kind=kind)
+    one = np.zeros((e, n), np.float32)
+    ctx.finalize(bufs[0].ptr, n, e, out=one, acc_kind=kind)
+    assert np.array_equal(sl, one[:, g0:g1])
+
+
+def test_multi_device_path_bit_identical_to_single():
+    """devices=[0, 0]: two contexts share the dynamic view queue, the finalize
+    reduces both accumulators slice by slice; fixed-point => identical matrix."""
+    wl = _workload(seed=25, n=50000, views=12, w=256, h=192, e=6)
+    single = accumulate_contributions(wl.scene, wl.pairs(), wl.num_objects).values
+    st: dict = {}
+    multi = accumulate_contributions(wl.scene, wl.pairs(), wl.num_objects, devices=[0, 0],
+                                     stats=st).values
+    assert np.array_equal(multi, single)
+    assert sum(st["views_per_device"]) == 12 and st["views"] == 12
+    assert sorted(set(st["view_device"])) == [0]
+    ref = _oracle_A(wl)
+    np.testing.assert_allclose(multi, ref, rtol=1e-6, atol=1e-9)
+    # fused argmax per slice: labels identical to the single-device solve
+    for mode, e in (("scene", 6),):
+        M1, a1 = solve(wl.scene, wl.pairs(), e, 0.1, mode)
+        M2, a2 = solve(wl.scene, wl.pairs(), e, 0.1, mode, devices=[0, 0, 0])
+        assert np.array_equal(M1.values, M2.values)
+        assert np.array_equal(a1.membership, a2.membership)
+        assert np.array_equal(a2.membership, oracle.assign_scene(M2.values, 0.1))
+    wl2 = _workload(seed=26, n=20000, views=5, e=2)
+    M1, a1 = solve(wl2.scene, wl2.pairs(), 2, -0.2, "binary")
+    M2, a2 = solve(wl2.scene, wl2.pairs(), 2, -0.2, "binary", devices=[0, 0])
+    assert np.array_equal(M1.values, M2.values) and np.array_equal(a1.labels, a2.labels)
+
+
+def test_multi_device_label_error_is_the_first_bad_view():
+    wl = _workload(seed=27, n=5000, views=9, w=96, h=64, e=2)
+    pairs = wl.pairs()
+    for v, lab in ((7, 9), (3, 4)):
+        m = pairs[v][1].labels.copy()
+        m[5, 6] = lab
+        pairs[v] = (pairs[v][0], LabelMask(pairs[v][0].view_id, m))
+    with pytest.raises(ValueError, match=r"view 3: label 4 at pixel \(5, 6\) exceeds object count 2"):
+        accumulate_contributions(wl.scene, pairs, 2, devices=[0, 0])
+
+
+def test_assign_does_not_wait_for_a_running_accumulation():
+    """The service's thread-pool assign (service.py:53-66) runs while a long
+    accumulation occupies the same GPU: no device-wide syncs, no context lock."""
+    wl = synth.make_workload(seed=28, n_gaussians=1_000_000, n_views=120, width=1008,
+                             height=756, num_objects=2)
+    A = np.random.default_rng(3).random((2, 1_000_000)).astype(np.float32)
+    _native.assign(A, 0.0, _native.MODE_BINARY)  # warm (pools, module load)
+    accumulate_contributions(wl.scene, wl.pairs()[:2], 2)  # warm: scene upload, workspaces
+    t = {}
+
+    def run_acc():
+        t["acc0"] = time.perf_counter()
+        accumulate_contributions(wl.scene, wl.pairs(), 2)
+        t["acc1"] = time.perf_counter()
+
+    th = threading.Thread(target=run_acc)
+    th.start()
+    while "acc0" not in t:
+        time.sleep(0.0005)
+    time.sleep(0.005)
+    ends = []
+    done = []
+
+    def run_assign():
+        lab = _native.assign(A, 0.25, _native.MODE_BINARY)
+        ends.append(time.perf_counter())
+        done.append(lab)
+
+    workers = [threading.Thread(target=run_assign) for _ in range(8)]
+    for w in workers:
+        w.start()
+    for w in workers:
+        w.join()
+    th.join()
+    assert len(done) == 8
+    assert all(np.array_equal(d, oracle.assign_binary(A, 0.25)) for d in done)
+    # every assign finished well before the accumulation did
+    assert max(ends) < t["acc1"], (max(ends) - t["acc0"], t["acc1"] - t["acc0"])

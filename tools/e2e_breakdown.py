@@ -24,7 +24,7 @@ for rep in range(3):
     ctx._scene_key = None
     ctx.set_scene(wl.scene)
     t["scene_upload"] = time.perf_counter() - t0
-    acc = ctx.alloc(8 * E * N).zero()
+    acc = ctx.acc_buffer(E, N).zero()
     t0 = time.perf_counter()
     st = ctx.accumulate([v for v, _ in pairs], [m.labels for _, m in pairs], E, 1 / 255, 1e-4, acc.ptr)
     t["accumulate_host_masks"] = time.perf_counter() - t0
