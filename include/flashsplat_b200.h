@@ -122,6 +122,21 @@ int fs_set_timing(fs_context *ctx, int enable);
 int fs_set_scene(fs_context *ctx, int64_t n, const double *means, const double *quats,
                  const double *scales, const double *opacities);
 
+/* load_scene_ply (ply.py:63-106) + GaussianScene (scene.py:71-110) on the
+ * device: verts is the checkpoint's binary_little_endian
+ * vertex block as stored in the file -- n records of stride_floats float32 --
+ * and offsets[17] the float offsets of x y z nx ny nz f_dc_0..2 opacity
+ * scale_0..2 rot_0..3 (the reference's REQUIRED_PROPERTIES order, ply.py:17-23)
+ * within a record.  One upload, then one kernel applies the activations
+ * (exp scales, logistic opacity, quaternion normalisation) and builds the
+ * resident scene.  bad[4] receives the first vertex with a non-finite required
+ * value, a zero quaternion norm, a non-positive scale and an opacity outside
+ * [0, 1] (-1: none); FS_EINVAL if any (the scene is then not resident).
+ * params (optional, n x 8 float64 host) receives the activated parameters
+ * (scale_0..2, opacity, normalised w x y z) for verification. */
+int fs_set_scene_ply(fs_context *ctx, int64_t n, const void *verts, int stride_floats,
+                     const int32_t *offsets, int64_t *bad, double *params);
+
 /* _project_arrays (scene.py:252-312) over the resident scene; host outputs
  * indexed by Gaussian (any may be NULL except alive). */
 int fs_project(fs_context *ctx, const fs_camera *cam, uint8_t *alive, double *mean2d,

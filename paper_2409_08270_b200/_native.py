@@ -34,7 +34,7 @@ EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
     "fs_copy_to_host", "fs_synchronize", "fs_set_stream", "fs_host_alloc", "fs_host_free",
-    "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_set_scene_ply", "fs_project", "fs_bin", "fs_bin_splats",
     "fs_accumulate", "fs_accumulate_multi", "fs_finalize", "fs_reduce_finalize",
     "fs_enable_peer_access", "fs_finalize_multi", "fs_assign", "fs_member_counts", "fs_render",
     "fs_render_splats", "fs_render_mask", "fs_decode_mask_png",
@@ -112,6 +112,7 @@ def load() -> ctypes.CDLL:
             "fs_host_pinned": ([P, ctypes.c_uint64], I),
             "fs_set_timing": ([P, I], I),
             "fs_set_scene": ([P, I64, P, P, P, P], I),
+            "fs_set_scene_ply": ([P, I64, P, I, P, P, P], I),
             "fs_project": ([P, P, P, P, P, P, P, P], I),
             "fs_bin": ([P, P, P, P, I64, ctypes.POINTER(I64)], I),
             "fs_bin_splats": ([P, I64, P, P, P, P, I, I, P, P, I64, ctypes.POINTER(I64)], I),
@@ -247,6 +248,13 @@ class Context:
 
     # -- scene ---------------------------------------------------------------
     def set_scene(self, scene) -> None:
+        if getattr(scene, "_ply_block", None) is not None:  # scene_io.PlyScene: raw records
+            key = ("ply", id(scene), len(scene))
+            if key != self._scene_key:
+                self.set_scene_ply(scene)
+                self._scene_key = key
+                self._scene_ref = scene
+            return
         key = (id(scene), len(scene), scene.means.ctypes.data, scene.rotations.ctypes.data,
                scene.scales.ctypes.data, scene.opacities.ctypes.data)
         if key == self._scene_key:
@@ -259,6 +267,20 @@ class Context:
         self._scene_key = key
         self._scene_ref = scene  # keep the id() stable while cached
         self.n = len(scene)
+
+    def set_scene_ply(self, scene, params: np.ndarray = None) -> np.ndarray:
+        """fs_set_scene_ply: a PlyScene's float32 records -> the resident scene
+        (activations + validation on the device).  Returns bad[4] (first
+        offending vertex per check, -1 = none); raises nothing itself."""
+        bad = np.full(4, -1, np.int64)
+        offs = np.ascontiguousarray(scene._ply_offsets, dtype=np.int32)
+        self._scene_key = None
+        rc = load().fs_set_scene_ply(self.handle, len(scene), scene._ply_block.ctypes.data,
+                                     int(scene._ply_stride), _p(offs), _p(bad), _p(params))
+        if rc != FS_OK and not (bad >= 0).any():
+            _check(rc)
+        self.n = len(scene) if rc == FS_OK else 0
+        return bad
 
     def set_arrays(self, means, quats, scales, opac) -> None:
         m = np.ascontiguousarray(means, dtype=np.float64).reshape(-1, 3)

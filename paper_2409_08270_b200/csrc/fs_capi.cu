@@ -110,6 +110,9 @@ struct fs_context {
     size_t fin_lab_cap = 0;
     unsigned char* fin_stage = nullptr;  // peer parts staged when P2P access is unavailable
     size_t fin_stage_cap = 0;
+    float* ply_raw = nullptr;     // fs_set_scene_ply: the uploaded vertex records
+    size_t ply_raw_cap = 0;
+    unsigned long long* ply_bad = nullptr;  // its four first-offender slots
     bool timing = false;
     std::vector<cudaEvent_t> stage_events;  // 4 per view when timing
     // grow-only scratch reused across calls (no cudaMalloc/cudaFree per call)
@@ -846,7 +849,8 @@ void fs_destroy(fs_context* ctx) {
     if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
     if (ctx->ev_stop) cudaEventDestroy(ctx->ev_stop);
     if (ctx->ev_caller) cudaEventDestroy(ctx->ev_caller);
-    for (void* p : {(void*)ctx->fin_tmp, (void*)ctx->fin_lab, (void*)ctx->fin_stage})
+    for (void* p : {(void*)ctx->fin_tmp, (void*)ctx->fin_lab, (void*)ctx->fin_stage,
+                    (void*)ctx->ply_raw, (void*)ctx->ply_bad})
         if (p) cudaFree(p);
     delete ctx;
 }
@@ -956,6 +960,65 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
                            ctx->mz, ctx->sig, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
+    return FS_OK;
+}
+
+int fs_set_scene_ply(fs_context* ctx, int64_t n, const void* verts, int stride_floats,
+                     const int32_t* offsets, int64_t* bad, double* params) {
+    if (!ctx || !offsets || !bad) return fail(FS_EINVAL, "fs_set_scene_ply: NULL argument");
+    if (n < 0 || n > 0x7fffffffLL) return fail(FS_EINVAL, "fs_set_scene_ply: bad vertex count %lld", (long long)n);
+    if (n > 0 && !verts) return fail(FS_EINVAL, "fs_set_scene_ply: NULL vertex block");
+    fs::PlyOffsets off;
+    for (int k = 0; k < fs::kPlyProps; ++k) {
+        if (offsets[k] < 0 || offsets[k] >= stride_floats)
+            return fail(FS_EINVAL, "fs_set_scene_ply: property offset %d outside the %d-float record",
+                        offsets[k], stride_floats);
+        off.k[k] = offsets[k];
+    }
+    for (int k = 0; k < 4; ++k) bad[k] = -1;
+    CK(cudaSetDevice(ctx->device));
+    int rc;
+    if ((rc = order_after_caller(ctx))) return rc;
+    ctx->n = 0;  // not resident until validated
+    if (n > ctx->scene_cap) {
+        if ((rc = dev_alloc(&ctx->mx, n)) || (rc = dev_alloc(&ctx->my, n)) ||
+            (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->opac, n)) || (rc = dev_alloc(&ctx->up_means, 3 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->up_quats, 4 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->up_scales, 3 * (size_t)n)))
+            return rc;
+        ctx->scene_cap = n;
+    }
+    if (n == 0) return FS_OK;
+    const size_t bytes = (size_t)n * stride_floats * sizeof(float);
+    if ((rc = grow(&ctx->ply_raw, &ctx->ply_raw_cap, bytes / sizeof(float)))) return rc;
+    if (!ctx->ply_bad && (rc = dev_alloc(&ctx->ply_bad, 4))) return rc;
+    cudaStream_t st = ctx->work[0].stream;
+    // the records as the file stores them: one DMA (pinned) or the staged
+    // ring, no host-side column gather or activation
+    if ((rc = upload(ctx, ctx->ply_raw, verts, bytes, st))) return rc;
+    CK(cudaMemsetAsync(ctx->ply_bad, 0xff, 4 * sizeof(unsigned long long), st));
+    double* dparams = nullptr;
+    if (params) CK(cudaMallocAsync(reinterpret_cast<void**>(&dparams), 64 * (size_t)n, st));
+    fs::launch_scene_setup_ply((int)n, ctx->ply_raw, stride_floats, off, ctx->mx, ctx->my, ctx->mz,
+                               ctx->sig, ctx->opac, ctx->ply_bad, dparams, st);
+    CK(cudaGetLastError());
+    if (params) {
+        CK(sync_copy(params, dparams, 64 * (size_t)n, cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(dparams, st));
+    }
+    unsigned long long b[4];
+    CK(sync_copy(b, ctx->ply_bad, sizeof(b), cudaMemcpyDeviceToHost, st));
+    bool any = false;
+    for (int k = 0; k < 4; ++k) {
+        bad[k] = b[k] == ~0ull ? -1 : (int64_t)b[k];
+        any |= bad[k] >= 0;
+    }
+    if (any)
+        return fail(FS_EINVAL, "fs_set_scene_ply: invalid vertices (first non-finite %lld, "
+                               "quaternion %lld, scale %lld, opacity %lld)", (long long)bad[0],
+                    (long long)bad[1], (long long)bad[2], (long long)bad[3]);
+    ctx->n = n;
     return FS_OK;
 }
 

@@ -32,6 +32,15 @@ __device__ __forceinline__ void count_rect_tiles(unsigned long long rc, int tile
 }
 
 // ---- fs_project.cu ----
+// float offsets of the PLY vertex properties in the reference's
+// REQUIRED_PROPERTIES order (ply.py:17-23)
+constexpr int kPlyProps = 17;
+struct PlyOffsets {
+    int k[kPlyProps];
+};
+void launch_scene_setup_ply(int n, const float* verts, int stride, const PlyOffsets& off,
+                            double* mx, double* my, double* mz, double* sig, double* opac,
+                            unsigned long long* bad, double* params, cudaStream_t st);
 void launch_scene_setup(int n, const double* means, const double* quats, const double* scales,
                         double* mx, double* my, double* mz, double* sig, cudaStream_t st);
 void launch_project(int n, const double* mx, const double* my, const double* mz,

@@ -15,6 +15,40 @@
 
 namespace fs {
 
+// World covariance Sigma = (R S)(R S)^T of a unit quaternion (w, x, y, z) and
+// scales (scene.py:228-249) -> its six unique entries (SoA, stride n).
+__device__ __forceinline__ void store_covariance(double w, double x, double y, double z, double s0,
+                                                 double s1, double s2, double* __restrict__ sig,
+                                                 size_t n, int i) {
+    double r[9];
+    r[0] = 1.0 - 2.0 * (y * y + z * z);
+    r[1] = 2.0 * (x * y - w * z);
+    r[2] = 2.0 * (x * z + w * y);
+    r[3] = 2.0 * (x * y + w * z);
+    r[4] = 1.0 - 2.0 * (x * x + z * z);
+    r[5] = 2.0 * (y * z - w * x);
+    r[6] = 2.0 * (x * z - w * y);
+    r[7] = 2.0 * (y * z + w * x);
+    r[8] = 1.0 - 2.0 * (x * x + y * y);
+    double m[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        m[3 * k + 0] = r[3 * k + 0] * s0;
+        m[3 * k + 1] = r[3 * k + 1] * s1;
+        m[3 * k + 2] = r[3 * k + 2] * s2;
+    }
+    // Sigma[i][j] = sum_k m[i][k] m[j][k]; symmetric bit-for-bit (same products, same order)
+    auto dot = [&](int a, int b) {
+        return m[3 * a + 0] * m[3 * b + 0] + m[3 * a + 1] * m[3 * b + 1] + m[3 * a + 2] * m[3 * b + 2];
+    };
+    sig[0 * n + i] = dot(0, 0);
+    sig[1 * n + i] = dot(0, 1);
+    sig[2 * n + i] = dot(0, 2);
+    sig[3 * n + i] = dot(1, 1);
+    sig[4 * n + i] = dot(1, 2);
+    sig[5 * n + i] = dot(2, 2);
+}
+
 // K0: AoS host layout (means N x 3, unit quats N x 4, scales N x 3) -> SoA
 // means + world covariance Sigma = (R S)(R S)^T (scene.py:228-249).
 __global__ void scene_setup_kernel(int n, const double* __restrict__ means_aos,
@@ -26,36 +60,64 @@ __global__ void scene_setup_kernel(int n, const double* __restrict__ means_aos,
         mx[i] = means_aos[3 * i + 0];
         my[i] = means_aos[3 * i + 1];
         mz[i] = means_aos[3 * i + 2];
-        double w = quats_aos[4 * i + 0], x = quats_aos[4 * i + 1];
-        double y = quats_aos[4 * i + 2], z = quats_aos[4 * i + 3];
-        double r[9];
-        r[0] = 1.0 - 2.0 * (y * y + z * z);
-        r[1] = 2.0 * (x * y - w * z);
-        r[2] = 2.0 * (x * z + w * y);
-        r[3] = 2.0 * (x * y + w * z);
-        r[4] = 1.0 - 2.0 * (x * x + z * z);
-        r[5] = 2.0 * (y * z - w * x);
-        r[6] = 2.0 * (x * z - w * y);
-        r[7] = 2.0 * (y * z + w * x);
-        r[8] = 1.0 - 2.0 * (x * x + y * y);
-        double s0 = scales_aos[3 * i + 0], s1 = scales_aos[3 * i + 1], s2 = scales_aos[3 * i + 2];
-        double m[9];
+        store_covariance(quats_aos[4 * i + 0], quats_aos[4 * i + 1], quats_aos[4 * i + 2],
+                         quats_aos[4 * i + 3], scales_aos[3 * i + 0], scales_aos[3 * i + 1],
+                         scales_aos[3 * i + 2], sig, (size_t)n, i);
+    }
+}
+
+// K0 for a splat checkpoint: the PLY's float32 vertex
+// records -> the resident float64 scene, with the loader's activations and
+// the scene's validation fused in (ply.py:84-98, scene.py:96-110):
+//   finite check of every required property             (ply.py:84-88)
+//   means = float64(x, y, z)                              (:94)
+//   scales = exp(float64(scale_k))                        (:95)
+//   opacity = 1 / (1 + exp(-float64(opacity)))            (:96)
+//   q = float64(rot_k) / ||q||, ||q|| = sqrt(((q0^2 + q1^2) + q2^2) + q3^2)
+//       (np.linalg.norm's sequential sum; scene.py:96-100)
+// bad[0..3] collect (atomicMin) the first vertex with a non-finite value, a
+// zero / non-finite quaternion norm, a non-positive scale and an opacity
+// outside [0, 1]; the host raises the reference's error for the first
+// category that fired.  off[] = float offsets within a record, in the
+// reference's REQUIRED_PROPERTIES order (x y z nx ny nz f_dc_0..2 opacity
+// scale_0..2 rot_0..3).
+__global__ void scene_setup_ply_kernel(int n, const float* __restrict__ verts, int stride,
+                                       PlyOffsets off, double* __restrict__ mx,
+                                       double* __restrict__ my, double* __restrict__ mz,
+                                       double* __restrict__ sig, double* __restrict__ opac,
+                                       unsigned long long* __restrict__ bad,
+                                       double* __restrict__ params /* nullable: n x 8 */) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float* rec = verts + (size_t)i * stride;
+        float v[kPlyProps];
+        bool finite = true;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            m[3 * k + 0] = r[3 * k + 0] * s0;
-            m[3 * k + 1] = r[3 * k + 1] * s1;
-            m[3 * k + 2] = r[3 * k + 2] * s2;
+        for (int k = 0; k < kPlyProps; ++k) {
+            v[k] = __ldg(rec + off.k[k]);
+            finite &= isfinite(v[k]);
         }
-        // Sigma[i][j] = sum_k m[i][k] m[j][k]; symmetric bit-for-bit (same products, same order)
-        auto dot = [&](int a, int b) {
-            return m[3 * a + 0] * m[3 * b + 0] + m[3 * a + 1] * m[3 * b + 1] + m[3 * a + 2] * m[3 * b + 2];
-        };
-        sig[0 * (size_t)n + i] = dot(0, 0);
-        sig[1 * (size_t)n + i] = dot(0, 1);
-        sig[2 * (size_t)n + i] = dot(0, 2);
-        sig[3 * (size_t)n + i] = dot(1, 1);
-        sig[4 * (size_t)n + i] = dot(1, 2);
-        sig[5 * (size_t)n + i] = dot(2, 2);
+        if (!finite) {
+            atomicMin(&bad[0], (unsigned long long)i);
+            continue;
+        }
+        mx[i] = (double)v[0];
+        my[i] = (double)v[1];
+        mz[i] = (double)v[2];
+        const double s0 = exp((double)v[10]), s1 = exp((double)v[11]), s2 = exp((double)v[12]);
+        const double o = 1.0 / (1.0 + exp(-(double)v[9]));
+        const double q0 = (double)v[13], q1 = (double)v[14], q2 = (double)v[15], q3 = (double)v[16];
+        const double norm = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
+        if (!(norm > 0.0) || !isfinite(norm)) atomicMin(&bad[1], (unsigned long long)i);
+        if (!(s0 > 0.0 && s1 > 0.0 && s2 > 0.0)) atomicMin(&bad[2], (unsigned long long)i);
+        if (!(o >= 0.0 && o <= 1.0)) atomicMin(&bad[3], (unsigned long long)i);
+        opac[i] = o;
+        const double w = q0 / norm, x = q1 / norm, y = q2 / norm, z = q3 / norm;
+        store_covariance(w, x, y, z, s0, s1, s2, sig, (size_t)n, i);
+        if (params) {  // the activated GaussianScene parameters, for verification
+            double* p = params + 8 * (size_t)i;
+            p[0] = s0; p[1] = s1; p[2] = s2; p[3] = o;
+            p[4] = w; p[5] = x; p[6] = y; p[7] = z;
+        }
     }
 }
 
@@ -308,6 +370,16 @@ void launch_scene_setup(int n, const double* means, const double* quats, const d
     int grid = (n + 255) / 256;
     if (grid > 4096) grid = 4096;
     scene_setup_kernel<<<grid, 256, 0, st>>>(n, means, quats, scales, mx, my, mz, sig);
+}
+
+void launch_scene_setup_ply(int n, const float* verts, int stride, const PlyOffsets& off,
+                            double* mx, double* my, double* mz, double* sig, double* opac,
+                            unsigned long long* bad, double* params, cudaStream_t st) {
+    if (n <= 0) return;
+    int grid = (n + 255) / 256;
+    if (grid > 4096) grid = 4096;
+    scene_setup_ply_kernel<<<grid, 256, 0, st>>>(n, verts, stride, off, mx, my, mz, sig, opac, bad,
+                                                 params);
 }
 
 void launch_project(int n, const double* mx, const double* my, const double* mz,
