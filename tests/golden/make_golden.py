@@ -388,9 +388,57 @@ def gen_fullres():
     return cases
 
 
+def gen_scene_ply(tmpdir):
+    """Splat checkpoints loaded by the reference's own load_scene_ply (ply.py:63-106):
+    the file bytes and the activated float64 arrays.  The
+    second file interleaves extra per-vertex properties (f_rest_*, a non-standard
+    order) so a loader must honour the header's property offsets."""
+    from splatlift import ply as ref_ply
+    cases = {}
+    rng = np.random.default_rng(31)
+    n = 3000
+    base = dict(x=rng.normal(size=n), y=rng.normal(size=n), z=rng.uniform(2, 6, n),
+                nx=np.zeros(n), ny=np.zeros(n), nz=np.zeros(n),
+                f_dc_0=rng.normal(size=n), f_dc_1=rng.normal(size=n), f_dc_2=rng.normal(size=n),
+                opacity=rng.normal(0, 3, n), scale_0=rng.uniform(-7, 1, n),
+                scale_1=rng.uniform(-7, 1, n), scale_2=rng.uniform(-7, 1, n),
+                rot_0=rng.normal(size=n), rot_1=rng.normal(size=n), rot_2=rng.normal(size=n),
+                rot_3=rng.normal(size=n))
+    # extreme but valid values: opacity logits far out, near-degenerate quaternions
+    base["opacity"][:4] = [40.0, -40.0, 700.0, -700.0]
+    base["rot_1"][4:8] = base["rot_2"][4:8] = base["rot_3"][4:8] = 0.0
+    base["rot_0"][4:8] = [1e-30, 3e-38, 2.0, -1.0]
+    layouts = {
+        "plain": list(ref_ply.REQUIRED_PROPERTIES),
+        "interleaved": (["f_rest_0", "rot_3", "x", "f_rest_1", "scale_2", "opacity"] +
+                        [p for p in ref_ply.REQUIRED_PROPERTIES
+                         if p not in ("rot_3", "x", "scale_2", "opacity")] + ["f_rest_2"]),
+    }
+    for name, props in layouts.items():
+        rec = np.zeros(n, dtype=np.dtype([(p, "<f4") for p in props]))
+        for p in props:
+            rec[p] = base[p] if p in base else rng.normal(size=n)
+        path = Path(tmpdir) / f"{name}.ply"
+        head = ["ply", "format binary_little_endian 1.0", f"element vertex {n}"]
+        head += [f"property float {p}" for p in props] + ["end_header"]
+        with open(path, "wb") as fh:
+            fh.write(("\n".join(head) + "\n").encode("ascii"))
+            rec.tofile(fh)
+        sc = ref_ply.load_scene_ply(path)
+        cases[name] = dict(ply=np.frombuffer(path.read_bytes(), dtype=np.uint8),
+                           means=sc.means, rotations=sc.rotations, scales=sc.scales,
+                           opacities=sc.opacities, colors=sc.colors_dc)
+    return cases
+
+
 def main(which=None):
     if which == "fullres":
         save("accumulate_fullres", gen_fullres())
+        return
+    if which == "ply":
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            save("scene_ply", gen_scene_ply(d))
         return
     if which in (None, "render"):
         save("render", gen_render())

@@ -76,3 +76,30 @@ def test_matches_reference_loader(tmp_path):
     a, b = ref_ply.load_scene_ply(tmp_path / "r.ply"), load_scene_ply(tmp_path / "r.ply")
     for k in ("means", "rotations", "scales", "opacities", "colors_dc"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_host_loader_matches_reference_golden(tmp_path):
+    """The host loader against the arrays the reference's load_scene_ply produced
+    (tests/golden/scene_ply.npz, make_golden.py ``ply``), bit for bit; the lazy
+    PlyScene (device path) builds the same host arrays."""
+    from conftest import load_golden
+    from paper_2409_08270_b200.scene_io import PlyScene, _read_header
+
+    for case, c in load_golden("scene_ply").items():
+        p = tmp_path / f"{case}.ply"
+        p.write_bytes(bytes(c["ply"]))
+        s = load_scene_ply(p)
+        count, names, offset = _read_header(p.read_bytes()[:1 << 16])
+        verts = np.memmap(p, dtype=np.dtype([(q, "<f4") for q in names]), mode="r",
+                          offset=offset, shape=(count,))
+        block = np.memmap(p, dtype=np.float32, mode="r", offset=offset, shape=(count, len(names)))
+        lazy = PlyScene(p, count, names, block, verts)
+        for k, ref in (("means", "means"), ("rotations", "rotations"), ("scales", "scales"),
+                       ("opacities", "opacities"), ("colors_dc", "colors")):
+            assert np.array_equal(getattr(s, k), c[ref]), (case, k)
+            assert np.array_equal(getattr(lazy, k), c[ref]), (case, k)
+        assert len(lazy) == count
+        # offsets of the required properties in the record, reference order
+        assert [names[i] for i in lazy._ply_offsets] == list(
+            ("x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2", "opacity",
+             "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"))
