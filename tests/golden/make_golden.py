@@ -431,9 +431,72 @@ def gen_scene_ply(tmpdir):
     return cases
 
 
+def fixture_case(fix, pairs=None):
+    """Inputs of a reference SynthFixture's training views, verbatim."""
+    pairs = fix.training_views() if pairs is None else pairs
+    out = {f"in_{a}": c for a, c in scene_arrays(fix.scene).items()}
+    out["cams"] = np.stack([cam_row(v) for v, _ in pairs])
+    out["masks"] = np.stack([m.labels for _, m in pairs])
+    return out
+
+
+def gen_acceptance():
+    """Inputs and reference answers for the acceptance suite restated on the GPU
+    (tests/test_gpu_acceptance.py): reference tests/test_acceptance.py:53-77
+    (global optimality vs the exhaustive oracle, 200 seeded instances),
+    :140-197 (gamma nesting, scale invariance, scene/binary consistency),
+    :230-247 (latency fixture) and tests/test_solver.py:100-159."""
+    from splatlift import brute_force_oracle, objective_value
+    from splatlift.synth import make_random, make_two_cluster
+    X = ref.EXACT_BLEND
+    cases = {}
+    t0 = time.perf_counter()
+    master = np.random.default_rng(1234)  # test_acceptance.py:56-66, same draws
+    for case in range(200):
+        seed = int(master.integers(0, 2**31))
+        fix = make_random(seed=seed, n_gaussians=int(master.integers(4, 13)),
+                          n_views=int(master.integers(1, 4)), width=int(master.integers(8, 17)),
+                          height=int(master.integers(8, 17)))
+        pairs = fix.training_views()
+        c = fixture_case(fix, pairs)
+        matrix = ref.accumulate_contributions(fix.scene, pairs, 2, X)
+        labels = ref.assign_binary(matrix, 0.0).labels
+        best_labels, best = brute_force_oracle(fix.scene, pairs, X)
+        c.update(A=matrix.values, labels=labels, best_labels=best_labels,
+                 best=np.float64(best),
+                 achieved=np.float64(objective_value(fix.scene, pairs, labels, X)))
+        cases[f"opt{case:03d}"] = c
+    print(f"  optimality instances: {time.perf_counter() - t0:.1f}s", flush=True)
+    for case in range(5):  # test_acceptance.py:146-150
+        fix = make_random(seed=900 + case, n_gaussians=40, n_views=2, width=24, height=24)
+        cases[f"mono{case}"] = fixture_case(fix)
+    for case in range(20):  # test_acceptance.py:176-180
+        e = 3 + case % 3
+        fix = make_random(seed=500 + case, n_gaussians=20, n_views=2, width=16, height=16,
+                          num_objects=e)
+        c = fixture_case(fix)
+        c["E"] = np.int64(e)
+        cases[f"rel{case:02d}"] = c
+    for seed in range(6):  # test_solver.py:115-118
+        fix = make_random(seed=seed, n_gaussians=15, n_views=2, width=16, height=16,
+                          num_objects=4)
+        c = fixture_case(fix)
+        c["E"] = np.int64(4)
+        cases[f"solver_rel{seed}"] = c
+    fix = make_two_cluster(seed=42, n_gaussians=2000, n_views=12, width=128, height=128,
+                           n_mask_views=6)  # test_acceptance.py:47-51
+    c = fixture_case(fix)
+    c["A"] = ref.accumulate_contributions(fix.scene, fix.training_views(), 2).values
+    cases["cluster"] = c
+    return cases
+
+
 def main(which=None):
     if which == "fullres":
         save("accumulate_fullres", gen_fullres())
+        return
+    if which == "acceptance":
+        save("acceptance", gen_acceptance())
         return
     if which == "ply":
         import tempfile

@@ -140,3 +140,20 @@ def test_oracle_matches_reference_at_benchmark_resolution():
     assert np.count_nonzero(A != c["A"]) <= A.size // 10000
     np.testing.assert_allclose(A, c["A"], rtol=1e-6, atol=1e-9)
     assert np.array_equal(oracle.assign_scene(c["A"], 0.0), c["labels_g0"])
+
+
+def test_oracle_on_acceptance_instances():
+    """The oracle reproduces the reference's matrices and labels on the 200
+    optimality instances and the two-cluster fixture (tests/golden/acceptance.npz)."""
+    from conftest import cam_from_row
+    acc = load_golden("acceptance")
+    for k, c in acc.items():
+        if not (k.startswith("opt") or k == "cluster"):
+            continue
+        cams = [oracle.camera_of(cam_from_row(r, i)) for i, r in enumerate(c["cams"])]
+        floors = (0.0, 0.0) if k.startswith("opt") else (1 / 255, 1e-4)
+        A = oracle.accumulate(c["in_means"], c["in_quats"], c["in_scales"], c["in_opac"], cams,
+                              list(c["masks"]), 2, *floors, threads=4)
+        np.testing.assert_allclose(A, c["A"], rtol=1e-6, atol=1e-12)
+        if k.startswith("opt"):
+            assert np.array_equal(oracle.assign_binary(A, 0.0), c["labels"]), k
