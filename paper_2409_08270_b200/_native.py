@@ -16,7 +16,10 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libflashsplat_b200.so"
+# FS_LIB=checked selects the bounds-checked build (csrc/Makefile ``checked``)
+LIB_PATH = (Path(__file__).resolve().parent
+            / ("_lib_checked" if os.environ.get("FS_LIB") == "checked" else "_lib")
+            / "libflashsplat_b200.so")
 
 FS_OK, FS_EINVAL, FS_ECUDA, FS_ENOMEM, FS_ELABEL = 0, 1, 2, 3, 4
 MODE_BINARY, MODE_SCENE = 0, 1

@@ -202,9 +202,14 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int
             const unsigned long long e = ((k >> shift) << 32) | (unsigned int)(g0 + j * kBinThreads);
             const unsigned int tx0 = r & 0xFFFF, tx1 = (r >> 16) & 0xFFFF;
             const unsigned int ty0 = (r >> 32) & 0xFFFF, ty1 = (r >> 48) & 0xFFFF;
+            FS_CHECK(tx1 < (unsigned)tiles_x && ty1 * (unsigned)tiles_x + tx1 < (unsigned)ntiles);
             for (unsigned int ty = ty0; ty <= ty1; ++ty)
-                for (unsigned int tx = tx0; tx <= tx1; ++tx)
-                    b.inst[atomicAdd(&s_cur[ty * (unsigned)tiles_x + tx], 1u)] = e;
+                for (unsigned int tx = tx0; tx <= tx1; ++tx) {
+                    const unsigned int t = ty * (unsigned)tiles_x + tx;
+                    const unsigned int at = atomicAdd(&s_cur[t], 1u);
+                    FS_CHECK(at < b.tile_start[t + 1] && at < b.capacity);
+                    b.inst[at] = e;
+                }
         }
     }
 }

@@ -14,6 +14,7 @@
 // growing them (the raster kernel skips an overflowed view, so nothing was
 // added for it).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -147,6 +148,15 @@ int report_error(int code, const char* msg) { return fail(code, "%s", msg); }
 }  // namespace fs
 
 using fs::fail;
+
+namespace {
+// NVTX range for the duration of an entry point (header-only NVTX v3: free
+// unless a profiler injects itself)
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -549,6 +559,7 @@ int accumulate_on(fs_context* ctx, const ViewPlan& plan, const fs_camera* cams,
                   const uint16_t* const* masks, int masks_on_device, int num_objects,
                   double alpha_floor, double t_floor, int acc_kind, void* acc,
                   std::atomic<int>* queue, CtxRun& R) {
+    Range nvtx_range("view loop (project -> bin -> raster per view)");
     CK(cudaSetDevice(ctx->device));
     int rc;
     const int n_views = plan.n_views;
@@ -932,6 +943,7 @@ int fs_set_timing(fs_context* ctx, int enable) {
 
 int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* quats,
                  const double* scales, const double* opacities) {
+    Range nvtx_range("fs_set_scene");
     if (!ctx) return fail(FS_EINVAL, "fs_set_scene: NULL context");
     if (n < 0 || n > 0x7fffffffLL) return fail(FS_EINVAL, "fs_set_scene: bad Gaussian count %lld", (long long)n);
     if (n > 0 && (!means || !quats || !scales || !opacities))
@@ -965,6 +977,7 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
 
 int fs_set_scene_ply(fs_context* ctx, int64_t n, const void* verts, int stride_floats,
                      const int32_t* offsets, int64_t* bad, double* params) {
+    Range nvtx_range("fs_set_scene_ply");
     if (!ctx || !offsets || !bad) return fail(FS_EINVAL, "fs_set_scene_ply: NULL argument");
     if (n < 0 || n > 0x7fffffffLL) return fail(FS_EINVAL, "fs_set_scene_ply: bad vertex count %lld", (long long)n);
     if (n > 0 && !verts) return fail(FS_EINVAL, "fs_set_scene_ply: NULL vertex block");
@@ -1024,6 +1037,7 @@ int fs_set_scene_ply(fs_context* ctx, int64_t n, const void* verts, int stride_f
 
 int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* mean2d,
                double* conic, double* depth, int64_t* radius, fs_projection_stats* stats) {
+    Range nvtx_range("fs_project");
     if (!ctx || !cam || !alive) return fail(FS_EINVAL, "fs_project: NULL argument");
     int rc = check_cam(*cam, 0);
     if (rc) return rc;
@@ -1086,6 +1100,7 @@ static int copy_tile_lists(fs::Work& w, int ntiles, unsigned int n_valid, int64_
 
 int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t* items,
            int64_t items_capacity, int64_t* n_items) {
+    Range nvtx_range("fs_bin");
     if (!ctx || !cam || !tile_offsets || !n_items) return fail(FS_EINVAL, "fs_bin: NULL argument");
     int rc = check_cam(*cam, 0);
     if (rc) return rc;
@@ -1168,6 +1183,7 @@ int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double
 int fs_accumulate(fs_context* ctx, int n_views, const fs_camera* cams, const uint16_t* const* masks,
                   int masks_on_device, int num_objects, double alpha_floor, double t_floor,
                   int acc_kind, void* acc, fs_accumulate_stats* stats) {
+    Range nvtx_range("fs_accumulate");
     if (!ctx) return fail(FS_EINVAL, "fs_accumulate: NULL context");
     if (stats) {
         memset(stats, 0, sizeof(*stats));
@@ -1189,6 +1205,7 @@ int fs_accumulate_multi(fs_context* const* ctxs, int n_ctx, int n_views, const f
                         const uint16_t* const* masks, int num_objects, double alpha_floor,
                         double t_floor, int acc_kind, void* const* accs, int32_t* view_ctx,
                         fs_accumulate_stats* stats) {
+    Range nvtx_range("fs_accumulate_multi");
     if (!ctxs || n_ctx < 1 || n_ctx > fs::kMaxParts || !accs)
         return fail(FS_EINVAL, "fs_accumulate_multi: need 1..%d contexts and accumulators",
                     fs::kMaxParts);
@@ -1241,6 +1258,7 @@ int fs_enable_peer_access(fs_context* ctx, int peer_device) {
 int fs_reduce_finalize(fs_context* ctx, int acc_kind, const void* const* parts, int n_parts,
                        int64_t part_g0, int64_t n, int num_objects, int64_t g0, int64_t g1,
                        float* out, int64_t ld, int out_on_device) {
+    Range nvtx_range("fs_reduce_finalize");
     if (!ctx) return fail(FS_EINVAL, "fs_reduce_finalize: NULL context");
     if (acc_kind != FS_ACC_F64 && acc_kind != FS_ACC_FIXED)
         return fail(FS_EINVAL, "bad accumulator kind %d", acc_kind);
@@ -1277,6 +1295,7 @@ int fs_finalize(fs_context* ctx, int acc_kind, const void* acc, int64_t n, int n
 int fs_finalize_multi(fs_context* const* ctxs, int n_ctx, int acc_kind, void* const* accs,
                       int64_t n, int num_objects, float* out, float gamma, int mode,
                       uint8_t* labels) {
+    Range nvtx_range("fs_finalize_multi");
     if (!ctxs || n_ctx < 1 || n_ctx > fs::kMaxParts || !accs)
         return fail(FS_EINVAL, "fs_finalize_multi: need 1..%d contexts and accumulators",
                     fs::kMaxParts);
@@ -1326,6 +1345,7 @@ int fs_finalize_multi(fs_context* const* ctxs, int n_ctx, int acc_kind, void* co
 
 int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float gamma, int mode,
               uint8_t* out, int on_device) {
+    Range nvtx_range("fs_assign");
     if ((!A || !out) && n > 0) return fail(FS_EINVAL, "fs_assign: NULL argument");
     if (mode != FS_MODE_BINARY && mode != FS_MODE_SCENE) return fail(FS_EINVAL, "fs_assign: bad mode %d", mode);
     if (mode == FS_MODE_BINARY && num_objects != 2)
@@ -1363,6 +1383,7 @@ int fs_assign(fs_context* ctx, const float* A, int64_t n, int num_objects, float
 }
 
 int fs_member_counts(fs_context* ctx, const uint8_t* m, int64_t n, int rows, int64_t* counts) {
+    Range nvtx_range("fs_member_counts");
     if (!ctx || !counts || (!m && n > 0 && rows > 0)) return fail(FS_EINVAL, "fs_member_counts: NULL argument");
     if (n < 0 || rows < 0) return fail(FS_EINVAL, "fs_member_counts: bad shape");
     if (rows == 0) return FS_OK;
@@ -1384,7 +1405,8 @@ int fs_member_counts(fs_context* ctx, const uint8_t* m, int64_t n, int rows, int
 namespace {
 
 fs::RasterArgs render_args(fs::Work& w, int width, int height, double alpha_floor,
-                           double t_floor, double* out, int channels, const double* ch_dev) {
+                           double t_floor, double* out, int channels, const double* ch_dev,
+                           long long n_ids) {
     const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
     const size_t px = (size_t)width * height;
     fs::RasterArgs ra{};
@@ -1393,6 +1415,7 @@ fs::RasterArgs render_args(fs::Work& w, int width, int height, double alpha_floo
     ra.tiles_x = tx;
     ra.ntiles = ntiles;
     ra.num_objects = 1;
+    ra.n_gaussians = n_ids;  // gids index the records / channel
     ra.af_eff = alpha_floor > 0.0 ? alpha_floor : -1.0;  // rasterizer.py:181-182
     ra.tf_eff = t_floor > 0.0 ? t_floor : -1.0;          // rasterizer.py:193-194
     ra.sort = tile_sort_args(w);
@@ -1426,7 +1449,7 @@ int render_scene_device(fs_context* ctx, const fs_camera* cam, const uint8_t* me
         ex.member = member_dev;
         enqueue_bin(ctx, w, to_cam(*cam), alpha_floor, 1, ex);
         fs::launch_raster_render(render_args(w, cam->width, cam->height, alpha_floor, t_floor, out,
-                                             channels, ch_dev),
+                                             channels, ch_dev, ctx->n),
                                  w.stream);
         CK(cudaGetLastError());
         fs::ViewCounters vc{};
@@ -1475,6 +1498,7 @@ extern "C" {
 int fs_render(fs_context* ctx, const fs_camera* cam, const uint8_t* member, double alpha_floor,
               double transmittance_floor, const double* channel, int channels, double* value,
               double* alpha, double* depth) {
+    Range nvtx_range("fs_render");
     if (!ctx || !cam || !alpha || !depth) return fail(FS_EINVAL, "fs_render: NULL argument");
     if (channels != 0 && channels != 1 && channels != 3)
         return fail(FS_EINVAL, "fs_render: channels must be 0, 1 or 3, got %d", channels);
@@ -1514,6 +1538,7 @@ int fs_render_splats(fs_context* ctx, int width, int height, int64_t k, const do
                      const int64_t* tile_offsets, const int64_t* items, double alpha_floor,
                      double transmittance_floor, const double* channel, int channels,
                      double* value, double* alpha, double* depth_out) {
+    Range nvtx_range("fs_render_splats");
     if (!ctx || !tile_offsets || !alpha || !depth_out ||
         (k > 0 && (!mean2d || !conic || !depth || !opacity)))
         return fail(FS_EINVAL, "fs_render_splats: NULL argument");
@@ -1575,7 +1600,7 @@ int fs_render_splats(fs_context* ctx, int width, int height, int64_t k, const do
     fs::launch_splat_records((int)k, d_mean, d_conic, d_depth, d_opac, alpha_floor, w.r32, w.r64,
                              w.k64, ctx->num_sms, st);
     fs::RasterArgs ra = render_args(w, width, height, alpha_floor, transmittance_floor, ctx->rn_f64,
-                                    channels, channels ? d_ch : nullptr);
+                                    channels, channels ? d_ch : nullptr, k);
     ra.render.lists = ctx->rn_u32;
     ra.tile_order = ctx->rn_u32 + lists.size();
     fs::launch_raster_render(ra, st);
@@ -1592,6 +1617,7 @@ int fs_render_splats(fs_context* ctx, int width, int height, int64_t k, const do
 int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* membership,
                    int num_objects, double tau, double alpha_floor, double transmittance_floor,
                    uint16_t* labels) {
+    Range nvtx_range("fs_render_mask");
     if (!ctx || !cam || !labels || (!membership && ctx->n > 0))
         return fail(FS_EINVAL, "fs_render_mask: NULL argument");
     if (num_objects < 1 || num_objects > 65536)
@@ -1641,7 +1667,8 @@ int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* members
         const int grid = (int)std::min<size_t>((px + 255) / 256, (size_t)ctx->num_sms * 8);
         const int ngrid = (int)std::min<size_t>((n + 255) / 256, (size_t)ctx->num_sms * 8);
         const fs::RasterArgs ra = render_args(w, cam->width, cam->height, alpha_floor,
-                                              transmittance_floor, ctx->rn_f64, 0, nullptr);
+                                              transmittance_floor, ctx->rn_f64, 0, nullptr,
+                                              (long long)n);
         for (int obj : objs) {
             member_rect_kernel<<<std::max(ngrid, 1), 256, 0, st>>>(
                 ctx->rn_rect, ctx->rn_member + (size_t)obj * n, (long long)n, w.rect);

@@ -10,7 +10,28 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Device-side bounds / invariant checks, compiled in only for the checked build
+// (make checked -> _lib_checked/, FS_LIB=checked): compute-sanitizer is not
+// available on the GPU pool, so the shared-memory and global indices the
+// kernels compute are asserted instead and the GPU test-suite is run against
+// that build.  A failed check prints its location and traps.
+#ifdef FS_CHECKS
+#define FS_CHECK(cond)                                                                     \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("FS_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                              \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define FS_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
 
 namespace fs {
 

@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         const bool hit = cand != 0u;
         const unsigned int bal = __ballot_sync(0xffffffffu, hit);
         if (hit) {
+            FS_CHECK(g < (unsigned)a.n_gaussians && cnt + __popc(bal) <= kRing);
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
             W.cm[slot] = cand;
             W.gid[slot] = g;
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                     while (mm) {
                         const int k = __ffs(mm) - 1;
                         mm &= mm - 1u;
+                        FS_CHECK(q < (unsigned)(kMini * 32) && k < nm);
                         W.queue[q++] = (unsigned short)((k << 5) | lane);
                     }
                 }
@@ -317,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 for (int q0 = lane; q0 < total; q0 += 32) {
                     const unsigned int e = W.queue[q0];
                     const int k = e >> 5, src = e & 31;
+                    FS_CHECK(k < nm && q0 < kMini * 32);
                     const Rec64 q = W.rec[k];
                     // pixel centre (k + 0.5, j + 0.5) of the source lane, exact in float64
                     const double cx = (double)(x0 + (src & 15)) + 0.5;
@@ -386,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                         const bool fire = lane < kMini && k < nm && v > 0.0 && gl < (unsigned)a.num_objects;
                         if (fire) {
+                            FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians);
                             acc_add<kFixed>(acc, acc_fx,
                                             (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + gl, v);
                             ++atom;
@@ -398,6 +402,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         mm &= mm - 1u;
                         const double w = myval[k * kRowStride + lane];
                         if (w > 0.0) {
+                            FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians &&
+                                     label < n_obj);
                             acc_add<kFixed>(acc, acc_fx,
                                             (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label, w);
                             ++atom;

@@ -170,8 +170,13 @@ static __device__ void smem_count_sort(PK pk, unsigned short* b, unsigned int n,
         run += c[j];
     }
     __syncthreads();
-    for (unsigned int i = threadIdx.x; i < n; i += kThreads)
-        b[atomicAdd(&hist[digit_of(pk(i), m)], 1u)] = (unsigned short)i;
+    for (unsigned int i = threadIdx.x; i < n; i += kThreads) {
+        const unsigned int d = digit_of(pk(i), m);
+        FS_CHECK(d < 2048u);
+        const unsigned int at = atomicAdd(&hist[d], 1u);
+        FS_CHECK(at < n);
+        b[at] = (unsigned short)i;
+    }
     __syncthreads();
 }
 
@@ -200,6 +205,7 @@ static __device__ __forceinline__ void place_digit_runs(PK pk, Entry entry, cons
                 pos += (kj != key ? kj < key : entry_less(entry(j), entry(i), K)) ? 1u : 0u;
             }
         }
+        FS_CHECK(pos < n && i < n);
         store(pos, i);
     }
 }
@@ -260,6 +266,7 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
     unsigned int* misc = whist + 2048;
     unsigned short* b = reinterpret_cast<unsigned short*>(misc + 64);
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(misc + 62);
+    FS_CHECK(reinterpret_cast<unsigned char*>(b + cap) <= smem + smem_bytes);
     if (n <= cap) {
         a = bulk_load_bucket(in, n, region, bar);  // TMA: global bucket -> shared memory
         const unsigned long long* sa = a;
@@ -281,6 +288,7 @@ static __device__ __noinline__ void sort_tile_list(const unsigned long long* in,
         unsigned int* misc2 = hist2 + 2048;
         unsigned int* pks = misc2 + 64;
         unsigned short* idx2 = reinterpret_cast<unsigned short*>(pks + cap2);
+        FS_CHECK(reinterpret_cast<unsigned char*>(idx2 + n) <= smem + smem_bytes);
         for (unsigned int i = threadIdx.x; i < n; i += kThreads) pks[i] = pk_of(in[i]);
         __syncthreads();
         auto pk = [pks](unsigned int i) { return pks[i]; };
