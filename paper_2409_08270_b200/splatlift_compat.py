@@ -20,6 +20,14 @@ read the documented attributes) and return objects with the reference's
 attributes and file formats (``values`` / ``save`` / ``load``;
 ``labels`` / ``membership`` / ``save``).  ``uninstall()`` restores the
 originals.
+
+Multi-GPU: ``install(devices=...)`` makes the rebound
+``accumulate_contributions`` -- the CLI's ``splatlift accumulate``
+(cli.py:96-107) and any user code -- split the views over those GPUs from
+the calling process (``multidevice.py``: one native thread per GPU, dynamic
+view queue, peer-memory reduction).  The default ``"auto"`` uses every
+visible GPU when there is more than one (``FLASHSPLAT_DEVICES=0,1,...`` or
+``all`` overrides); ``None`` keeps one GPU.
 """
 
 from __future__ import annotations
@@ -46,6 +54,28 @@ _TARGETS = {
     "load_scene_ply": ["splatlift", "splatlift.ply", "splatlift.cli"],
 }
 _saved: dict = {}
+_devices = None  # GPU list the rebound accumulate_contributions spreads views over
+
+
+def resolve_devices(devices="auto"):
+    """None, or the list of CUDA ordinals to use (``"auto"``: all GPUs if > 1)."""
+    import os
+    env = os.environ.get("FLASHSPLAT_DEVICES")
+    if devices == "auto" and env:
+        devices = "all" if env.strip() == "all" else [int(x) for x in env.split(",") if x.strip()]
+    if devices in ("auto", "all"):
+        from . import _native
+        try:
+            count = _native.device_count()
+        except _native.NativeUnavailable:
+            count = 0
+        if devices == "auto" and count < 2:
+            return None
+        return list(range(count)) if count else None
+    if devices is None:
+        return None
+    devices = [int(d) for d in devices]
+    return devices if len(devices) > 1 else None
 
 
 def _replacement(name):
@@ -88,6 +118,8 @@ def _replacement(name):
 
         def accumulate_contributions(scene, views, num_objects, blend=None, **kw):
             from .rasterizer import DEFAULT_BLEND
+            if _devices is not None and "device" not in kw and "process_group" not in kw:
+                kw.setdefault("devices", list(_devices))
             m = _contrib.accumulate_contributions(scene, views, num_objects,
                                                   blend if blend is not None else DEFAULT_BLEND,
                                                   **kw)
@@ -106,7 +138,9 @@ def _replacement(name):
     return assign
 
 
-def install() -> None:
+def install(devices="auto") -> None:
+    global _devices
+    _devices = resolve_devices(devices)
     for name, modules in _TARGETS.items():
         fn = _replacement(name)
         for modname in modules:
@@ -120,6 +154,8 @@ def install() -> None:
 
 
 def uninstall() -> None:
+    global _devices
+    _devices = None
     for (modname, name), fn in _saved.items():
         setattr(importlib.import_module(modname), name, fn)
     _saved.clear()

@@ -100,3 +100,29 @@ def test_file_formats_byte_identical_to_reference(splatlift, tmp_path):
                 == (tmp_path / f"ref_{mode}.bin").read_bytes())
         back = splatlift.Assignment.load(tmp_path / f"ours_{mode}.bin")
         assert back.mode == mode and back.member_counts() == Assignment(mode, 0.25, **kw).member_counts()
+
+
+def test_install_devices_reach_the_multi_gpu_path(splatlift, monkeypatch):
+    """install(devices=[...]) makes the rebound accumulate (the CLI's, cli.py:104)
+    split views over those GPUs; one device / None keeps the single-GPU path."""
+    from paper_2409_08270_b200 import splatlift_compat
+    from paper_2409_08270_b200 import contributions as contrib
+    import splatlift.cli as cli
+    import numpy as np
+    seen = {}
+
+    def fake(scene, views, num_objects, blend, **kw):
+        seen.update(kw)
+        return contrib.ContributionMatrix(values=np.zeros((num_objects, 1), np.float32))
+
+    monkeypatch.setattr(contrib, "accumulate_contributions", fake)
+    for devices, expect in (([0, 1, 2], [0, 1, 2]), ([3], None), (None, None)):
+        seen.clear()
+        splatlift_compat.install(devices=devices)
+        try:
+            cli.accumulate_contributions(object(), [], 2)
+        finally:
+            splatlift_compat.uninstall()
+        assert seen.get("devices") == expect
+    monkeypatch.setenv("FLASHSPLAT_DEVICES", "1,0")
+    assert splatlift_compat.resolve_devices("auto") == [1, 0]
