@@ -51,6 +51,15 @@ constexpr int kMini = 16;      // strip hits per mini-batch
 constexpr int kRing = 64;       // per-warp ring of strip hits (>= kMini - 1 + 32)
 constexpr int kRowStride = 33;  // doubles per padded w/alpha row (bank-conflict-free transpose)
 constexpr int kMaxGroups = 4;   // label groups per warp reduced before the atomics
+// A warp's pixel block: kBH rows x kBW columns of the 16 x 16 tile, lane l at
+// column l % kBW, row l / kBW (bit l of a candidate mask).
+#ifndef FS_BLOCK_W
+#define FS_BLOCK_W 8
+#endif
+constexpr int kBW = FS_BLOCK_W;
+constexpr int kBH = 32 / kBW;
+constexpr unsigned int kRowMask = (kBW == 32) ? 0xffffffffu : ((1u << kBW) - 1u);
+static_assert(kBW == 8 || kBW == 16, "warp pixel blocks are 2 x 16 or 4 x 8");
 
 struct WarpSmem {
     Rec64 rec[kMini];        // float64 records of the mini-batch's hits
@@ -127,10 +136,11 @@ __device__ __forceinline__ unsigned int warp_transpose16x32(unsigned int x, int 
 // Candidate columns of one pixel row for one splat: the pixels whose float32
 // power clears the conservative cut, from the roots of the quadratic
 //   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
-// (widened by float32 rounding margins).  Returns a 16-bit column mask.
+// (widened by float32 rounding margins).  Returns a kBW-bit column mask of the
+// columns x0 .. x0 + kBW - 1.
 __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0,
                                                        float inv_a) {
-    if (!(s.cut > -INFINITY)) return 0xFFFFu;  // exact blend: no alpha floor
+    if (!(s.cut > -INFINITY)) return kRowMask;  // exact blend: no alpha floor
     const float dv = v_centre - s.my;
     const float Q = -2.0f * s.cut;
     const float detc = s.a * s.c - s.b * s.b;
@@ -146,10 +156,47 @@ __device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_c
     const float eps = 0.03f + 1e-5f * fabsf(ctr);
     const float lo = ceilf(ctr - half - eps) - (float)x0;
     const float hi = floorf(ctr + half + eps) - (float)x0;
-    if (hi < 0.0f || lo > 15.0f || lo > hi) return 0u;
+    if (hi < 0.0f || lo > (float)(kBW - 1) || lo > hi) return 0u;
     const int c0 = lo < 0.0f ? 0 : (int)lo;
-    const int c1 = hi > 15.0f ? 15 : (int)hi;
+    const int c1 = hi > (float)(kBW - 1) ? kBW - 1 : (int)hi;
     return (2u << c1) - (1u << c0);
+}
+
+// Candidate mask of a whole kBH x kBW block (bit r * kBW + c = pixel (xb + c,
+// v_lo - 0.5 + r)): row_candidates for every row with the splat's per-row
+// invariants (1/a, Q, det, a*Q) computed once.  Same float32 expressions and
+// margins as row_candidates, up to float32 rounding (~1e-6 px against the 0.03 px
+// interval margin).
+__device__ __forceinline__ unsigned int block_candidates(const Rec32& s, float v_lo, int xb) {
+    if (!(s.cut > -INFINITY)) return 0xffffffffu;  // exact blend: no alpha floor
+    float inv_a;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_a) : "f"(s.a));
+    const float Q = -2.0f * s.cut;
+    const float detc = s.a * s.c - s.b * s.b;
+    const float t1 = s.a * Q, at1 = fabsf(t1);
+    const float base = s.mx - 0.5f, binv = s.b * inv_a, xf = (float)xb;
+    unsigned int cand = 0;
+#pragma unroll
+    for (int r = 0; r < kBH; ++r) {
+        const float dv = (v_lo + (float)r) - s.my;
+        const float t2 = detc * dv * dv;
+        const float D = t1 - t2 + 1e-5f * (at1 + fabsf(t2)) + 1e-20f;
+        if (D >= 0.0f) {
+            float sq;
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));
+            const float ctr = base - binv * dv;
+            const float half = sq * inv_a;
+            const float eps = 0.03f + 1e-5f * fabsf(ctr);
+            const float lo = ceilf(ctr - half - eps) - xf;
+            const float hi = floorf(ctr + half + eps) - xf;
+            if (!(hi < 0.0f || lo > (float)(kBW - 1) || lo > hi)) {
+                const int c0 = lo < 0.0f ? 0 : (int)lo;
+                const int c1 = hi > (float)(kBW - 1) ? kBW - 1 : (int)hi;
+                cand |= ((2u << c1) - (1u << c0)) << (r * kBW);
+            }
+        }
+    }
+    return cand;
 }
 
 // float64 depth of a gid from its order-preserving key (inverse of f64_sort_key)
@@ -167,8 +214,10 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     if (vc->overflow) return;
     const int tile = (int)a.tile_order[blockIdx.x];  // longest buckets first
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int x0 = (tile % a.tiles_x) * kTile, y0 = (tile / a.tiles_x) * kTile;
-    const int px = x0 + (tid & 15), py = y0 + (tid >> 4);
+    // the warp's pixel block inside the tile, and this lane's pixel
+    const int xb = (tile % a.tiles_x) * kTile + (warp % (kTile / kBW)) * kBW;
+    const int yb = (tile / a.tiles_x) * kTile + (warp / (kTile / kBW)) * kBH;
+    const int px = xb + lane % kBW, py = yb + lane / kBW;
     const bool inside = px < a.width && py < a.height;
     const unsigned int label = (!kRender && inside) ? a.mask[(size_t)py * a.width + px] : 0u;
     if (!kRender) {
@@ -202,8 +251,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
     WarpSmem& W = S.w[warp];
     const unsigned int lt_mask = (1u << lane) - 1u;
     // the warp's pixel-centre strip
-    const float u_lo = (float)x0 + 0.5f, u_hi = (float)x0 + 15.5f;
-    const float v_lo = (float)(y0 + 2 * warp) + 0.5f, v_hi = v_lo + 1.0f;
+    const float u_lo = (float)xb + 0.5f, u_hi = u_lo + (float)(kBW - 1);
+    const float v_lo = (float)yb + 0.5f, v_hi = v_lo + (float)(kBH - 1);
 
     // The warp's label groups (fixed for the whole walk): lanes sharing a label.
     // With at most kMaxGroups distinct labels, C reduces w per (splat, label)
@@ -255,9 +304,15 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         if (idx < n_list) {
             if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
                   v_lo > s.my + s.hy)) {
-                float inv_a;  // shared by both rows (one MUFU instead of two)
+#ifdef FS_ROW_SCREEN
+                float inv_a;  // shared by the rows (one MUFU)
                 asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_a) : "f"(s.a));
-                cand = row_candidates(s, v_lo, x0, inv_a) | (row_candidates(s, v_hi, x0, inv_a) << 16);
+#pragma unroll
+                for (int r = 0; r < kBH; ++r)
+                    cand |= row_candidates(s, v_lo + (float)r, xb, inv_a) << (r * kBW);
+#else
+                cand = block_candidates(s, v_lo, xb);
+#endif
             }
         }
         steps += min(32u, n_list - c);
@@ -268,6 +323,11 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
             W.cm[slot] = cand;
             W.gid[slot] = g;
+#ifdef FS_PREFETCH_REC64
+            // the hit's float64 record is read when its mini-batch starts: start the
+            // L2 -> L1 move now so that load does not wait a full L2 round trip
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.r64 + g));
+#endif
         }
         cnt += __popc(bal);
         __syncwarp();
@@ -322,8 +382,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                     FS_CHECK(k < nm && q0 < kMini * 32);
                     const Rec64 q = W.rec[k];
                     // pixel centre (k + 0.5, j + 0.5) of the source lane, exact in float64
-                    const double cx = (double)(x0 + (src & 15)) + 0.5;
-                    const double cy = (double)(y0 + 2 * warp + (src >> 4)) + 0.5;
+                    const double cx = (double)(xb + src % kBW) + 0.5;
+                    const double cy = (double)(yb + src / kBW) + 0.5;
                     // power = -0.5 * (a*du*du + c*dv*dv) - b*du*dv   (contributions.py:142-145)
                     const double ddu = __dsub_rn(cx, q.mx);
                     const double ddv = __dsub_rn(cy, q.my);
