@@ -227,6 +227,15 @@ def atomic_peak(acc_bytes):
     return res["16MB_C2"]["f64_rand16"] * 1e9, key, res[key]["f64_rand16"] * 1e9
 
 
+def pipe_peaks():
+    """Measured pipe rates of this B200 (tools/pipe_peak.cu -> profiles/r2_pipe_peak.json):
+    DFMA / FFMA / MUFU.EX2 thread-ops per SM per clock."""
+    p = ROOT / "profiles" / "r2_pipe_peak.json"
+    if not p.exists():
+        return None
+    return json.loads(p.read_text())
+
+
 def cpu_baseline(wl, views_override=None):
     """Oracle (float64 restatement, pinned to the reference) on all host threads."""
     import oracle
@@ -504,6 +513,29 @@ def main():
     clk_summary = clk.summary()
     sm_hz = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
     issue_peak = 148 * 4 * sm_hz  # warp-instructions / s (one issue slot per scheduler per clock)
+    # work-normalised compute roofline, measured this run: exact alpha evaluations
+    # per second of raster time; the FP64 work per evaluation and the warp
+    # instructions per evaluation are properties of this build (ncu, raster_traffic.json)
+    evals_per_launch = iso["exact_evals"] / views_n
+    eval_rate = evals_per_launch / raster_avg_s if raster_avg_s > 0 else None
+    pk = pipe_peaks()
+    compute = None
+    if eval_rate and rec.get("fp64_thread_ops_per_exact_eval"):
+        f64_peak = pk["dfma_per_sm_clk"] * 148 * sm_hz if pk else 64 * 148 * sm_hz
+        f64_ach = eval_rate * rec["fp64_thread_ops_per_exact_eval"]
+        inst_ach = eval_rate * rec["warp_instructions_per_exact_eval"]
+        compute = {
+            "exact_alpha_evals_per_launch": evals_per_launch,
+            "exact_alpha_evals_per_s": eval_rate,
+            "fp64": {"ops_per_exact_eval": rec["fp64_thread_ops_per_exact_eval"],
+                     "achieved_ops_per_s": f64_ach, "peak_ops_per_s": f64_peak,
+                     "frac": f64_ach / f64_peak,
+                     "peak_source": "profiles/r2_pipe_peak.json (tools/pipe_peak.cu, DFMA "
+                                    "thread-ops/SM/clk) x 148 SMs x this run's SM clock"},
+            "issue": {"warp_instructions_per_exact_eval": rec["warp_instructions_per_exact_eval"],
+                      "achieved_per_s": inst_ach, "peak_per_s": issue_peak,
+                      "frac": inst_ach / issue_peak},
+            "per_eval_constants_source": rec.get("source")}
     stage_sum = st["prep_ms"] + st["bin_ms"] + st["raster_ms"]
     line = {
         "metric": "view-pixels/sec of contribution accumulation",
@@ -529,6 +561,7 @@ def main():
                      "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": raster_avg_s * 1e3,
                      "share_of_serial_step": iso["raster_ms"] / iso["gpu_ms"] if iso["gpu_ms"] else None,
                      "timing": "CUDA events around each raster launch on its stream, 1-stream pass",
+                     "compute": compute,
                      "binding": {
                          "resource": "SM warp-instruction issue (not HBM: see DESIGN.md)",
                          "warp_instructions_per_launch": instr,
@@ -546,7 +579,7 @@ def main():
                                         "per warp instruction, L2-resident buffer)",
                          "uniform_random_per_s_at_accumulator_size": atom_sized,
                          "accumulator_size_class": atom_key,
-                         "l2_atomic_alu_pct_of_peak_ncu": rec.get("l2_atomic_alu_pct_of_peak")},
+                         "l2_red_pct_of_peak_ncu": rec.get("l2_red_pct_of_peak")},
                      "warp_efficiency": {
                          "threads_per_inst": rec.get("warp_efficiency_threads_per_inst"),
                          "pred_on_threads_per_inst":
