@@ -336,8 +336,8 @@ def main():
     part = torch.empty(acc.numel() // world, dtype=acc.dtype, device="cuda")
     A_sl = torch.zeros((E, chunk), dtype=torch.float32, device="cuda")
     L_sl = torch.zeros((rows, chunk), dtype=torch.uint8, device="cuda")
-    A_all = torch.empty((world, E, chunk), dtype=torch.float32, device="cuda")
-    L_all = torch.empty((world, rows, chunk), dtype=torch.uint8, device="cuda")
+    A_all = torch.empty(world * E * chunk, dtype=torch.float32, device="cuda")
+    L_all = torch.empty(world * rows * chunk, dtype=torch.uint8, device="cuda")
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 
     def step(timing=False):
@@ -357,10 +357,12 @@ def main():
                                 out_on_device=True, acc_kind=kind)
         _native.assign(None, 0.0, mode, ctx=ctx, on_device_ptr=A_sl.data_ptr(), n=chunk, e=E,
                        out_ptr=L_sl.data_ptr())
-        dist.all_gather_into_tensor(A_all, A_sl, group=group)
-        dist.all_gather_into_tensor(L_all, L_sl, group=group)
-        A32.view(E, N).copy_(A_all.permute(1, 0, 2).reshape(E, world * chunk)[:, :N])
-        out.view(rows, N).copy_(L_all.permute(1, 0, 2).reshape(rows, world * chunk)[:, :N])
+        dist.all_gather_into_tensor(A_all, A_sl.reshape(-1), group=group)
+        dist.all_gather_into_tensor(L_all, L_sl.reshape(-1), group=group)
+        A32.view(E, N).copy_(A_all.view(world, E, chunk).permute(1, 0, 2)
+                             .reshape(E, world * chunk)[:, :N])
+        out.view(rows, N).copy_(L_all.view(world, rows, chunk).permute(1, 0, 2)
+                                .reshape(rows, world * chunk)[:, :N])
         return st
 
     stats = []

@@ -115,12 +115,14 @@ def reduce_scatter_finalize(ctx, acc, n: int, num_objects: int, acc_kind: int, g
     g0, g1 = rank * chunk, min(n, rank * chunk + chunk)
     if g1 > g0:
         with ctx.lock:
-            ctx.set_stream(torch.cuda.current_stream(acc.device).cuda_stream)
+            if acc.is_cuda:
+                ctx.set_stream(torch.cuda.current_stream(acc.device).cuda_stream)
             ctx.reduce_finalize([part.data_ptr()], g0, n, e, g0, g1, sl.data_ptr(), chunk,
                                 out_on_device=True, acc_kind=acc_kind)
-    gathered = torch.empty((world, e, chunk), dtype=torch.float32, device=acc.device)
-    dist.all_gather_into_tensor(gathered, sl, group=group)
-    return gathered.permute(1, 0, 2).reshape(e, world * chunk)[:, :n].contiguous()
+    gathered = torch.empty(world * e * chunk, dtype=torch.float32, device=acc.device)
+    dist.all_gather_into_tensor(gathered, sl.reshape(-1), group=group)
+    return (gathered.view(world, e, chunk).permute(1, 0, 2).reshape(e, world * chunk)[:, :n]
+            .contiguous())
 
 
 def sharded_matrix_device(scene, views, num_objects: int, blend, group, device, acc_kind: int):

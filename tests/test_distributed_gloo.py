@@ -6,6 +6,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch.multiprocessing as mp
 
 import oracle
@@ -105,3 +106,66 @@ def test_two_rank_label_error_agreement(tmp_path):
     msgs = [open(f"{out}.{r}.txt").read() for r in (0, 1)]
     assert msgs[0] == msgs[1]
     assert "view 1: label 5 at pixel (2, 3) exceeds object count 2" in msgs[0]
+
+
+class _HostFinalizeCtx:
+    """CPU stand-in for the library's fs_reduce_finalize (fixed-point parts ->
+    float32 slice), so the reduce-scatter / all-gather reassembly of
+    distributed.reduce_scatter_finalize runs on gloo."""
+
+    def __init__(self):
+        import threading
+        self.lock = threading.Lock()
+
+    def set_stream(self, handle):
+        pass
+
+    def reduce_finalize(self, parts, part_g0, n, e, g0, g1, out_ptr, ld, out_on_device=True,
+                        acc_kind=1):
+        import ctypes
+        rows = g1 - part_g0
+        words = np.ctypeslib.as_array((ctypes.c_uint64 * (rows * e * 2)).from_address(parts[0]))
+        w = words.reshape(rows, e, 2)[g0 - part_g0:]
+        val = ((w[..., 0].astype(object) << 32) + w[..., 1].astype(object))
+        f = np.array([[float(x) * 2.0 ** -59 for x in r] for r in val], np.float64)
+        out = np.ctypeslib.as_array((ctypes.c_float * (e * ld)).from_address(out_ptr)).reshape(e, ld)
+        out[:, :g1 - g0] = f.T.astype(np.float32)
+
+
+def _rs_worker(rank, world, port, out_path, n, e):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_08270_b200 import _native
+    from paper_2409_08270_b200.distributed import alloc_accumulator, reduce_scatter_finalize
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    acc = alloc_accumulator(n, e, world, _native.ACC_FIXED, "cpu")
+    rng = np.random.default_rng(100 + rank)
+    words = acc.view(-1, e, 2)
+    words[:n] = torch.from_numpy(rng.integers(0, 2 ** 40, (n, e, 2), dtype=np.int64))
+    A = reduce_scatter_finalize(_HostFinalizeCtx(), acc, n, e, _native.ACC_FIXED,
+                                dist.group.WORLD, None)
+    np.save(f"{out_path}.{rank}.npy", A.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 7), (3, 10), (2, 1)])
+def test_reduce_scatter_finalize_reassembles_the_matrix(tmp_path, world, n):
+    """Padding to equal Gaussian slices, reduce-scatter of the fixed-point words,
+    per-slice cast and all-gather give every rank the E x N matrix of the summed
+    accumulators (distributed.py; the NCCL path runs the same code on GPUs)."""
+    e = 3
+    port = _free_port()
+    out = str(tmp_path / "A")
+    mp.spawn(_rs_worker, args=(world, port, out, n, e), nprocs=world, join=True)
+    total = np.zeros((n, e, 2), dtype=object)
+    for r in range(world):
+        total += np.random.default_rng(100 + r).integers(0, 2 ** 40, (n, e, 2),
+                                                         dtype=np.int64).astype(object)
+    val = (total[..., 0] << 32) + total[..., 1]
+    expect = np.array([[float(x) * 2.0 ** -59 for x in row] for row in val]).T.astype(np.float32)
+    for r in range(world):
+        got = np.load(f"{out}.{r}.npy")
+        assert got.shape == (e, n)
+        assert np.array_equal(got, expect)
