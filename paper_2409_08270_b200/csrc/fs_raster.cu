@@ -391,7 +391,11 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                     const double t2 = __dmul_rn(__dmul_rn(q.c, ddv), ddv);
                     const double t3 = __dmul_rn(__dmul_rn(q.b, ddu), ddv);
                     const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), t3);
+#ifdef FS_ABLATE_EXP  // timing-only ablation: wrong results
+                    const double alpha = __dmul_rn(q.o, (double)__expf((float)power));
+#else
                     const double alpha = __dmul_rn(q.o, exp(power));  // :146-147
+#endif
                     const double ac = alpha < kAlphaClamp ? alpha : kAlphaClamp;
                     // below the floor: no weight, no transmittance update (:148-149) --
                     // exactly what alpha = 0 does in B (w = 0 * T, T * (1 - 0) = T)
