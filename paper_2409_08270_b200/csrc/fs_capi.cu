@@ -1213,6 +1213,11 @@ int fs_accumulate_multi(fs_context* const* ctxs, int n_ctx, int n_views, const f
         memset(stats, 0, sizeof(*stats));
         stats->label_error_view = -1;
     }
+    for (int i = 0; i < n_ctx; ++i)
+        for (int j = 0; j < i; ++j)
+            if (ctxs[i] == ctxs[j])
+                return fail(FS_EINVAL, "fs_accumulate_multi: context %d is listed twice (one host "
+                                       "thread per context: use distinct contexts)", i);
     int rc;
     ViewPlan plan;
     if ((rc = plan_views(n_views, cams, masks, num_objects, acc_kind, plan))) return rc;
@@ -1309,6 +1314,10 @@ int fs_finalize_multi(fs_context* const* ctxs, int n_ctx, int acc_kind, void* co
         return fail(FS_EINVAL, "scene assignment requires E>=2, got E=%d", num_objects);
     if (mode != -1 && !(gamma >= -1.0f && gamma <= 1.0f))
         return fail(FS_EINVAL, "gamma must lie in [-1, 1], got %g", (double)gamma);
+    for (int i = 0; i < n_ctx; ++i)
+        for (int j = 0; j < i; ++j)
+            if (ctxs[i] == ctxs[j])
+                return fail(FS_EINVAL, "fs_finalize_multi: context %d is listed twice", i);
     if (n <= 0 || num_objects <= 0) return FS_OK;
     if (!out || (mode != -1 && !labels)) return fail(FS_EINVAL, "fs_finalize_multi: NULL output");
     // Column slice i of A is reduced, cast and argmax'ed on context i, reading

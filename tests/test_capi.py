@@ -61,3 +61,23 @@ def test_compute_without_gpu_fails_loudly(lib):
     from paper_2409_08270_b200 import _native
     with pytest.raises(_native.NativeUnavailable):
         _native.Context(0)
+
+
+def test_multi_entry_points_validate_before_touching_contexts(lib):
+    """fs_accumulate_multi / fs_finalize_multi reject a context listed twice (one host
+    thread per context) and bad counts before dereferencing anything (no GPU needed)."""
+    import ctypes
+    from paper_2409_08270_b200 import _native
+    dummy = ctypes.c_void_p(0x1000)
+    two = (ctypes.c_void_p * 2)(dummy, dummy)
+    accs = (ctypes.c_void_p * 2)(ctypes.c_void_p(0x2000), ctypes.c_void_p(0x3000))
+    rc = lib.fs_accumulate_multi(two, 2, 0, None, None, 2, 1 / 255, 1e-4, _native.ACC_FIXED,
+                                 accs, None, None)
+    assert rc == _native.FS_EINVAL and b"listed twice" in lib.fs_last_error()
+    rc = lib.fs_finalize_multi(two, 2, _native.ACC_FIXED, accs, 10, 2, None, 0.0, -1, None)
+    assert rc == _native.FS_EINVAL and b"listed twice" in lib.fs_last_error()
+    rc = lib.fs_accumulate_multi(two, 0, 0, None, None, 2, 1 / 255, 1e-4, _native.ACC_FIXED,
+                                 accs, None, None)
+    assert rc == _native.FS_EINVAL
+    rc = lib.fs_finalize_multi(two, 1, 7, accs, 10, 2, None, 0.0, -1, None)
+    assert rc == _native.FS_EINVAL and b"accumulator kind" in lib.fs_last_error()
