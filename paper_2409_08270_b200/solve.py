@@ -54,11 +54,14 @@ class LabelSolver:
 
     def accumulate(self, views: Sequence, num_objects: int,
                    blend: BlendConfig = DEFAULT_BLEND, download: bool = True,
-                   process_group=None):
+                   process_group=None, devices: Optional[Sequence[int]] = None):
         """Accumulate A on the device (and keep it there); optionally view-sharded.
 
         With ``process_group`` every rank validates all views (same errors on
-        every rank), accumulates its shard and one all-reduce joins them.
+        every rank), accumulates its shard, and a reduce-scatter + all-gather
+        leave the full matrix on every rank's device.  With ``devices`` the
+        views are split over those GPUs from this process (multidevice.py) and
+        the matrix is then kept on this solver's device for the re-assignments.
         """
         views = list(views)
         e = int(num_objects)
@@ -69,6 +72,15 @@ class LabelSolver:
             check_shapes(views, e)
         ctx = self.ctx
         kind = acc_kind_of(self.deterministic, blend)
+        if devices is not None and n:
+            from .multidevice import solve_multi
+            values, _ = solve_multi(self.scene, views, e, blend, devices, kind)
+            with ctx.lock:
+                A, out = self._buffers(e, n)
+                A.from_host(values)
+                self._A_cur, self._out_cur = A, out
+            self.num_objects = e
+            return ContributionMatrix(values=values) if download else None
         if process_group is not None and n:
             # reduce-scatter + sliced cast + all-gather (distributed.py); the
             # gathered E x N matrix stays on this rank's device

@@ -205,3 +205,22 @@ def test_assign_does_not_wait_for_a_running_accumulation():
     assert all(np.array_equal(d, oracle.assign_binary(A, 0.25)) for d in done)
     # every assign finished well before the accumulation did
     assert max(ends) < t["acc1"], (max(ends) - t["acc0"], t["acc1"] - t["acc0"])
+
+
+def test_multi_device_exact_blend_and_resident_solver():
+    """devices= with EXACT_BLEND (float64 accumulators, reduced in part order by the
+    finalize) and LabelSolver.accumulate(devices=...) followed by device re-assigns."""
+    from paper_2409_08270_b200 import EXACT_BLEND, LabelSolver
+    wl = _workload(seed=29, n=8000, views=4, w=96, h=80, e=3)
+    one = accumulate_contributions(wl.scene, wl.pairs(), 3, EXACT_BLEND).values
+    two = accumulate_contributions(wl.scene, wl.pairs(), 3, EXACT_BLEND, devices=[0, 0]).values
+    np.testing.assert_allclose(two, one, rtol=1e-6, atol=1e-12)
+    cams = [oracle.camera_of(v) for v in wl.views]
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, cams, list(wl.masks), 3, 0.0, 0.0, threads=4)
+    np.testing.assert_allclose(two, ref, rtol=1e-6, atol=1e-9)
+    s = LabelSolver(wl.scene)
+    M = s.accumulate(wl.pairs(), 3, devices=[0, 0])
+    assert np.array_equal(M.values, accumulate_contributions(wl.scene, wl.pairs(), 3).values)
+    for g in (-0.2, 0.0, 0.4):
+        assert np.array_equal(s.assign(g, "scene").membership, oracle.assign_scene(M.values, g))
