@@ -599,6 +599,16 @@ def main():
         # the --impl reference arm, which repeats it warmup + steps times)
         k = args.cpu_views or 3 * (os.cpu_count() or 1)
         line["cpu_baseline"] = {k2: v for k2, v in cpu_baseline(wl, k).items() if k2 != "seconds"}
+        ref_np = ROOT / "profiles" / "r2_reference_numpy_c2.json"
+        if args.config == "C2" and ref_np.exists():
+            # the reference itself (numpy) cannot run on the GPU box (/root/reference is not
+            # there): its C2 per-view rate, measured in the build container, for context
+            r = json.loads(ref_np.read_text())
+            line["cpu_baseline"]["reference_numpy_build_host"] = {
+                "view_px_per_s_one_core": r["single_process_view_px_per_s"],
+                "view_px_per_s_parallel": r["parallel_view_px_per_s"],
+                "processes": r["processes"], "source": "profiles/r2_reference_numpy_c2.json",
+                "note": "tools/time_reference_numpy.py, build container, not the GPU box"}
     print(json.dumps(line), flush=True)
     if group is not None:
         dist.destroy_process_group()
