@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                 }
                 __syncwarp();
                 // ---- B: every lane walks its own candidates in list order ----
-                {
+                if (kRender || grouped) {
                     unsigned int mm = mine;
                     while (mm) {
                         const int k = __ffs(mm) - 1;
@@ -411,30 +411,50 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         double w = 0.0;
                         if (active) {
                             const double alpha = myval[k * kRowStride + lane];  // 0: below floor
-                            {
-                                w = __dmul_rn(alpha, T);                     // :150
-                                T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
-                                active = !(T < tf_eff);                      // :156-157
-                                if (kRender) {
-                                    // rasterizer.py:184-191, summed in list order per pixel
-                                    const unsigned int g = W.gid[(head + k) & (kRing - 1)];
-                                    const double z = depth_of_key(a.sort.keys.k64[g]);
-                                    r_acc = __dadd_rn(r_acc, w);
-                                    d_acc = __dadd_rn(d_acc, __dmul_rn(z, w));
+                            w = __dmul_rn(alpha, T);                     // :150
+                            T = __dmul_rn(T, __dsub_rn(1.0, alpha));     // :155
+                            active = !(T < tf_eff);                      // :156-157
+                            if (kRender) {
+                                // rasterizer.py:184-191, summed in list order per pixel
+                                const unsigned int g = W.gid[(head + k) & (kRing - 1)];
+                                const double z = depth_of_key(a.sort.keys.k64[g]);
+                                r_acc = __dadd_rn(r_acc, w);
+                                d_acc = __dadd_rn(d_acc, __dmul_rn(z, w));
 #pragma unroll
-                                    for (int ch = 0; ch < 3; ++ch)
-                                        if (ch < n_ch)
-                                            v_acc[ch] = __dadd_rn(
-                                                v_acc[ch],
-                                                __dmul_rn(w, a.render.channel[(size_t)g * n_ch + ch]));
-                                }
+                                for (int ch = 0; ch < 3; ++ch)
+                                    if (ch < n_ch)
+                                        v_acc[ch] = __dadd_rn(
+                                            v_acc[ch],
+                                            __dmul_rn(w, a.render.channel[(size_t)g * n_ch + ch]));
                             }
                         }
                         myval[k * kRowStride + lane] = w;
                     }
+                } else {
+                    // ungrouped warp (more than kMaxGroups labels, e.g. iid masks): every
+                    // contributing pixel adds its own weight, issued straight from the walk
+                    unsigned int mm = active ? mine : 0u;
+                    while (mm) {
+                        const int k = __ffs(mm) - 1;
+                        mm &= mm - 1u;
+                        const double alpha = myval[k * kRowStride + lane];  // 0: below floor
+                        const double w = __dmul_rn(alpha, T);              // :150
+                        T = __dmul_rn(T, __dsub_rn(1.0, alpha));           // :155
+                        if (w > 0.0 && lbl_ok) {
+                            FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians);
+                            acc_add<kFixed>(acc, acc_fx,
+                                            (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label,
+                                            w);
+                            ++atom;
+                        }
+                        if (T < tf_eff) {                                   // :156-157
+                            active = false;
+                            break;
+                        }
+                    }
                 }
                 __syncwarp();
-                // ---- C: aggregation + float64 atomics ----
+                // ---- C: aggregation + float64 atomics (ungrouped warps added in B) ----
                 if (kRender) {
                     // no scatter: the pixel keeps its own sums
                 } else if (grouped) {
@@ -456,20 +476,6 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                             FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians);
                             acc_add<kFixed>(acc, acc_fx,
                                             (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + gl, v);
-                            ++atom;
-                        }
-                    }
-                } else if (lbl_ok) {
-                    unsigned int mm = mine;
-                    while (mm) {
-                        const int k = __ffs(mm) - 1;
-                        mm &= mm - 1u;
-                        const double w = myval[k * kRowStride + lane];
-                        if (w > 0.0) {
-                            FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians &&
-                                     label < n_obj);
-                            acc_add<kFixed>(acc, acc_fx,
-                                            (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label, w);
                             ++atom;
                         }
                     }
