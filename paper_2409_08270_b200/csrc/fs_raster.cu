@@ -187,6 +187,7 @@ __device__ __forceinline__ unsigned int block_candidates(const Rec32& s, float v
             const float ctr = base - binv * dv;
             const float half = sq * inv_a;
             const float eps = 0.03f + 1e-5f * fabsf(ctr);
+#ifdef FS_SCREEN_FLOAT_CLAMP
             const float lo = ceilf(ctr - half - eps) - xf;
             const float hi = floorf(ctr + half + eps) - xf;
             if (!(hi < 0.0f || lo > (float)(kBW - 1) || lo > hi)) {
@@ -194,6 +195,13 @@ __device__ __forceinline__ unsigned int block_candidates(const Rec32& s, float v
                 const int c1 = hi > (float)(kBW - 1) ? kBW - 1 : (int)hi;
                 cand |= ((2u << c1) - (1u << c0)) << (r * kBW);
             }
+#else
+            // the same interval with rounding conversions and integer clamps; empty
+            // when c1 < c0 (bounded to +-1e9 first so the block offset cannot overflow)
+            const int c0 = max(__float2int_ru(fminf(ctr - half - eps, 1.0e9f)) - xb, 0);
+            const int c1 = min(__float2int_rd(fmaxf(ctr + half + eps, -1.0e9f)) - xb, kBW - 1);
+            if (c0 <= c1) cand |= ((2u << c1) - (1u << c0)) << (r * kBW);
+#endif
         }
     }
     return cand;
