@@ -206,6 +206,14 @@ class ClockSampler:
                 "samples": len(sm), "window": window}
 
 
+def workload_config(args, wl):
+    """The workload's `config` object -- identical in both arms (--impl ours / reference)."""
+    return {"workload": CONFIG_TEXT[args.config] + (" (iid labels)" if args.iid else ""),
+            "name": args.config + ("-iid" if args.iid else ""),
+            "gaussians": len(wl.scene), "views": len(wl.views),
+            "image": f"{wl.views[0].width}x{wl.views[0].height}", "num_objects": wl.num_objects}
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -279,8 +287,7 @@ def run_reference(args, rank, world):
         "value": value, "unit": "view-px/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_TEXT[args.config], "name": args.config,
-                   "sample_views": k, "gaussians": len(wl.scene)},
+        "config": workload_config(args, wl),
         "cpu_baseline": {"value": value, "unit": "view-px/s", "cores": r["cores"], "kind": "port",
                          "sample": r["sample"]},
         "e2e": {"value": value, "unit": "view-px/s", "h2d_bytes_per_step": 0,
@@ -544,16 +551,14 @@ def main():
         "value": value, "unit": "view-px/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": s_per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_TEXT[args.config] + (" (iid labels)" if args.iid else ""),
-                   "name": args.config + ("-iid" if args.iid else ""),
-                   "gaussians": N, "views": len(wl.views),
-                   "image": f"{wl.views[0].width}x{wl.views[0].height}", "num_objects": E,
-                   "parallelism": f"views sharded over {world} GPU(s)" + (
-                       ", reduce-scatter + sliced cast/argmax + all-gather (NCCL)" if world > 1 else ""),
-                   "accumulator": "fixed-point (deterministic)" if kind == _native.ACC_FIXED
-                   else "float64 atomics",
-                   "l2": "inputs larger than L2 (masks %.0f MB + scene %.0f MB)" % (
-                       wl.masks.nbytes / 1e6, N * 88 / 1e6)},
+        "config": workload_config(args, wl),
+        "run": {"parallelism": f"views sharded over {world} GPU(s)" + (
+                    ", reduce-scatter + sliced cast/argmax + all-gather (NCCL)" if world > 1 else ""),
+                "accumulator": "fixed-point (deterministic)" if kind == _native.ACC_FIXED
+                else "float64 atomics",
+                "streams": args.streams,
+                "l2": "inputs larger than L2 between steps (masks %.0f MB + scene %.0f MB)" % (
+                    wl.masks.nbytes / 1e6, N * 88 / 1e6)},
         "solve_s_per_scene": s_per_step,
         "e2e": e2e,
         "gpu_launches": int(sum(s["launches"] for s in stats) + 2 * args.steps),
