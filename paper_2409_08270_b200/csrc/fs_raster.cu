@@ -58,7 +58,6 @@ constexpr int kMaxGroups = 4;   // label groups per warp reduced before the atom
 #endif
 constexpr int kBW = FS_BLOCK_W;
 constexpr int kBH = 32 / kBW;
-constexpr unsigned int kRowMask = (kBW == 32) ? 0xffffffffu : ((1u << kBW) - 1u);
 static_assert(kBW == 8 || kBW == 16, "warp pixel blocks are 2 x 16 or 4 x 8");
 
 struct WarpSmem {
@@ -133,40 +132,14 @@ __device__ __forceinline__ unsigned int warp_transpose16x32(unsigned int x, int 
     return x;
 }
 
-// Candidate columns of one pixel row for one splat: the pixels whose float32
-// power clears the conservative cut, from the roots of the quadratic
-//   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
-// (widened by float32 rounding margins).  Returns a kBW-bit column mask of the
-// columns x0 .. x0 + kBW - 1.
-__device__ __forceinline__ unsigned int row_candidates(const Rec32& s, float v_centre, int x0,
-                                                       float inv_a) {
-    if (!(s.cut > -INFINITY)) return kRowMask;  // exact blend: no alpha floor
-    const float dv = v_centre - s.my;
-    const float Q = -2.0f * s.cut;
-    const float detc = s.a * s.c - s.b * s.b;
-    const float t1 = s.a * Q, t2 = detc * dv * dv;
-    const float D = t1 - t2 + 1e-5f * (fabsf(t1) + fabsf(t2)) + 1e-20f;
-    if (!(D >= 0.0f)) return 0u;
-    // approximate square root (MUFU; inv_a likewise, once per splat by the caller):
-    // ~1e-7 relative, far inside the 0.03 px interval margin below
-    float sq;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(D));
-    const float ctr = s.mx - 0.5f - s.b * dv * inv_a;
-    const float half = sq * inv_a;
-    const float eps = 0.03f + 1e-5f * fabsf(ctr);
-    const float lo = ceilf(ctr - half - eps) - (float)x0;
-    const float hi = floorf(ctr + half + eps) - (float)x0;
-    if (hi < 0.0f || lo > (float)(kBW - 1) || lo > hi) return 0u;
-    const int c0 = lo < 0.0f ? 0 : (int)lo;
-    const int c1 = hi > (float)(kBW - 1) ? kBW - 1 : (int)hi;
-    return (2u << c1) - (1u << c0);
-}
-
 // Candidate mask of a whole kBH x kBW block (bit r * kBW + c = pixel (xb + c,
-// v_lo - 0.5 + r)): row_candidates for every row with the splat's per-row
-// invariants (1/a, Q, det, a*Q) computed once.  Same float32 expressions and
-// margins as row_candidates, up to float32 rounding (~1e-6 px against the 0.03 px
-// interval margin).
+// v_lo - 0.5 + r)): per row, the pixels whose float32 power clears the
+// conservative cut, from the roots of the quadratic
+//   a du^2 + 2 b dv du + c dv^2 <= Q,   Q = -2 * cut
+// widened by float32 rounding margins (1e-5 relative on the discriminant, 0.03 px
+// + 1e-5 relative on the interval ends); the splat's per-row invariants (1/a, Q,
+// det, a*Q) are computed once.  sqrt / rcp are the MUFU approximations (~1e-7
+// relative, far inside the margins).
 __device__ __forceinline__ unsigned int block_candidates(const Rec32& s, float v_lo, int xb) {
     if (!(s.cut > -INFINITY)) return 0xffffffffu;  // exact blend: no alpha floor
     float inv_a;
@@ -174,7 +147,7 @@ __device__ __forceinline__ unsigned int block_candidates(const Rec32& s, float v
     const float Q = -2.0f * s.cut;
     const float detc = s.a * s.c - s.b * s.b;
     const float t1 = s.a * Q, at1 = fabsf(t1);
-    const float base = s.mx - 0.5f, binv = s.b * inv_a, xf = (float)xb;
+    const float base = s.mx - 0.5f, binv = s.b * inv_a;
     unsigned int cand = 0;
 #pragma unroll
     for (int r = 0; r < kBH; ++r) {
@@ -187,21 +160,11 @@ __device__ __forceinline__ unsigned int block_candidates(const Rec32& s, float v
             const float ctr = base - binv * dv;
             const float half = sq * inv_a;
             const float eps = 0.03f + 1e-5f * fabsf(ctr);
-#ifdef FS_SCREEN_FLOAT_CLAMP
-            const float lo = ceilf(ctr - half - eps) - xf;
-            const float hi = floorf(ctr + half + eps) - xf;
-            if (!(hi < 0.0f || lo > (float)(kBW - 1) || lo > hi)) {
-                const int c0 = lo < 0.0f ? 0 : (int)lo;
-                const int c1 = hi > (float)(kBW - 1) ? kBW - 1 : (int)hi;
-                cand |= ((2u << c1) - (1u << c0)) << (r * kBW);
-            }
-#else
             // the same interval with rounding conversions and integer clamps; empty
             // when c1 < c0 (bounded to +-1e9 first so the block offset cannot overflow)
             const int c0 = max(__float2int_ru(fminf(ctr - half - eps, 1.0e9f)) - xb, 0);
             const int c1 = min(__float2int_rd(fmaxf(ctr + half + eps, -1.0e9f)) - xb, kBW - 1);
             if (c0 <= c1) cand |= ((2u << c1) - (1u << c0)) << (r * kBW);
-#endif
         }
     }
     return cand;
@@ -312,15 +275,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         if (idx < n_list) {
             if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
                   v_lo > s.my + s.hy)) {
-#ifdef FS_ROW_SCREEN
-                float inv_a;  // shared by the rows (one MUFU)
-                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_a) : "f"(s.a));
-#pragma unroll
-                for (int r = 0; r < kBH; ++r)
-                    cand |= row_candidates(s, v_lo + (float)r, xb, inv_a) << (r * kBW);
-#else
                 cand = block_candidates(s, v_lo, xb);
-#endif
             }
         }
         steps += min(32u, n_list - c);
@@ -331,11 +286,6 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
             W.cm[slot] = cand;
             W.gid[slot] = g;
-#ifdef FS_PREFETCH_REC64
-            // the hit's float64 record is read when its mini-batch starts: start the
-            // L2 -> L1 move now so that load does not wait a full L2 round trip
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.r64 + g));
-#endif
         }
         cnt += __popc(bal);
         __syncwarp();
@@ -399,11 +349,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                     const double t2 = __dmul_rn(__dmul_rn(q.c, ddv), ddv);
                     const double t3 = __dmul_rn(__dmul_rn(q.b, ddu), ddv);
                     const double power = __dsub_rn(__dmul_rn(-0.5, __dadd_rn(t1, t2)), t3);
-#ifdef FS_ABLATE_EXP  // timing-only ablation: wrong results
-                    const double alpha = __dmul_rn(q.o, (double)__expf((float)power));
-#else
                     const double alpha = __dmul_rn(q.o, exp(power));  // :146-147
-#endif
                     const double ac = alpha < kAlphaClamp ? alpha : kAlphaClamp;
                     // below the floor: no weight, no transmittance update (:148-149) --
                     // exactly what alpha = 0 does in B (w = 0 * T, T * (1 - 0) = T)
