@@ -317,6 +317,9 @@ def main():
     from paper_2409_08270_b200 import _native, solve
     from paper_2409_08270_b200.distributed import alloc_accumulator, padded_rows, shard_views
 
+    if local >= torch.cuda.device_count():
+        sys.exit(f"bench.py: rank {rank} needs cuda:{local} but only "
+                 f"{torch.cuda.device_count()} GPU(s) are visible (--gpus {args.gpus})")
     torch.cuda.set_device(local)
     group = None
     if world > 1 or "RANK" in os.environ:  # torchrun: NCCL path even for one rank
