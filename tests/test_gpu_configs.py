@@ -105,3 +105,14 @@ def test_iid_label_worst_case(cfg):
 def test_c2_binary_full_resolution():
     """C2: 1M Gaussians, 1008x756, binary, 8 views."""
     _parity("C2_8views", synth.config_workload("C2", n_views=8), [0.0, 0.5])
+
+
+def test_c2_full_200_views():
+    """C2 at its full size: 1M Gaussians, all 200 views of 1008x756 (the bench
+    workload itself), against the oracle on all host threads."""
+    _parity("C2_full", synth.config_workload("C2"), [0.0])
+
+
+def test_c5_full_100_views():
+    """C5 at its full size: 100 noisy views, gamma in {0, 0.2, 0.5}."""
+    _parity("C5_full", synth.config_workload("C5"), [0.0, 0.2, 0.5])
