@@ -116,3 +116,8 @@ def test_c2_full_200_views():
 def test_c5_full_100_views():
     """C5 at its full size: 100 noisy views, gamma in {0, 0.2, 0.5}."""
     _parity("C5_full", synth.config_workload("C5"), [0.0, 0.2, 0.5])
+
+
+def test_c3_full_200_views():
+    """C3 at its full size: 1M Gaussians, 200 views, L=32 (128 MB matrix)."""
+    _parity("C3_full", synth.config_workload("C3"), [0.0])
