@@ -39,17 +39,16 @@ def load_mask_png(path) -> np.ndarray:
 
     Grayscale 8/16-bit PNGs -- the wire format -- are decoded natively
     (``fs_decode_mask_png``: zlib inflate + row unfiltering in C++, no GIL);
-    every other flavour goes through Pillow exactly as the reference does.
+    every other flavour (palette, interlaced, ...) goes through Pillow exactly as
+    the reference does.  No silent fallback: without the library this raises
+    ``NativeUnavailable`` like every other entry point.
     """
     from PIL import Image
 
     from . import _native
 
     data = Path(path).read_bytes()
-    try:
-        arr = _native.decode_mask_png(data)
-    except _native.NativeUnavailable:
-        arr = None
+    arr = _native.decode_mask_png(data)  # raises NativeUnavailable without the library
     if arr is not None:
         return arr
     with Image.open(path) as im:
