@@ -224,3 +224,15 @@ def test_multi_device_exact_blend_and_resident_solver():
     assert np.array_equal(M.values, accumulate_contributions(wl.scene, wl.pairs(), 3).values)
     for g in (-0.2, 0.0, 0.4):
         assert np.array_equal(s.assign(g, "scene").membership, oracle.assign_scene(M.values, g))
+
+
+@pytest.mark.parametrize("e", [9, 40])
+def test_multi_device_large_e_tile_finalize(e):
+    """E > 8 takes the 32 x 32 transposing finalize: summed over three contexts'
+    accumulators (devices=[0, 0, 0]) it must equal the single-GPU matrix, labels too."""
+    wl = _workload(seed=30 + e, n=33333, views=5, w=160, h=128, e=e)
+    M1, a1 = solve(wl.scene, wl.pairs(), e, 0.1, "scene")
+    M3, a3 = solve(wl.scene, wl.pairs(), e, 0.1, "scene", devices=[0, 0, 0])
+    assert np.array_equal(M1.values, M3.values)
+    assert np.array_equal(a1.membership, a3.membership)
+    np.testing.assert_allclose(M3.values, _oracle_A(wl), rtol=1e-6, atol=1e-9)
