@@ -13,8 +13,11 @@
  *   - float64 host arrays are C-contiguous numpy layouts (N x 3 means,
  *     N x 4 unit quaternions (w, x, y, z), N x 3 scales, N opacities);
  *   - float32 matrices are E x N row-major (ContributionMatrix.values layout,
- *     contributions.py:52-55); the float64 accumulator of fs_accumulate is
- *     N x E (Gaussian-major) and fs_finalize converts between the two;
+ *     contributions.py:52-55); the accumulator of fs_accumulate is N x E
+ *     (Gaussian-major; FS_ACC_FIXED or FS_ACC_F64 entries) and the finalize
+ *     entry points convert between the two;
+ *   - no entry point synchronises the whole device: work is ordered after the
+ *     caller's stream (fs_set_stream) and complete when the call returns;
  *   - "device" pointers are CUDA device addresses on the context's device.
  */
 #ifndef FLASHSPLAT_B200_H
