@@ -125,6 +125,11 @@ int fs_set_timing(fs_context *ctx, int enable);
 int fs_set_scene(fs_context *ctx, int64_t n, const double *means, const double *quats,
                  const double *scales, const double *opacities);
 
+/* The resident scene of src (set by fs_set_scene / fs_set_scene_ply) copied
+ * into dst device to device -- over NVLink when they sit on different GPUs --
+ * so a multi-GPU solve reads the host scene once instead of once per GPU. */
+int fs_copy_scene(fs_context *dst, const fs_context *src);
+
 /* load_scene_ply (ply.py:63-106) + GaussianScene (scene.py:71-110) on the
  * device: verts is the checkpoint's binary_little_endian
  * vertex block as stored in the file -- n records of stride_floats float32 --

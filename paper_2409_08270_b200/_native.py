@@ -37,7 +37,8 @@ EXPORTS = (
     "fs_last_error", "fs_version", "fs_create", "fs_destroy", "fs_device_count",
     "fs_device_alloc", "fs_device_free", "fs_memset_zero", "fs_copy_to_device",
     "fs_copy_to_host", "fs_synchronize", "fs_set_stream", "fs_host_alloc", "fs_host_free",
-    "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_set_scene_ply", "fs_project", "fs_bin", "fs_bin_splats",
+    "fs_host_pinned", "fs_set_timing", "fs_set_scene", "fs_set_scene_ply", "fs_copy_scene",
+    "fs_project", "fs_bin", "fs_bin_splats",
     "fs_accumulate", "fs_accumulate_multi", "fs_finalize", "fs_reduce_finalize",
     "fs_enable_peer_access", "fs_finalize_multi", "fs_assign", "fs_member_counts", "fs_render",
     "fs_render_splats", "fs_render_mask", "fs_decode_mask_png",
@@ -116,6 +117,7 @@ def load() -> ctypes.CDLL:
             "fs_set_timing": ([P, I], I),
             "fs_set_scene": ([P, I64, P, P, P, P], I),
             "fs_set_scene_ply": ([P, I64, P, I, P, P, P], I),
+            "fs_copy_scene": ([P, P], I),
             "fs_project": ([P, P, P, P, P, P, P, P], I),
             "fs_bin": ([P, P, P, P, I64, ctypes.POINTER(I64)], I),
             "fs_bin_splats": ([P, I64, P, P, P, P, I, I, P, P, I64, ctypes.POINTER(I64)], I),
@@ -270,6 +272,16 @@ class Context:
         self._scene_key = key
         self._scene_ref = scene  # keep the id() stable while cached
         self.n = len(scene)
+
+    def copy_scene_from(self, src: "Context") -> None:
+        """fs_copy_scene: take src's resident scene (device to device / NVLink)."""
+        if src is self:
+            return
+        self._scene_key = None
+        _check(load().fs_copy_scene(self.handle, src.handle))
+        self._scene_key = src._scene_key
+        self._scene_ref = getattr(src, "_scene_ref", None)
+        self.n = src.n
 
     def set_scene_ply(self, scene, params: np.ndarray = None) -> np.ndarray:
         """fs_set_scene_ply: a PlyScene's float32 records -> the resident scene

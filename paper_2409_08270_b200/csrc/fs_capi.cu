@@ -941,6 +941,40 @@ int fs_set_timing(fs_context* ctx, int enable) {
     return FS_OK;
 }
 
+int fs_copy_scene(fs_context* dst, const fs_context* src) {
+    Range nvtx_range("fs_copy_scene");
+    if (!dst || !src) return fail(FS_EINVAL, "fs_copy_scene: NULL context");
+    if (dst == src) return FS_OK;
+    const long long n = src->n;
+    CK(cudaSetDevice(dst->device));
+    int rc;
+    if ((rc = order_after_caller(dst))) return rc;
+    if (n > dst->scene_cap) {
+        if ((rc = dev_alloc(&dst->mx, n)) || (rc = dev_alloc(&dst->my, n)) ||
+            (rc = dev_alloc(&dst->mz, n)) || (rc = dev_alloc(&dst->sig, 6 * (size_t)n)) ||
+            (rc = dev_alloc(&dst->opac, n)) || (rc = dev_alloc(&dst->up_means, 3 * (size_t)n)) ||
+            (rc = dev_alloc(&dst->up_quats, 4 * (size_t)n)) ||
+            (rc = dev_alloc(&dst->up_scales, 3 * (size_t)n)))
+            return rc;
+        dst->scene_cap = n;
+    }
+    dst->n = 0;
+    if (n > 0) {
+        // the source is resident (its setup call host-synchronised); device -> device over
+        // NVLink when the contexts sit on different GPUs
+        cudaStream_t st = dst->work[0].stream;
+        const double* s_arr[5] = {src->mx, src->my, src->mz, src->sig, src->opac};
+        double* d_arr[5] = {dst->mx, dst->my, dst->mz, dst->sig, dst->opac};
+        const size_t cnt[5] = {(size_t)n, (size_t)n, (size_t)n, 6 * (size_t)n, (size_t)n};
+        for (int k = 0; k < 5; ++k)
+            CK(cudaMemcpyPeerAsync(d_arr[k], dst->device, s_arr[k], src->device,
+                                   sizeof(double) * cnt[k], st));
+        CK(cudaStreamSynchronize(st));
+    }
+    dst->n = n;
+    return FS_OK;
+}
+
 int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* quats,
                  const double* scales, const double* opacities) {
     Range nvtx_range("fs_set_scene");

@@ -5,8 +5,9 @@ accumulate call at :104) and the service (service.py:56-66) -- run in one
 process, so a torchrun-only multi-GPU path never reaches them.  This path
 does, from one process:
 
-* one library context (streams + workspaces) per GPU, the same scene
-  uploaded to each (uploads run in parallel: ctypes drops the GIL);
+* one library context (streams + workspaces) per GPU; the host scene is
+  uploaded to the first and copied device to device to the others
+  (``fs_copy_scene``, NVLink peer copies), so it crosses PCIe once;
 * ``fs_accumulate_multi``: one native host thread per GPU pops views from a
   shared queue whenever one of its streams frees up, so faster GPUs take
   more views (A is additive over views, contributions.py:103-116);
@@ -67,8 +68,13 @@ def solve_multi(scene, views: Sequence, num_objects: int, blend, devices: Sequen
     for c in locks:
         c.lock.acquire()
     try:
+        # the host scene crosses PCIe once: the first GPU uploads it, the others copy
+        # the resident arrays device to device (NVLink peer copies between GPUs)
+        ctxs[0].set_scene(scene)
         with ThreadPoolExecutor(len(ctxs)) as pool:
-            list(pool.map(lambda c: c.set_scene(scene), ctxs))
+            list(pool.map(lambda c: c.copy_scene_from(ctxs[0])
+                          if c._scene_key != ctxs[0]._scene_key or c._scene_key is None else None,
+                          ctxs[1:]))
             accs = list(pool.map(lambda c: c.acc_buffer(e, n, acc_kind, role="acc_multi").zero(),
                                  ctxs))
         try:
