@@ -119,3 +119,19 @@ def test_device_load_errors_match_host_loader(tmp_path, edits, message):
     # the failed upload leaves no scene resident: a good checkpoint loads afterwards
     good = _write(tmp_path, "good", c["ply"])
     assert len(load_scene_ply(good, device=0)) == len(c["means"])
+
+
+def test_device_loaded_scene_on_several_contexts(tmp_path):
+    """A PlyScene resident on one context reaches the others by fs_copy_scene
+    (devices=[0, 0]): same matrix and labels as the single-context solve."""
+    c = PLY["plain"]
+    dev = load_scene_ply(_write(tmp_path, "m", c["ply"]), device=0)
+    cams = [CameraView(view_id=i, width=128, height=96, fx=80.0, fy=80.0, cx=64.5, cy=48.5 - 2 * i,
+                       world_to_camera=np.eye(4), near_clip=0.01) for i in range(4)]
+    rng = np.random.default_rng(6)
+    pairs = [(v, fs.LabelMask(v.view_id, rng.integers(0, 2, (96, 128)).astype(np.uint16)))
+             for v in cams]
+    M1, a1 = solve(dev, pairs, 2, 0.0, "binary")
+    M2, a2 = solve(dev, pairs, 2, 0.0, "binary", devices=[0, 0])
+    assert np.array_equal(M1.values, M2.values) and np.array_equal(a1.labels, a2.labels)
+    assert M1.values.sum() > 0
