@@ -236,3 +236,32 @@ def test_multi_device_large_e_tile_finalize(e):
     assert np.array_equal(M1.values, M3.values)
     assert np.array_equal(a1.membership, a3.membership)
     np.testing.assert_allclose(M3.values, _oracle_A(wl), rtol=1e-6, atol=1e-9)
+
+
+def test_multi_device_ragged_views_and_empty_masks():
+    """Views of different sizes (edge tiles, a 1x1 view), an all-background mask and a
+    view that sees nothing, split over two contexts: equal to one context, bit for bit,
+    and to the oracle."""
+    from paper_2409_08270_b200 import CameraView
+    wl = _workload(seed=31, n=20000, views=2, w=200, h=150, e=3)
+    base = wl.views[0]
+    sizes = [(200, 150), (333, 77), (48, 300), (1, 1), (17, 250)]
+    rng = np.random.default_rng(8)
+    pairs = []
+    for i, (w, h) in enumerate(sizes):
+        v = CameraView(i, w, h, base.fx, base.fy, w / 2 + 0.5, h / 2 + 0.5,
+                       base.world_to_camera, base.near_clip)
+        lab = rng.integers(0, 3, (h, w)).astype(np.uint16) if i != 2 else np.zeros((h, w), np.uint16)
+        pairs.append((v, LabelMask(i, lab)))
+    behind = np.array(base.world_to_camera, dtype=np.float64)
+    behind[:3, :3] = -behind[:3, :3]  # looks away from the scene
+    pairs.append((CameraView(5, 64, 64, 64.0, 64.0, 32.5, 32.5, behind, 0.01),
+                  LabelMask(5, rng.integers(0, 3, (64, 64)).astype(np.uint16))))
+    one = accumulate_contributions(wl.scene, pairs, 3).values
+    two = accumulate_contributions(wl.scene, pairs, 3, devices=[0, 0]).values
+    assert np.array_equal(one, two)
+    cams = [oracle.camera_of(v) for v, _ in pairs]
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, cams, [m.labels for _, m in pairs], 3, threads=4)
+    np.testing.assert_allclose(two, ref, rtol=1e-6, atol=1e-9)
+    assert one.sum() > 0
