@@ -225,17 +225,22 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def atomic_peak(acc_bytes):
-    """R_atom (tools/atomic_peak.cu): the L2 float64 RED ceiling -- random lanes into an
-    L2-resident buffer -- plus, for context, the uniform-random rate into a buffer of the
-    accumulator's size (a floor: real scatters have far more locality)."""
-    p = ROOT / "profiles" / "r1_atomic_peak.json"
+def atomic_peak(acc_bytes, fixed=False):
+    """R_atom (tools/atomic_peak.cu): the L2 ceiling of the accumulator adds -- 16 random
+    lanes per warp instruction into an L2-resident buffer (float64 RED, or the fixed-point
+    accumulator's pair of uint64 REDs) -- plus, for context, the uniform-random rate into a
+    buffer of the accumulator's size (a floor: real scatters have far more locality)."""
+    p = ROOT / "profiles" / "r2_atomic_peak.json"
+    if not p.exists():
+        p = ROOT / "profiles" / "r1_atomic_peak.json"
     if not p.exists():
         return None, None, None
     res = json.loads(p.read_text())["results"]
-    key = "16MB_C2" if acc_bytes <= (64 << 20) else ("256MB_C3" if acc_bytes <= (768 << 20)
-                                                      else "1536MB_C4")
-    return res["16MB_C2"]["f64_rand16"] * 1e9, key, res[key]["f64_rand16"] * 1e9
+    key = "fixed_pair_rand16" if fixed and "fixed_pair_rand16" in res["16MB_C2"] else "f64_rand16"
+    scale = 2 if key == "fixed_pair_rand16" else 1  # the fixed classes hold twice the bytes
+    cls = ("16MB_C2" if acc_bytes <= scale * (64 << 20) else
+           ("256MB_C3" if acc_bytes <= scale * (768 << 20) else "1536MB_C4"))
+    return res["16MB_C2"][key] * 1e9, cls, res[cls][key] * 1e9
 
 
 def pipe_peaks():
@@ -524,7 +529,8 @@ def main():
         except Exception:
             traffic = None
     atom_rate = iso["atomics"] / views_n / raster_avg_s if raster_avg_s > 0 else None
-    atom_peak, atom_key, atom_sized = atomic_peak(E * N * BYTES_PER_ATOMIC[kind])
+    atom_peak, atom_key, atom_sized = atomic_peak(E * N * BYTES_PER_ATOMIC[kind],
+                                                  fixed=kind == _native.ACC_FIXED)
     clk_summary = clk.summary()
     sm_hz = (clk_summary.get("sm_mhz") or 1965.0) * 1e6
     issue_peak = 148 * 4 * sm_hz  # warp-instructions / s (one issue slot per scheduler per clock)
@@ -585,9 +591,11 @@ def main():
                          "achieved_per_s": atom_rate,
                          "peak_per_s": atom_peak,
                          "frac": (atom_rate / atom_peak) if (atom_rate and atom_peak) else None,
-                         "peak_source": "profiles/r1_atomic_peak.json 16MB_C2 f64_rand16 "
-                                        "(tools/atomic_peak.cu: float64 RED, 16 random lanes "
-                                        "per warp instruction, L2-resident buffer)",
+                         "peak_source": "profiles/r2_atomic_peak.json 16MB_C2 "
+                                        + ("fixed_pair_rand16 (two uint64 REDs per add" if kind
+                                           == _native.ACC_FIXED else "f64_rand16 (float64 RED")
+                                        + ", 16 random lanes per warp instruction, L2-resident "
+                                        "buffer; tools/atomic_peak.cu)",
                          "uniform_random_per_s_at_accumulator_size": atom_sized,
                          "accumulator_size_class": atom_key,
                          "l2_red_pct_of_peak_ncu": rec.get("l2_red_pct_of_peak")},

@@ -34,6 +34,11 @@ def test_atomic_roofline_uses_the_l2_ceiling():
     assert key == "16MB_C2" and peak > 0 and sized == peak
     peak2, key2, sized2 = bench.atomic_peak(1536 << 20)
     assert key2 == "1536MB_C4" and peak2 == peak and sized2 < peak
+    # the fixed-point accumulator: its own (pair-of-REDs) ceiling, classes of twice the bytes
+    pf, kf, sf = bench.atomic_peak(32 << 20, fixed=True)
+    assert kf == "16MB_C2" and 0 < pf < peak and sf == pf
+    pf2, kf2, sf2 = bench.atomic_peak(3072 << 20, fixed=True)
+    assert kf2 == "1536MB_C4" and sf2 < pf
 
 
 def test_reference_arm_line(capsys):

@@ -8,6 +8,9 @@
 //   rand16   16 active lanes (the raster's grouped path fires <= 16 per warp)
 //   coal     32 lanes, one contiguous 256 B segment per warp instruction
 //   f32      rand32 with float32 (the north star's fp32 N x L alternative)
+//   fixed_pair_rand16  the deterministic accumulator's add: two u64 REDs into the
+//            (hi, lo) words of one 16-byte entry, 16 random lanes (entry adds/s,
+//            over the doubled accumulator size of the same config)
 // over accumulators of 16 MB (C2: E=2 x 1 M float64), 256 MB (C3) and
 // 1.5 GB (C4: E=64 x 3 M).  CUDA events, best of 5 after a warm-up.
 //
@@ -56,6 +59,47 @@ __global__ void __launch_bounds__(256) red_kernel(T* acc, unsigned long long n, 
     }
 }
 
+// The deterministic accumulator's add (FS_ACC_FIXED): two uint64 REDs into the
+// (hi, lo) words of one 16-byte entry, 16 random lanes per warp instruction.
+__global__ void __launch_bounds__(256) fixed_pair_kernel(unsigned long long* acc,
+                                                         unsigned long long n_entries, int iters,
+                                                         unsigned long long seed) {
+    const unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    unsigned long long h = mix(t ^ seed);
+    for (int i = 0; i < iters; ++i) {
+        h = mix(h + 0x9e3779b97f4a7c15ull);
+        unsigned long long* p = acc + 2 * (h % n_entries);
+        if (lane < 16) {
+            asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(h >> 40) : "memory");
+            asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p + 1), "l"(h & 0xffffffffull)
+                         : "memory");
+        }
+    }
+}
+
+static double run_fixed(unsigned long long* acc, unsigned long long n_entries) {
+    const int blocks = 148 * 8, threads = 256, iters = 256;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    fixed_pair_kernel<<<blocks, threads>>>(acc, n_entries, iters, 1);
+    CK(cudaDeviceSynchronize());
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        CK(cudaEventRecord(a));
+        fixed_pair_kernel<<<blocks, threads>>>(acc, n_entries, iters, 2 + r);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (ms < best) best = ms;
+    }
+    CK(cudaEventDestroy(a));
+    CK(cudaEventDestroy(b));
+    return (double)blocks * threads / 32 * 16 * iters / (best * 1e-3);  // entry adds per second
+}
+
 template <typename T, int kPattern>
 static double run(T* acc, unsigned long long n, int lanes) {
     const int blocks = 148 * 8, threads = 256, iters = 256;
@@ -86,10 +130,12 @@ int main() {
     int clk_khz = 0;
     CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
     const unsigned long long sizes[3] = {16ull << 20, 256ull << 20, 1536ull << 20};
+    // the fixed-point accumulator of the same configs is twice as large (16 B per entry)
+    const unsigned long long fixed_sizes[3] = {32ull << 20, 512ull << 20, 3072ull << 20};
     const char* names[3] = {"16MB_C2", "256MB_C3", "1536MB_C4"};
     void* buf;
-    CK(cudaMalloc(&buf, sizes[2]));
-    CK(cudaMemset(buf, 0, sizes[2]));
+    CK(cudaMalloc(&buf, fixed_sizes[2]));
+    CK(cudaMemset(buf, 0, fixed_sizes[2]));
     printf("{\n \"device\": \"%s\", \"sms\": %d, \"sm_clock_mhz_nominal\": %d,\n", p.name,
            p.multiProcessorCount, clk_khz / 1000);
     printf(" \"how\": \"tools/atomic_peak.cu: %d blocks x 256 threads x 256 iterations of atomicAdd "
@@ -102,9 +148,10 @@ int main() {
         const double r16 = run<double, kRand16>((double*)buf, n64, 16);
         const double rc = run<double, kCoal>((double*)buf, n64, 32);
         const double rf = run<float, kRand32>((float*)buf, n32, 32);
+        const double rx = run_fixed((unsigned long long*)buf, fixed_sizes[s] / 16);
         printf("  \"%s\": {\"f64_rand32\": %.2f, \"f64_rand16\": %.2f, \"f64_coalesced\": %.2f, "
-               "\"f32_rand32\": %.2f}%s\n",
-               names[s], r32 * 1e-9, r16 * 1e-9, rc * 1e-9, rf * 1e-9, s < 2 ? "," : "");
+               "\"f32_rand32\": %.2f, \"fixed_pair_rand16\": %.2f}%s\n",
+               names[s], r32 * 1e-9, r16 * 1e-9, rc * 1e-9, rf * 1e-9, rx * 1e-9, s < 2 ? "," : "");
     }
     printf(" }\n}\n");
     CK(cudaFree(buf));
