@@ -265,3 +265,21 @@ def test_multi_device_ragged_views_and_empty_masks():
                             wl.scene.opacities, cams, [m.labels for _, m in pairs], 3, threads=4)
     np.testing.assert_allclose(two, ref, rtol=1e-6, atol=1e-9)
     assert one.sum() > 0
+
+
+def test_many_objects_large_e():
+    """E = 300 objects (uint16 labels well above 255): iid labels, ungrouped per-pixel
+    adds, the transposing finalize over 10 row tiles and the scene argmax over 300 rows,
+    against the oracle; devices=[0, 0] gives the same matrix."""
+    wl = _workload(seed=33, n=6000, views=3, w=96, h=72, e=2)
+    rng = np.random.default_rng(12)
+    pairs = [(v, LabelMask(v.view_id, rng.integers(0, 300, (v.height, v.width)).astype(np.uint16)))
+             for v in wl.views]
+    A = accumulate_contributions(wl.scene, pairs, 300).values
+    cams = [oracle.camera_of(v) for v in wl.views]
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, cams, [m.labels for _, m in pairs], 300, threads=4)
+    np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+    M2, a2 = solve(wl.scene, pairs, 300, 0.0, "scene", devices=[0, 0])
+    assert np.array_equal(M2.values, A)
+    assert np.array_equal(a2.membership, oracle.assign_scene(A, 0.0))
