@@ -21,9 +21,8 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 fs = pytest.importorskip("paper_2409_08270_b200")
-from paper_2409_08270_b200 import DEFAULT_BLEND, LabelMask, accumulate_contributions, solve  # noqa: E402
+from paper_2409_08270_b200 import LabelMask, accumulate_contributions, solve  # noqa: E402
 from paper_2409_08270_b200 import _native, synth  # noqa: E402
-from paper_2409_08270_b200.multidevice import device_contexts  # noqa: E402
 
 
 def _workload(seed=21, n=30000, views=6, w=200, h=150, e=4, **kw):
