@@ -45,11 +45,28 @@ __device__ __forceinline__ int primary_shift(const unsigned long long* oa) {
     return hb > 31 ? hb - 31 : 0;
 }
 
-// per-block tile histogram of a contiguous gid range -> count[t * g + b]
+// The rectangle rc clipped to the tile rows [ty_lo, ty_hi) of a band; false if empty.
+template <bool kBanded>
+__device__ __forceinline__ bool band_rows(unsigned long long rc, int ty_lo, int ty_hi,
+                                          unsigned int& ty0, unsigned int& ty1) {
+    if (rc == ~0ull) return false;
+    ty0 = (unsigned int)((rc >> 32) & 0xFFFF);
+    ty1 = (unsigned int)((rc >> 48) & 0xFFFF);
+    if (!kBanded) return true;  // one band: every row of the image
+    ty0 = max(ty0, (unsigned int)ty_lo);
+    ty1 = min(ty1, (unsigned int)(ty_hi - 1));
+    return ty0 <= ty1;
+}
+
+// per-block tile histogram of a contiguous gid range -> count[t * g + b], for the
+// tile rows [ty_lo, ty_hi) (one band: the whole image unless it has more than
+// kMaxTiles tiles, whose histograms would not fit shared memory)
+template <bool kBanded>
 __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinBuffers b, int ntiles,
-                                                             int tiles_x) {
+                                                             int tiles_x, int ty_lo, int ty_hi) {
     extern __shared__ unsigned int s_hist[];
-    for (int t = threadIdx.x; t < ntiles; t += kBinThreads) s_hist[t] = 0;
+    const int t_lo = ty_lo * tiles_x, nband = min(ntiles, ty_hi * tiles_x) - t_lo;
+    for (int t = threadIdx.x; t < nband; t += kBinThreads) s_hist[t] = 0;
     __syncthreads();
     int lo, hi;
     gid_range(b.n, blockIdx.x, gridDim.x, lo, hi);
@@ -62,11 +79,18 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinBuffers b, in
             rc[j] = g < hi ? b.rect[g] : ~0ull;
         }
 #pragma unroll
-        for (int j = 0; j < kUnroll; ++j) count_rect_tiles(rc[j], tiles_x, s_hist);
+        for (int j = 0; j < kUnroll; ++j) {
+            unsigned int ty0, ty1;
+            if (!band_rows<kBanded>(rc[j], ty_lo, ty_hi, ty0, ty1)) continue;
+            const unsigned int tx0 = rc[j] & 0xFFFF, tx1 = (rc[j] >> 16) & 0xFFFF;
+            for (unsigned int ty = ty0; ty <= ty1; ++ty)
+                for (unsigned int tx = tx0; tx <= tx1; ++tx)
+                    atomicAdd(&s_hist[ty * (unsigned)tiles_x + tx - t_lo], 1u);
+        }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < ntiles; t += kBinThreads)
-        b.count_bt[(size_t)t * gridDim.x + blockIdx.x] = s_hist[t];
+    for (int t = threadIdx.x; t < nband; t += kBinThreads)
+        b.count_bt[(size_t)(t + t_lo) * gridDim.x + blockIdx.x] = s_hist[t];
 }
 
 // per tile (one warp each): exclusive scan of the tile's row of the count
@@ -174,12 +198,15 @@ __global__ void __launch_bounds__(1024) tile_start_kernel(const unsigned int* __
 
 // per-block: cursors = bucket start + the block's offset inside the bucket,
 // then shared-memory atomics place every instance of the block's gid range
+template <bool kBanded>
 __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int ntiles, int tiles_x,
-                                                            const ViewCounters* __restrict__ vc) {
+                                                            const ViewCounters* __restrict__ vc,
+                                                            int ty_lo, int ty_hi) {
     if (vc->overflow) return;
     extern __shared__ unsigned int s_cur[];
-    for (int t = threadIdx.x; t < ntiles; t += kBinThreads)
-        s_cur[t] = b.tile_start[t] + b.count_bt[(size_t)t * gridDim.x + blockIdx.x];
+    const int t_lo = ty_lo * tiles_x, nband = min(ntiles, ty_hi * tiles_x) - t_lo;
+    for (int t = threadIdx.x; t < nband; t += kBinThreads)
+        s_cur[t] = b.tile_start[t + t_lo] + b.count_bt[(size_t)(t + t_lo) * gridDim.x + blockIdx.x];
     __syncthreads();
     const int shift = primary_shift(b.key_oa);
     const unsigned long long z = ~b.key_oa[1];  // AND of the visible keys
@@ -200,13 +227,14 @@ __global__ void __launch_bounds__(kBinThreads) bin_emit_kernel(BinBuffers b, int
             const unsigned long long k = key[j] == ~0ull ? z : key[j];
             // instance = (32-bit primary depth key, gid)
             const unsigned long long e = ((k >> shift) << 32) | (unsigned int)(g0 + j * kBinThreads);
+            unsigned int ty0, ty1;
+            if (!band_rows<kBanded>(r, ty_lo, ty_hi, ty0, ty1)) continue;
             const unsigned int tx0 = r & 0xFFFF, tx1 = (r >> 16) & 0xFFFF;
-            const unsigned int ty0 = (r >> 32) & 0xFFFF, ty1 = (r >> 48) & 0xFFFF;
             FS_CHECK(tx1 < (unsigned)tiles_x && ty1 * (unsigned)tiles_x + tx1 < (unsigned)ntiles);
             for (unsigned int ty = ty0; ty <= ty1; ++ty)
                 for (unsigned int tx = tx0; tx <= tx1; ++tx) {
                     const unsigned int t = ty * (unsigned)tiles_x + tx;
-                    const unsigned int at = atomicAdd(&s_cur[t], 1u);
+                    const unsigned int at = atomicAdd(&s_cur[t - t_lo], 1u);
                     FS_CHECK(at < b.tile_start[t + 1] && at < b.capacity);
                     b.inst[at] = e;
                 }
@@ -266,23 +294,40 @@ __global__ void splat_keys_kernel(int k, const double* __restrict__ mean2d,
 int bin_blocks(int num_sms) { return 2 * num_sms; }
 
 cudaError_t bin_configure() {
-    cudaError_t e = cudaFuncSetAttribute(bin_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(kMaxTiles * sizeof(unsigned int)));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(bin_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kMaxTiles * sizeof(unsigned int)));
+    const int bytes = (int)(kMaxTiles * sizeof(unsigned int));
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(bin_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) ||
+        (e = cudaFuncSetAttribute(bin_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) ||
+        (e = cudaFuncSetAttribute(bin_emit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
+    return cudaFuncSetAttribute(bin_emit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
                 cudaStream_t st) {
     const int g = bin_blocks(num_sms);
-    const size_t smem = sizeof(unsigned int) * (size_t)ntiles;
-    bin_count_kernel<<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x);
+    // tile-row bands whose per-block histograms fit shared memory (one band for
+    // every image up to kMaxTiles tiles)
+    const int ty_n = (ntiles + tiles_x - 1) / tiles_x;
+    const int band = std::max(1, kMaxTiles / tiles_x);
+    const size_t smem = sizeof(unsigned int) * (size_t)std::min(ntiles, band * tiles_x);
+    const bool banded = band < ty_n;
+    for (int y = 0; y < ty_n; y += band) {
+        if (banded)
+            bin_count_kernel<true><<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, y, std::min(ty_n, y + band));
+        else
+            bin_count_kernel<false><<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, 0, ty_n);
+    }
     tile_scan_kernel<<<(ntiles + kWarps - 1) / kWarps, kThreads, 0, st>>>(b.count_bt, ntiles, g,
                                                                          b.tile_total);
     tile_start_kernel<<<1, 1024, 0, st>>>(b.tile_total, ntiles, b.capacity, vc, b.tile_start,
                                           b.tile_order);
-    bin_emit_kernel<<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, vc);
+    for (int y = 0; y < ty_n; y += band) {
+        if (banded)
+            bin_emit_kernel<true><<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, vc, y, std::min(ty_n, y + band));
+        else
+            bin_emit_kernel<false><<<g, kBinThreads, smem, st>>>(b, ntiles, tiles_x, vc, 0, ty_n);
+    }
 }
 
 size_t tile_sort_smem_bytes(unsigned int cap) {

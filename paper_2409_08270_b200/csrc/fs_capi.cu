@@ -386,8 +386,9 @@ int check_cam(const fs_camera& c, int idx) {
                     c.height);
     long long tiles = (long long)fs::tiles_x_of(c.width) * fs::tiles_y_of(c.height);
     if (tiles > (1 << 24)) return fail(FS_EINVAL, "view %d: image too large (%lld tiles)", idx, tiles);
-    if (tiles > fs::kMaxTiles)
-        return fail(FS_EINVAL, "view %d: image too large (%lld tiles > %d)", idx, tiles, fs::kMaxTiles);
+    if (fs::tiles_x_of(c.width) > fs::kMaxTiles)  // one tile row per binning band at least
+        return fail(FS_EINVAL, "view %d: image too wide (%d tile columns > %d)", idx,
+                    fs::tiles_x_of(c.width), fs::kMaxTiles);
     return FS_OK;
 }
 

@@ -21,16 +21,6 @@ __device__ __forceinline__ unsigned long long tile_rect(double mx, double my, do
            ((unsigned long long)ty0 << 32) | ((unsigned long long)ty1 << 48);
 }
 
-// One instance per covered tile.
-__device__ __forceinline__ void count_rect_tiles(unsigned long long rc, int tiles_x,
-                                                 unsigned int* count) {
-    if (rc == ~0ull || !count) return;
-    const unsigned int tx0 = rc & 0xFFFF, tx1 = (rc >> 16) & 0xFFFF;
-    const unsigned int ty0 = (rc >> 32) & 0xFFFF, ty1 = (rc >> 48) & 0xFFFF;
-    for (unsigned int ty = ty0; ty <= ty1; ++ty)
-        for (unsigned int tx = tx0; tx <= tx1; ++tx) atomicAdd(&count[ty * (unsigned)tiles_x + tx], 1u);
-}
-
 // ---- fs_project.cu ----
 // float offsets of the PLY vertex properties in the reference's
 // REQUIRED_PROPERTIES order (ply.py:17-23)
@@ -71,7 +61,7 @@ struct BinBuffers {
                                         // bucket's depth-ordered gids in sorted_view()
     unsigned int capacity;
 };
-constexpr int kMaxTiles = 49152;        // per-block tile histograms live in shared memory
+constexpr int kMaxTiles = 49152;        // tiles per binning band (per-block histograms in smem)
 int bin_blocks(int num_sms);
 cudaError_t bin_configure();
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,

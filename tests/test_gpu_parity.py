@@ -479,7 +479,8 @@ def test_large_label_ids():
 
 
 def test_near_maximum_tile_count():
-    """A 4096 x 2992 view (47 872 tiles, just under the 49 152 limit)."""
+    """A 4096 x 2992 view (47 872 tiles, just under one 49 152-tile binning band)
+    and a 4096 x 3200 view (51 200 tiles: two bands)."""
     from paper_2409_08270_b200 import CameraView
     rng = np.random.default_rng(3)
     n = 3000
@@ -493,9 +494,12 @@ def test_near_maximum_tile_count():
     pairs = [(v, LabelMask(0, lab))]
     A = accumulate_contributions(scene, pairs, 2).values
     np.testing.assert_allclose(A, _oracle_A(scene, pairs, 2), rtol=1e-6, atol=1e-9)
-    too_big = CameraView(0, 4096, 3200, 3000.0, 3000.0, 2048.0, 1600.0, np.eye(4))
-    with pytest.raises(Exception, match="too large"):
-        accumulate_contributions(scene, [(too_big, LabelMask(0, np.zeros((3200, 4096), np.uint16)))], 2)
+    two_bands = CameraView(0, 4096, 3200, 3000.0, 3000.0, 2048.0, 1600.0, np.eye(4))
+    lab2 = np.zeros((3200, 4096), np.uint16)
+    lab2[1600:, :] = 1
+    pairs2 = [(two_bands, LabelMask(0, lab2))]
+    A2 = accumulate_contributions(scene, pairs2, 2).values
+    np.testing.assert_allclose(A2, _oracle_A(scene, pairs2, 2), rtol=1e-6, atol=1e-9)
 
 
 @pytest.mark.parametrize("blend", [DEFAULT_BLEND, EXACT_BLEND], ids=["default", "exact"])
@@ -611,3 +615,17 @@ def test_concurrent_calls_from_threads():
                            range(4)))
     for o in outs:
         np.testing.assert_allclose(o, serial, rtol=1e-6, atol=1e-9)
+
+
+def test_image_beyond_one_binning_band():
+    """A 6000 x 5000 view has 117 375 tiles, more than one shared-memory binning
+    band (49 152): the banded count/emit passes must give the oracle's matrix."""
+    import os
+    wl = synth.make_workload(seed=44, n_gaussians=20000, n_views=1, width=6000, height=5000,
+                             num_objects=3)
+    A = accumulate_contributions(wl.scene, wl.pairs(), 3).values
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, [oracle.camera_of(wl.views[0])], [wl.masks[0]],
+                            3, threads=os.cpu_count())
+    np.testing.assert_allclose(A, ref, rtol=1e-6, atol=1e-9)
+    assert A.sum() > 0
