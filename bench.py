@@ -79,7 +79,8 @@ def self_launch(args) -> int:
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
            str(Path(__file__).resolve())] + sys.argv[1:]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS setup in the log
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator / NVLS setup in the log ...
+    env.setdefault("NCCL_DEBUG_FILE", "/tmp/flashsplat_nccl.%h.%p.log")  # ... not on stdout
     env.setdefault("OMP_NUM_THREADS", "1")
     return subprocess.call(cmd, env=env)
 
