@@ -282,3 +282,39 @@ def test_many_objects_large_e():
     M2, a2 = solve(wl.scene, pairs, 300, 0.0, "scene", devices=[0, 0])
     assert np.array_equal(M2.values, A)
     assert np.array_equal(a2.membership, oracle.assign_scene(A, 0.0))
+
+
+def test_multi_device_instance_overflow_retry():
+    """Views whose instance count overflows a context's buffers are re-run after
+    growing them -- also on the dynamic queue (the retry uses the view's own log
+    slot and global index)."""
+    from paper_2409_08270_b200 import CameraView, GaussianScene
+    n = 1500
+    rng = np.random.default_rng(0)
+    scene = GaussianScene(np.c_[rng.uniform(-0.1, 0.1, (n, 2)), rng.uniform(2, 3, n)],
+                          np.tile([1.0, 0, 0, 0], (n, 1)), np.full((n, 3), 2.0),
+                          rng.uniform(0.8, 0.95, n))
+    views = [CameraView(i, 1920, 1088, 1000.0 + 5 * i, 1000.0, 960.0, 544.0, np.eye(4))
+             for i in range(3)]
+    pairs = [(v, LabelMask(i, rng.integers(0, 2, (1088, 1920), dtype=np.uint16)))
+             for i, v in enumerate(views)]
+    fresh = [_native.Context(0, streams=2), _native.Context(0, streams=2)]
+    try:
+        from paper_2409_08270_b200.contributions import acc_kind_of
+        kind = acc_kind_of(True)
+        for c in fresh:
+            c.set_scene(scene)
+        accs = [c.acc_buffer(2, n, kind).zero() for c in fresh]
+        st, owner = _native.accumulate_multi(fresh, [v for v, _ in pairs],
+                                             [m.labels for _, m in pairs], 2, 1 / 255, 1e-4,
+                                             [a.ptr for a in accs], kind)
+        assert st["retried_views"] >= 1 and sorted(set(owner.tolist())) <= [0, 1]
+        out = np.zeros((2, n), np.float32)
+        _native.finalize_multi(fresh, [a.ptr for a in accs], n, 2, out, acc_kind=kind)
+    finally:
+        for c in fresh:
+            c.close()
+    cams = [oracle.camera_of(v) for v in views]
+    ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities, cams,
+                            [m.labels for _, m in pairs], 2, threads=8)
+    np.testing.assert_allclose(out, ref, rtol=1e-6, atol=1e-9)
