@@ -55,6 +55,7 @@ _TARGETS = {
 }
 _saved: dict = {}
 _devices = None  # GPU list the rebound accumulate_contributions spreads views over
+_device_ply = False  # load_scene_ply uploads + activates on the GPU (scene_io.PlyScene)
 
 
 def resolve_devices(devices="auto"):
@@ -87,6 +88,10 @@ def _replacement(name):
         from .scene_io import load_scene_ply as impl
 
         def load_scene_ply(path):
+            if _device_ply:
+                # raw records activated on the GPU; a GaussianScene whose float64 host
+                # arrays are built only if read (scene_io.PlyScene)
+                return impl(path, device=_devices[0] if _devices else 0)
             s = impl(path)  # memory-mapped columns; the caller's own scene type
             return ref_scene(means=s.means, rotations=s.rotations, scales=s.scales,
                              opacities=s.opacities, colors_dc=s.colors_dc,
@@ -138,9 +143,14 @@ def _replacement(name):
     return assign
 
 
-def install(devices="auto") -> None:
-    global _devices
+def install(devices="auto", device_ply: bool = False) -> None:
+    """Rebind the reference's entry points.  ``devices``: see resolve_devices.
+    ``device_ply``: the rebound ``load_scene_ply`` (the CLI's, cli.py:97) uploads the
+    checkpoint's raw records and activates them on the GPU (scene_io.PlyScene) instead
+    of returning the reference's host-activated scene type."""
+    global _devices, _device_ply
     _devices = resolve_devices(devices)
+    _device_ply = bool(device_ply)
     for name, modules in _TARGETS.items():
         fn = _replacement(name)
         for modname in modules:
@@ -154,8 +164,9 @@ def install(devices="auto") -> None:
 
 
 def uninstall() -> None:
-    global _devices
+    global _devices, _device_ply
     _devices = None
+    _device_ply = False
     for (modname, name), fn in _saved.items():
         setattr(importlib.import_module(modname), name, fn)
     _saved.clear()

@@ -126,3 +126,22 @@ def test_install_devices_reach_the_multi_gpu_path(splatlift, monkeypatch):
         assert seen.get("devices") == expect
     monkeypatch.setenv("FLASHSPLAT_DEVICES", "1,0")
     assert splatlift_compat.resolve_devices("auto") == [1, 0]
+
+
+def test_install_device_ply_routes_the_cli_loader(splatlift, monkeypatch):
+    """install(device_ply=True): the CLI's load_scene_ply (cli.py:97) goes through the
+    device ingestion path (scene_io.load_scene_ply(path, device=...))."""
+    from paper_2409_08270_b200 import scene_io, splatlift_compat
+    import splatlift.cli as cli
+    seen = {}
+
+    def fake(path, device=None):
+        seen["device"] = device
+        return "scene"
+
+    monkeypatch.setattr(scene_io, "load_scene_ply", fake)
+    splatlift_compat.install(devices=[2, 3], device_ply=True)
+    try:
+        assert cli.load_scene_ply("x.ply") == "scene" and seen["device"] == 2
+    finally:
+        splatlift_compat.uninstall()
