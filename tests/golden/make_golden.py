@@ -491,7 +491,58 @@ def gen_acceptance():
     return cases
 
 
+def gen_fuzz(seeds=None, budget_s=240.0):
+    """The reference's own outputs on the adversarial fuzz cases of
+    tests/fuzz_cases.py (inputs regenerated at test time, pinned by digest):
+    A (float32 and float64), assign_scene membership / assign_binary labels at
+    the case's gamma, and render_view (alpha, depth; a 3-channel property composited alongside) plus
+    render_scene_mask of the first view."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import fuzz_cases as fz
+    from splatlift import maskrender as ref_mask
+    from splatlift import rasterizer as ref_rast
+    from splatlift import solver as ref_solver
+
+    cases, spent = {}, 0.0
+    for seed in (seeds if seeds is not None else range(fz.N_CASES)):
+        c = fz.case_arrays(seed)
+        n = len(c["opac"])
+        px = sum(int(r[0]) * int(r[1]) for r in c["cams"])
+        if n * px > 4e8 or n * c["E"] > 25000:  # fixture size and reference time
+            continue
+        t0 = time.perf_counter()
+        scene = ref_scene.GaussianScene(c["means"], c["quats"], c["scales"], c["opac"])
+        views = [ref_scene.CameraView(view_id=i, width=int(r[0]), height=int(r[1]), fx=r[2],
+                                      fy=r[3], cx=r[4], cy=r[5], world_to_camera=r[7:].reshape(4, 4),
+                                      near_clip=r[6]) for i, r in enumerate(c["cams"])]
+        pairs = [(v, ref_contrib.LabelMask(v.view_id, m)) for v, m in zip(views, c["masks"])]
+        blend = ref.BlendConfig(*c["floors"])
+        out = accumulate_case(scene, pairs, c["E"], blend, store_inputs=False)
+        del out["A64"]  # the reference's float32 matrix is the fixture
+        M = ref_contrib.ContributionMatrix(out["A"])
+        out["membership"] = ref_solver.assign_scene(M, c["gamma"]).membership.astype(np.uint8)
+        if c["E"] == 2:
+            out["labels"] = ref_solver.assign_binary(M, c["gamma"]).labels.astype(np.uint8)
+        ch, memb, tau = fz.render_extras(seed, n, c["E"])
+        if views[0].width * views[0].height <= 6000:  # render fixtures of the small views
+            r = ref_rast.render_view(scene, views[0], ch, blend)
+            out.update(r_alpha=r.alpha, r_depth=r.depth)
+            asn = ref_solver.Assignment(mode="scene", gamma=0.0, membership=memb.astype(bool))
+            out["r_mask"] = ref_mask.render_scene_mask(scene, asn, views[0], tau, blend).labels
+        out["digest"] = np.frombuffer(fz.digest(c).encode(), np.uint8)
+        cases[f"s{seed}"] = out
+        spent += time.perf_counter() - t0
+        print(f"  fuzz seed {seed}: N={n} px={px} E={c['E']} {time.perf_counter() - t0:.1f}s",
+              flush=True)
+        if spent > budget_s:
+            break
+    return cases
+
+
 def main(which=None):
+    if which == "fuzz":
+        save("fuzz", gen_fuzz())
+        return
     if which == "fullres":
         save("accumulate_fullres", gen_fullres())
         return
