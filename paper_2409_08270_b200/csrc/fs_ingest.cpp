@@ -54,14 +54,22 @@ extern "C" int fs_decode_mask_png(const uint8_t* data, int64_t size, uint16_t* o
     uint32_t w = 0, h = 0;
     int depth = 0, ctype = -1, interlace = 0;
     std::vector<uint8_t> idat;
-    bool seen_ihdr = false, seen_iend = false;
+    bool seen_ihdr = false, seen_iend = false, seen_idat = false;
     while (pos + 12 <= size && !seen_iend) {
         const uint32_t len = be32(data + pos);
         const uint8_t* type = data + pos + 4;
         const uint8_t* body = data + pos + 8;
         if (pos + 12 + (int64_t)len > size) return fs::fail(FS_EINVAL, "truncated PNG chunk");
+        // Pillow verifies the CRC of every chunk it parses before the image data
+        // and rejects the file on a mismatch; decline such files so the caller's
+        // Pillow path raises the reference's error instead of decoding them
+        if (!seen_idat && memcmp(type, "IDAT", 4) != 0 &&
+            crc32(crc32(0L, type, 4), body, len) != be32(body + len))
+            return fs::fail(FS_EINVAL, "PNG chunk CRC mismatch");
         if (!memcmp(type, "IHDR", 4)) {
             if (len < 13) return fs::fail(FS_EINVAL, "bad IHDR");
+            if (body[10] != 0 || body[11] != 0)
+                return fs::fail(FS_EINVAL, "unsupported PNG compression / filter method");
             w = be32(body);
             h = be32(body + 4);
             depth = body[8];
@@ -69,6 +77,7 @@ extern "C" int fs_decode_mask_png(const uint8_t* data, int64_t size, uint16_t* o
             interlace = body[12];
             seen_ihdr = true;
         } else if (!memcmp(type, "IDAT", 4)) {
+            seen_idat = true;
             idat.insert(idat.end(), body, body + len);
         } else if (!memcmp(type, "IEND", 4)) {
             seen_iend = true;

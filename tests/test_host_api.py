@@ -180,3 +180,48 @@ def test_native_png_decoder_matches_pillow():
     pal.save(buf, format="PNG")
     assert _native.decode_mask_png(buf.getvalue()) is None
     assert _native.decode_mask_png(b"not a png") is None
+
+
+def test_native_png_decoder_on_corrupted_files_defers_to_pillow():
+    """Corrupted / truncated mask files: the native decoder either declines
+    (None -> the Pillow path, which raises or decodes exactly as the reference
+    does) or returns exactly what Pillow decodes -- never data from a file the
+    reference would reject (e.g. a damaged IHDR: Pillow checks chunk CRCs)."""
+    import io
+
+    from PIL import Image, PngImagePlugin
+
+    from paper_2409_08270_b200 import _native
+
+    def pillow(data):
+        try:
+            with Image.open(io.BytesIO(data)) as im:
+                return np.asarray(im.convert("I"), np.int32).astype(np.uint16)
+        except Exception:
+            return None
+
+    rng = np.random.default_rng(3)
+    for trial in range(1500):
+        h, w = (int(x) for x in rng.integers(1, 40, 2))
+        a = (rng.integers(0, 65536, (h, w)).astype(np.uint16) if trial % 2
+             else rng.integers(0, 256, (h, w)).astype(np.uint8))
+        info = None
+        if trial % 5 == 0:
+            info = PngImagePlugin.PngInfo()
+            info.add_text("k", "v" * int(rng.integers(1, 30)))
+        buf = io.BytesIO()
+        Image.fromarray(a).save(buf, format="PNG", pnginfo=info)
+        d = bytearray(buf.getvalue())
+        mode = trial % 3
+        if mode == 0:
+            for _ in range(int(rng.integers(1, 4))):
+                d[int(rng.integers(8, len(d)))] = int(rng.integers(0, 256))
+        elif mode == 1:
+            d = d[:int(rng.integers(8, len(d)))]
+        else:
+            d[int(rng.integers(8, len(d)))] ^= 1 << int(rng.integers(0, 8))
+        got = _native.decode_mask_png(bytes(d))
+        if got is not None:
+            ref = pillow(bytes(d))
+            assert ref is not None, f"trial {trial}: native decoded a file Pillow rejects"
+            assert np.array_equal(got, ref), f"trial {trial}"
