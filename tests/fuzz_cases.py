@@ -147,3 +147,39 @@ def label_band(oracle, values, gamma, scene_mode, rtol=1e-4, atol=1e-6):
     margin = oracle.decision_margin(values, gamma)
     band = np.abs(margin) <= 4 * (rtol + atol / np.maximum(total, 1e-30))
     return band.any(axis=0) if scene_mode else band[1]
+
+
+PLY_VALUES = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-45, 3e38, -3e38, 88.7, 710.0, -750.0,
+              800.0, -800.0, 1e-30]
+
+
+def ply_edits(seed, n_vertices, names):
+    """Random value edits [(vertex, property, float32 value)] for a PLY record
+    table: special values (NaN, +-inf, +-0, denormal, float32 extremes, exp
+    overflow / underflow arguments, huge logits) dropped into random
+    properties, and sometimes a zeroed or tiny quaternion."""
+    rng = np.random.default_rng(5000 + seed)
+    edits = []
+    for _ in range(int(rng.integers(1, 6))):
+        v = int(rng.integers(0, n_vertices))
+        if rng.random() < 0.2:
+            val = 0.0 if rng.random() < 0.5 else 1e-30
+            edits += [(v, f"rot_{k}", val) for k in range(4)]
+        else:  # half of the edits hit the activated properties
+            hot = [q for q in names if q.startswith(("scale_", "rot_")) or q == "opacity"]
+            prop = str(rng.choice(hot if rng.random() < 0.5 else names))
+            edits.append((v, prop, float(rng.choice(PLY_VALUES))))
+    return edits
+
+
+def patch_ply(raw, edits):
+    """Binary little-endian PLY bytes with record values overwritten."""
+    raw = bytes(raw)
+    head_end = raw.index(b"end_header\n") + len(b"end_header\n")
+    names = [ln.split()[2] for ln in raw[:head_end].decode().splitlines()
+             if ln.startswith("property")]
+    rec = np.frombuffer(raw[head_end:], dtype=np.dtype([(p, "<f4") for p in names])).copy()
+    with np.errstate(over="ignore"):
+        for v, p, val in edits:
+            rec[p][v] = np.float32(val)
+    return raw[:head_end] + rec.tobytes(), names

@@ -135,3 +135,40 @@ def test_device_loaded_scene_on_several_contexts(tmp_path):
     M2, a2 = solve(dev, pairs, 2, 0.0, "binary", devices=[0, 0])
     assert np.array_equal(M1.values, M2.values) and np.array_equal(a1.labels, a2.labels)
     assert M1.values.sum() > 0
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_device_loader_fuzz_matches_host_loader(tmp_path, seed):
+    """The special-value checkpoints of tests/test_scene_io.py's fuzz (host loader
+    == reference loader there): the device path raises the same error, or
+    produces the same arrays (quaternions and means bit-exact, exp activations
+    within the ulp bounds above; +-inf / 0 where exp overflows / underflows)."""
+    from fuzz_cases import patch_ply, ply_edits
+
+    c = PLY["plain" if seed % 2 else "interleaved"]
+    _, names = patch_ply(c["ply"], [])
+    data, _ = patch_ply(c["ply"], ply_edits(seed, len(c["means"]), names))
+    path = _write(tmp_path, "f", data)
+    try:
+        host = load_scene_ply(path)
+        host_err = None
+    except SceneDataError as e:
+        host, host_err = None, e
+    if host_err is not None:
+        with pytest.raises(SceneDataError) as dev_err:
+            load_scene_ply(path, device=0)
+        assert str(dev_err.value) == str(host_err)
+        return
+    sc = load_scene_ply(path, device=0)
+    params = np.zeros((len(sc), 8))
+    ctx = _native.context(0)
+    with ctx.lock:
+        bad = ctx.set_scene_ply(sc, params)
+        ctx._scene_key = None
+    assert (bad < 0).all()
+    assert np.array_equal(params[:, 4:8], host.rotations)
+    fin = np.isfinite(host.scales) & (host.scales > 0)
+    assert np.array_equal(params[:, 0:3][~fin], host.scales[~fin])  # inf / 0 exactly
+    assert _ulps(params[:, 0:3][fin], host.scales[fin]).max() <= 1
+    assert _ulps(params[:, 3], host.opacities).max() <= 2
+    assert np.array_equal(sc.means, host.means)

@@ -103,3 +103,39 @@ def test_host_loader_matches_reference_golden(tmp_path):
         assert [names[i] for i in lazy._ply_offsets] == list(
             ("x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2", "opacity",
              "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"))
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_host_loader_fuzz_matches_reference_loader(tmp_path, seed):
+    """Checkpoints with special values (NaN, inf, +-0, denormals, exp overflow /
+    underflow arguments, zero quaternions) in random properties: the host loader
+    raises the reference loader's error, or returns its arrays bit for bit."""
+    if not REF.exists():
+        pytest.skip("reference package not available here")
+    sys.path.insert(0, str(REF))
+    try:
+        import splatlift.ply as ref_ply
+    finally:
+        sys.path.remove(str(REF))
+    from conftest import load_golden
+    from fuzz_cases import patch_ply, ply_edits
+
+    c = load_golden("scene_ply")["plain" if seed % 2 else "interleaved"]
+    _, names = patch_ply(c["ply"], [])
+    data, _ = patch_ply(c["ply"], ply_edits(seed, len(c["means"]), names))
+    p = tmp_path / "f.ply"
+    p.write_bytes(data)
+    try:
+        want = ref_ply.load_scene_ply(p)
+        want_err = None
+    except Exception as e:  # noqa: BLE001 -- the reference's own error is the expectation
+        want, want_err = None, e
+    if want_err is not None:  # same exception class (by name: two packages) and message
+        with pytest.raises(Exception) as got:
+            load_scene_ply(p)
+        assert type(got.value).__name__ == type(want_err).__name__
+        assert str(got.value) == str(want_err)
+    else:
+        got = load_scene_ply(p)
+        for k in ("means", "rotations", "scales", "opacities", "colors_dc"):
+            assert np.array_equal(getattr(got, k), getattr(want, k), equal_nan=True), k
