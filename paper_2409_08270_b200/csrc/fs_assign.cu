@@ -147,7 +147,13 @@ void launch_row_counts(const uint8_t* m, long long n, int rows, unsigned long lo
     long long bx = (n / 16 + 255) / 256;
     if (bx > 148 * 4) bx = 148 * 4;
     if (bx < 1) bx = 1;
-    row_count_kernel<<<dim3((unsigned)bx, (unsigned)rows), 256, 0, st>>>(m, n, counts);
+    // one grid row per matrix row; gridDim.y is capped at 65 535 and a scene
+    // assignment can have 65 536 rows (every uint16 label an object)
+    for (int r0 = 0; r0 < rows; r0 += 65535) {
+        const int nr = rows - r0 < 65535 ? rows - r0 : 65535;
+        row_count_kernel<<<dim3((unsigned)bx, (unsigned)nr), 256, 0, st>>>(m + (long long)r0 * n, n,
+                                                                          counts + r0);
+    }
 }
 
 void launch_finalize(const AccParts& parts, bool fixed, long long g0, long long g1, int e,

@@ -284,6 +284,31 @@ def test_many_objects_large_e():
     assert np.array_equal(a2.membership, oracle.assign_scene(A, 0.0))
 
 
+def test_maximum_label_count():
+    """E = 65 536 -- every uint16 label value is an object id (masks.py wire
+    format): labels up to 65 535 index the N x E accumulator (16-B entries, 1.5 GB
+    here), the finalize transposes 65 536 rows and the scene argmax runs over them;
+    against the oracle, also on two contexts."""
+    wl = _workload(seed=34, n=1500, views=2, w=64, h=48, e=2)
+    rng = np.random.default_rng(13)
+    E = 65536
+    pairs = []
+    for v in wl.views:
+        lab = rng.integers(0, E, (v.height, v.width)).astype(np.uint16)
+        lab[: v.height // 2, : v.width // 2] = 65535  # a coherent block of the top id
+        lab[v.height // 2:, v.width // 2:] = 0
+        pairs.append((v, LabelMask(v.view_id, lab)))
+    M, asn = solve(wl.scene, pairs, E, 0.0, "scene")
+    cams = [oracle.camera_of(v) for v in wl.views]
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, cams, [m.labels for _, m in pairs], E, threads=4)
+    np.testing.assert_allclose(M.values, ref, rtol=1e-6, atol=1e-9)
+    assert M.values[65535].sum() > 0 and M.values[0].sum() > 0
+    assert np.array_equal(asn.membership, oracle.assign_scene(M.values, 0.0))
+    M2, _ = solve(wl.scene, pairs, E, 0.0, "scene", devices=[0, 0])
+    assert np.array_equal(M2.values, M.values)
+
+
 def test_multi_device_instance_overflow_retry():
     """Views whose instance count overflows a context's buffers are re-run after
     growing them -- also on the dynamic queue (the retry uses the view's own log
