@@ -264,6 +264,14 @@ def test_edge_cases():
         lab = np.full((1, 1), E - 1, np.uint16)
         A = accumulate_contributions(g, [(one, LabelMask(0, lab))], E).values
         assert A.shape == (E, 1) and A[E - 1, 0] > 0 and A[:E - 1].sum() == 0
+    # N = 0 through the assignment and the fused entry points (reference: empty results)
+    assert assign_scene(ContributionMatrix(np.zeros((3, 0), np.float32)), 0.0).membership.shape == (3, 0)
+    assert assign_binary(ContributionMatrix(np.zeros((2, 0), np.float32)), 0.2).labels.shape == (0,)
+    from paper_2409_08270_b200 import solve
+    M, asn = solve(empty, [(v, m)], 2, 0.0, "binary")
+    assert M.values.shape == (2, 0) and asn.labels.shape == (0,)
+    M, asn = solve(empty, [(v, m)], 4, 0.0, "scene", devices=[0, 0])
+    assert M.values.shape == (4, 0) and asn.membership.shape == (4, 0)
 
 
 def test_instance_overflow_retry():
