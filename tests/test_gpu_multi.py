@@ -309,6 +309,32 @@ def test_maximum_label_count():
     assert np.array_equal(M2.values, M.values)
 
 
+def test_thousands_of_small_views():
+    """3 000 tiny views (16 x 12 .. 40 x 30, random poses around the scene): the view
+    loop, its per-view counters and stream rotation, and the dynamic queue over
+    three contexts -- against the oracle."""
+    from paper_2409_08270_b200 import CameraView
+    wl = _workload(seed=35, n=800, views=1, w=32, h=24, e=2)
+    rng = np.random.default_rng(14)
+    pairs = []
+    for i in range(3000):
+        w, h = int(rng.integers(16, 41)), int(rng.integers(12, 31))
+        w2c = np.eye(4)
+        w2c[:3, 3] = rng.normal(scale=0.2, size=3)
+        v = CameraView(i, w, h, 30.0, 30.0, w / 2, h / 2, w2c)
+        pairs.append((v, LabelMask(i, rng.integers(0, 5, (h, w)).astype(np.uint16))))
+    M, asn = solve(wl.scene, pairs, 5, 0.1, "scene")
+    cams = [oracle.camera_of(v) for v, _ in pairs]
+    ref = oracle.accumulate(wl.scene.means, wl.scene.rotations, wl.scene.scales,
+                            wl.scene.opacities, cams, [m.labels for _, m in pairs], 5, threads=8)
+    np.testing.assert_allclose(M.values, ref, rtol=1e-6, atol=1e-9)
+    assert M.values.sum() > 0
+    st = {}
+    M3, asn3 = solve(wl.scene, pairs, 5, 0.1, "scene", devices=[0, 0, 0], stats=st)
+    assert np.array_equal(M3.values, M.values) and np.array_equal(asn3.membership, asn.membership)
+    assert sum(st["views_per_device"]) == 3000
+
+
 def test_multi_device_instance_overflow_retry():
     """Views whose instance count overflows a context's buffers are re-run after
     growing them -- also on the dynamic queue (the retry uses the view's own log
