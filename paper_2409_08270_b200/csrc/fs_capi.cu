@@ -118,6 +118,12 @@ struct fs_context {
     std::vector<cudaEvent_t> stage_events;  // 4 per view when timing
     // grow-only scratch reused across calls (no cudaMalloc/cudaFree per call)
     long long scene_cap = 0;
+    // the resident scene is stored in spatial (Morton) order: slot p holds input
+    // Gaussian perm[p] (fs_order.cu); perm_on = false keeps input order
+    // (FS_SCENE_ORDER=0, for A/B measurements)
+    unsigned int* perm = nullptr;
+    bool perm_on = false;
+    double* up_opac = nullptr;    // opacity staging (permuted by the setup kernel)
     double* up_means = nullptr;   // AoS staging of the scene upload
     double* up_quats = nullptr;
     double* up_scales = nullptr;
@@ -409,6 +415,15 @@ fs::BinBuffers bin_buffers(fs::Work& w, int n, fs::ViewCounters* vc = nullptr) {
     return b;
 }
 
+// The resident scene's slot -> input id map, or nullptr when it is in input order.
+const unsigned int* scene_perm(const fs_context* ctx) { return ctx->perm_on ? ctx->perm : nullptr; }
+
+// Spatial scene order (fs_order.cu) unless FS_SCENE_ORDER=0.
+bool scene_order_enabled() {
+    const char* e = getenv("FS_SCENE_ORDER");
+    return !(e && e[0] == '0');
+}
+
 fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr,
                                 fs::ViewCounters* vc = nullptr) {
     fs::TileSortArgs t;
@@ -433,6 +448,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     const bool own = vc == nullptr;
     if (own) vc = w.vc;
+    ex.perm = scene_perm(ctx);
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
                        cull_floor, w.k64, w.rect, w.r32, w.r64, vc, ex,
                        ctx->num_sms, w.stream, own);
@@ -461,7 +477,8 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
     ra.af_eff = alpha_floor > 0.0 ? alpha_floor : -1.0;  // contributions.py:148-149
     ra.tf_eff = t_floor > 0.0 ? t_floor : -1.0;          // contributions.py:156-157
     ra.mask = mask;
-    ra.sort = tile_sort_args(w, nullptr, log);
+    // tile lists in (depth, input id) order (accumulator rows: Rec32::oid)
+    ra.sort = tile_sort_args(w, scene_perm(ctx), log);
     ra.r32 = w.r32;
     ra.r64 = w.r64;
     if (acc_kind == FS_ACC_FIXED)
@@ -849,6 +866,7 @@ void fs_destroy(fs_context* ctx) {
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
                     (void*)ctx->opac, (void*)ctx->view_log,
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
+                    (void*)ctx->up_opac, (void*)ctx->perm,
                     (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
                     (void*)ctx->rn_u32, (void*)ctx->rn_labels, (void*)ctx->rn_rect,
                     (void*)ctx->cnt})
@@ -955,7 +973,8 @@ int fs_copy_scene(fs_context* dst, const fs_context* src) {
             (rc = dev_alloc(&dst->mz, n)) || (rc = dev_alloc(&dst->sig, 6 * (size_t)n)) ||
             (rc = dev_alloc(&dst->opac, n)) || (rc = dev_alloc(&dst->up_means, 3 * (size_t)n)) ||
             (rc = dev_alloc(&dst->up_quats, 4 * (size_t)n)) ||
-            (rc = dev_alloc(&dst->up_scales, 3 * (size_t)n)))
+            (rc = dev_alloc(&dst->up_scales, 3 * (size_t)n)) ||
+            (rc = dev_alloc(&dst->up_opac, (size_t)n)) || (rc = dev_alloc(&dst->perm, (size_t)n)))
             return rc;
         dst->scene_cap = n;
     }
@@ -970,8 +989,12 @@ int fs_copy_scene(fs_context* dst, const fs_context* src) {
         for (int k = 0; k < 5; ++k)
             CK(cudaMemcpyPeerAsync(d_arr[k], dst->device, s_arr[k], src->device,
                                    sizeof(double) * cnt[k], st));
+        if (src->perm_on)
+            CK(cudaMemcpyPeerAsync(dst->perm, dst->device, src->perm, src->device,
+                                   sizeof(unsigned int) * (size_t)n, st));
         CK(cudaStreamSynchronize(st));
     }
+    dst->perm_on = src->perm_on;
     dst->n = n;
     return FS_OK;
 }
@@ -991,7 +1014,8 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
             (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
             (rc = dev_alloc(&ctx->opac, n)) || (rc = dev_alloc(&ctx->up_means, 3 * (size_t)n)) ||
             (rc = dev_alloc(&ctx->up_quats, 4 * (size_t)n)) ||
-            (rc = dev_alloc(&ctx->up_scales, 3 * (size_t)n)))
+            (rc = dev_alloc(&ctx->up_scales, 3 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->up_opac, (size_t)n)) || (rc = dev_alloc(&ctx->perm, (size_t)n)))
             return rc;
         ctx->scene_cap = n;
     }
@@ -1001,10 +1025,12 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
     if ((rc = upload(ctx, ctx->up_means, means, 24 * (size_t)n, st)) ||
         (rc = upload(ctx, ctx->up_quats, quats, 32 * (size_t)n, st)) ||
         (rc = upload(ctx, ctx->up_scales, scales, 24 * (size_t)n, st)) ||
-        (rc = upload(ctx, ctx->opac, opacities, 8 * (size_t)n, st)))
+        (rc = upload(ctx, ctx->up_opac, opacities, 8 * (size_t)n, st)))
         return rc;
-    fs::launch_scene_setup((int)n, ctx->up_means, ctx->up_quats, ctx->up_scales, ctx->mx, ctx->my,
-                           ctx->mz, ctx->sig, st);
+    ctx->perm_on = scene_order_enabled();
+    if (ctx->perm_on) CK(fs::launch_scene_order((int)n, ctx->up_means, ctx->perm, ctx->num_sms, st));
+    fs::launch_scene_setup((int)n, ctx->up_means, ctx->up_quats, ctx->up_scales, ctx->up_opac,
+                           scene_perm(ctx), ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return FS_OK;
@@ -1033,7 +1059,8 @@ int fs_set_scene_ply(fs_context* ctx, int64_t n, const void* verts, int stride_f
             (rc = dev_alloc(&ctx->mz, n)) || (rc = dev_alloc(&ctx->sig, 6 * (size_t)n)) ||
             (rc = dev_alloc(&ctx->opac, n)) || (rc = dev_alloc(&ctx->up_means, 3 * (size_t)n)) ||
             (rc = dev_alloc(&ctx->up_quats, 4 * (size_t)n)) ||
-            (rc = dev_alloc(&ctx->up_scales, 3 * (size_t)n)))
+            (rc = dev_alloc(&ctx->up_scales, 3 * (size_t)n)) ||
+            (rc = dev_alloc(&ctx->up_opac, (size_t)n)) || (rc = dev_alloc(&ctx->perm, (size_t)n)))
             return rc;
         ctx->scene_cap = n;
     }
@@ -1048,8 +1075,12 @@ int fs_set_scene_ply(fs_context* ctx, int64_t n, const void* verts, int stride_f
     CK(cudaMemsetAsync(ctx->ply_bad, 0xff, 4 * sizeof(unsigned long long), st));
     double* dparams = nullptr;
     if (params) CK(cudaMallocAsync(reinterpret_cast<void**>(&dparams), 64 * (size_t)n, st));
-    fs::launch_scene_setup_ply((int)n, ctx->ply_raw, stride_floats, off, ctx->mx, ctx->my, ctx->mz,
-                               ctx->sig, ctx->opac, ctx->ply_bad, dparams, st);
+    ctx->perm_on = scene_order_enabled();
+    if (ctx->perm_on)
+        CK(fs::launch_scene_order_ply((int)n, ctx->ply_raw, stride_floats, off, ctx->perm,
+                                      ctx->num_sms, st));
+    fs::launch_scene_setup_ply((int)n, ctx->ply_raw, stride_floats, off, scene_perm(ctx), ctx->mx,
+                               ctx->my, ctx->mz, ctx->sig, ctx->opac, ctx->ply_bad, dparams, st);
     CK(cudaGetLastError());
     if (params) {
         CK(sync_copy(params, dparams, 64 * (size_t)n, cudaMemcpyDeviceToHost, st));
@@ -1086,6 +1117,7 @@ int fs_project(fs_context* ctx, const fs_camera* cam, uint8_t* alive, double* me
         (rc = dev_alloc(&ex.conic, 3 * n1)) || (rc = dev_alloc(&ex.depth, n1)) ||
         (rc = dev_alloc(&ex.radius, n1)))
         return rc;
+    ex.perm = scene_perm(ctx);
     fs::launch_project((int)n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, to_cam(*cam), 0.0,
                        0, w.k64, w.rect, w.r32, w.r64, w.vc, ex,
                        ctx->num_sms, w.stream);
@@ -1148,7 +1180,7 @@ int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t
     for (int attempt = 0; attempt < 2; ++attempt) {
         if ((rc = ensure_work(ctx, w, ctx->n, ntiles, cap, 1))) return rc;
         enqueue_bin(ctx, w, k, 0.0, 0, fs::ProjectExport{});
-        fs::launch_tile_sort(ntiles, tile_sort_args(w), w.stream);
+        fs::launch_tile_sort(ntiles, tile_sort_args(w, scene_perm(ctx)), w.stream);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(w.stream));
         CK(sync_copy(&vc, w.vc, sizeof(vc), cudaMemcpyDeviceToHost, w.stream));
@@ -1156,7 +1188,15 @@ int fs_bin(fs_context* ctx, const fs_camera* cam, int64_t* tile_offsets, int64_t
         cap = (unsigned int)std::min<unsigned long long>(0x7fffffffull, (unsigned long long)vc.n_instances + 1024);
     }
     if (vc.overflow) return fail(FS_ENOMEM, "fs_bin: instance buffer overflow");
-    return copy_tile_lists(w, ntiles, vc.n_valid, tile_offsets, items, items_capacity, n_items);
+    if ((rc = copy_tile_lists(w, ntiles, vc.n_valid, tile_offsets, items, items_capacity, n_items)))
+        return rc;
+    if (items && scene_perm(ctx) && vc.n_valid) {  // slots -> input ids
+        std::vector<unsigned int> perm((size_t)ctx->n);
+        CK(sync_copy(perm.data(), ctx->perm, sizeof(unsigned int) * perm.size(),
+                     cudaMemcpyDeviceToHost, w.stream));
+        for (unsigned int i = 0; i < vc.n_valid; ++i) items[i] = perm[(size_t)items[i]];
+    }
+    return FS_OK;
 }
 
 int fs_bin_splats(fs_context* ctx, int64_t k, const double* mean2d, const double* depth,
@@ -1448,9 +1488,10 @@ int fs_member_counts(fs_context* ctx, const uint8_t* m, int64_t n, int rows, int
 // ---------------------------------------------------------------- rendering
 namespace {
 
+// perm: the scene's slot -> input id map (scene renders), nullptr for splat lists
 fs::RasterArgs render_args(fs::Work& w, int width, int height, double alpha_floor,
                            double t_floor, double* out, int channels, const double* ch_dev,
-                           long long n_ids) {
+                           long long n_ids, const unsigned int* perm = nullptr) {
     const int tx = fs::tiles_x_of(width), ntiles = tx * fs::tiles_y_of(height);
     const size_t px = (size_t)width * height;
     fs::RasterArgs ra{};
@@ -1462,7 +1503,7 @@ fs::RasterArgs render_args(fs::Work& w, int width, int height, double alpha_floo
     ra.n_gaussians = n_ids;  // gids index the records / channel
     ra.af_eff = alpha_floor > 0.0 ? alpha_floor : -1.0;  // rasterizer.py:181-182
     ra.tf_eff = t_floor > 0.0 ? t_floor : -1.0;          // rasterizer.py:193-194
-    ra.sort = tile_sort_args(w);
+    ra.sort = tile_sort_args(w, perm);
     ra.r32 = w.r32;
     ra.r64 = w.r64;
     ra.vc = w.vc;
@@ -1493,7 +1534,7 @@ int render_scene_device(fs_context* ctx, const fs_camera* cam, const uint8_t* me
         ex.member = member_dev;
         enqueue_bin(ctx, w, to_cam(*cam), alpha_floor, 1, ex);
         fs::launch_raster_render(render_args(w, cam->width, cam->height, alpha_floor, t_floor, out,
-                                             channels, ch_dev, ctx->n),
+                                             channels, ch_dev, ctx->n, scene_perm(ctx)),
                                  w.stream);
         CK(cudaGetLastError());
         fs::ViewCounters vc{};
@@ -1526,11 +1567,12 @@ __global__ void mask_combine_kernel(const double* __restrict__ alpha,
 // Tile rectangles of one object's members (the others are never binned, like
 // project_scene(member_mask=...), scene.py:346-350).
 __global__ void member_rect_kernel(const unsigned long long* __restrict__ all,
-                                   const uint8_t* __restrict__ member, long long n,
+                                   const uint8_t* __restrict__ member,
+                                   const unsigned int* __restrict__ perm, long long n,
                                    unsigned long long* __restrict__ rect) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
-        rect[i] = member[i] ? all[i] : ~0ull;
+        rect[i] = member[perm ? perm[i] : i] ? all[i] : ~0ull;  // member is by input id
 }
 
 int check_render_cam(const fs_camera* cam) { return check_cam(*cam, 0); }
@@ -1712,10 +1754,11 @@ int fs_render_mask(fs_context* ctx, const fs_camera* cam, const uint8_t* members
         const int ngrid = (int)std::min<size_t>((n + 255) / 256, (size_t)ctx->num_sms * 8);
         const fs::RasterArgs ra = render_args(w, cam->width, cam->height, alpha_floor,
                                               transmittance_floor, ctx->rn_f64, 0, nullptr,
-                                              (long long)n);
+                                              (long long)n, scene_perm(ctx));
         for (int obj : objs) {
             member_rect_kernel<<<std::max(ngrid, 1), 256, 0, st>>>(
-                ctx->rn_rect, ctx->rn_member + (size_t)obj * n, (long long)n, w.rect);
+                ctx->rn_rect, ctx->rn_member + (size_t)obj * n, scene_perm(ctx), (long long)n,
+                w.rect);
             fs::launch_bin(ntiles, tx, bin_buffers(w, (int)n, w.vc), w.vc, ctx->num_sms, st);
             CK(cudaMemsetAsync(ctx->rn_f64, 0, sizeof(double) * 2 * px, st));
             fs::launch_raster_render(ra, st);

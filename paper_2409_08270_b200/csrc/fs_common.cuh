@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 // Device-side bounds / invariant checks, compiled in only for the checked build
@@ -49,12 +50,27 @@ struct Camera {
     double near_clip;
 };
 
-// float32 screen record of one projected Gaussian (32 B, one per gid).
+// float32 screen record of one projected Gaussian (32 B, one per scene slot).
 // cut: power threshold below which alpha < alpha_floor for sure;
-// hx, hy: half extents of the alpha-floor ellipse (pixel units, inflated).
+// hxy: half extents (hx, hy) of the alpha-floor ellipse, pixel units, inflated
+//      and rounded UP to float16 (rec_hx / rec_hy: exact float32 values, the
+//      same ones for the binning's tile cull and the raster's strip test);
+// oid: the Gaussian's input id (accumulator row, channel row) -- scenes are
+//      stored in spatial order (fs_order.cu), so it differs from the slot.
 struct __align__(16) Rec32 {
-    float mx, my, a, b, c, cut, hx, hy;
+    float mx, my, a, b, c, cut;
+    unsigned int hxy, oid;
 };
+__device__ __forceinline__ unsigned int pack_hxy(float hx, float hy) {
+    const __half2 h = __halves2half2(__float2half_ru(hx), __float2half_ru(hy));
+    return *reinterpret_cast<const unsigned int*>(&h);
+}
+__device__ __forceinline__ float rec_hx(const Rec32& s) {
+    return __half2float(__ushort_as_half((unsigned short)(s.hxy & 0xffffu)));
+}
+__device__ __forceinline__ float rec_hy(const Rec32& s) {
+    return __half2float(__ushort_as_half((unsigned short)(s.hxy >> 16)));
+}
 
 // float64 record used for the exact contribution (48 B, one per gid).
 struct __align__(16) Rec64 {
@@ -87,6 +103,8 @@ struct ProjectExport {
     int64_t* radius; // N
     const uint8_t* member;  // N, input, nullable: only members are binned (render subsets,
                             // project_scene(member_mask=...), scene.py:346-350)
+    const unsigned int* perm;  // nullable: scene slot p holds input Gaussian perm[p]
+                               // (fs_order.cu); exports and member are by input id
 };
 
 __host__ __device__ inline int tiles_x_of(int w) { return (w + kTile - 1) / kTile; }

@@ -28,11 +28,20 @@ constexpr int kPlyProps = 17;
 struct PlyOffsets {
     int k[kPlyProps];
 };
+// perm (nullable): slot p of the resident arrays takes input Gaussian perm[p]
 void launch_scene_setup_ply(int n, const float* verts, int stride, const PlyOffsets& off,
-                            double* mx, double* my, double* mz, double* sig, double* opac,
-                            unsigned long long* bad, double* params, cudaStream_t st);
+                            const unsigned int* perm, double* mx, double* my, double* mz,
+                            double* sig, double* opac, unsigned long long* bad, double* params,
+                            cudaStream_t st);
 void launch_scene_setup(int n, const double* means, const double* quats, const double* scales,
-                        double* mx, double* my, double* mz, double* sig, cudaStream_t st);
+                        const double* opac_in, const unsigned int* perm, double* mx, double* my,
+                        double* mz, double* sig, double* opac, cudaStream_t st);
+// ---- fs_order.cu ----
+// Spatial (Morton) order of the scene: perm[p] = input id of slot p.
+cudaError_t launch_scene_order(int n, const double* means_aos, unsigned int* perm, int num_sms,
+                               cudaStream_t st);
+cudaError_t launch_scene_order_ply(int n, const float* verts, int stride, const PlyOffsets& off,
+                                   unsigned int* perm, int num_sms, cudaStream_t st);
 void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
                     int cull_floor, unsigned long long* keys, unsigned long long* rect,

@@ -51,18 +51,25 @@ __device__ __forceinline__ void store_covariance(double w, double x, double y, d
 
 // K0: AoS host layout (means N x 3, unit quats N x 4, scales N x 3) -> SoA
 // means + world covariance Sigma = (R S)(R S)^T (scene.py:228-249).
+// Slot p of the resident arrays takes input Gaussian i = perm[p] (spatial order,
+// fs_order.cu; perm == nullptr: input order).
 __global__ void scene_setup_kernel(int n, const double* __restrict__ means_aos,
                                    const double* __restrict__ quats_aos,
-                                   const double* __restrict__ scales_aos, double* __restrict__ mx,
+                                   const double* __restrict__ scales_aos,
+                                   const double* __restrict__ opac_in,
+                                   const unsigned int* __restrict__ perm, double* __restrict__ mx,
                                    double* __restrict__ my, double* __restrict__ mz,
-                                   double* __restrict__ sig /* 6 x n */) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        mx[i] = means_aos[3 * i + 0];
-        my[i] = means_aos[3 * i + 1];
-        mz[i] = means_aos[3 * i + 2];
+                                   double* __restrict__ sig /* 6 x n */,
+                                   double* __restrict__ opac) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const size_t i = perm ? perm[p] : (unsigned int)p;
+        opac[p] = opac_in[i];
+        mx[p] = means_aos[3 * i + 0];
+        my[p] = means_aos[3 * i + 1];
+        mz[p] = means_aos[3 * i + 2];
         store_covariance(quats_aos[4 * i + 0], quats_aos[4 * i + 1], quats_aos[4 * i + 2],
                          quats_aos[4 * i + 3], scales_aos[3 * i + 0], scales_aos[3 * i + 1],
-                         scales_aos[3 * i + 2], sig, (size_t)n, i);
+                         scales_aos[3 * i + 2], sig, (size_t)n, p);
     }
 }
 
@@ -81,13 +88,16 @@ __global__ void scene_setup_kernel(int n, const double* __restrict__ means_aos,
 // category that fired.  off[] = float offsets within a record, in the
 // reference's REQUIRED_PROPERTIES order (x y z nx ny nz f_dc_0..2 opacity
 // scale_0..2 rot_0..3).
+// Slot p takes vertex i = perm[p]; bad[] and params are by vertex index.
 __global__ void scene_setup_ply_kernel(int n, const float* __restrict__ verts, int stride,
-                                       PlyOffsets off, double* __restrict__ mx,
-                                       double* __restrict__ my, double* __restrict__ mz,
-                                       double* __restrict__ sig, double* __restrict__ opac,
+                                       PlyOffsets off, const unsigned int* __restrict__ perm,
+                                       double* __restrict__ mx, double* __restrict__ my,
+                                       double* __restrict__ mz, double* __restrict__ sig,
+                                       double* __restrict__ opac,
                                        unsigned long long* __restrict__ bad,
                                        double* __restrict__ params /* nullable: n x 8 */) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const unsigned int i = perm ? perm[p] : (unsigned int)p;
         const float* rec = verts + (size_t)i * stride;
         float v[kPlyProps];
         bool finite = true;
@@ -100,9 +110,9 @@ __global__ void scene_setup_ply_kernel(int n, const float* __restrict__ verts, i
             atomicMin(&bad[0], (unsigned long long)i);
             continue;
         }
-        mx[i] = (double)v[0];
-        my[i] = (double)v[1];
-        mz[i] = (double)v[2];
+        mx[p] = (double)v[0];
+        my[p] = (double)v[1];
+        mz[p] = (double)v[2];
         const double s0 = exp((double)v[10]), s1 = exp((double)v[11]), s2 = exp((double)v[12]);
         const double o = 1.0 / (1.0 + exp(-(double)v[9]));
         const double q0 = (double)v[13], q1 = (double)v[14], q2 = (double)v[15], q3 = (double)v[16];
@@ -110,9 +120,9 @@ __global__ void scene_setup_ply_kernel(int n, const float* __restrict__ verts, i
         if (!(norm > 0.0) || !isfinite(norm)) atomicMin(&bad[1], (unsigned long long)i);
         if (!(s0 > 0.0 && s1 > 0.0 && s2 > 0.0)) atomicMin(&bad[2], (unsigned long long)i);
         if (!(o >= 0.0 && o <= 1.0)) atomicMin(&bad[3], (unsigned long long)i);
-        opac[i] = o;
+        opac[p] = o;
         const double w = q0 / norm, x = q1 / norm, y = q2 / norm, z = q3 / norm;
-        store_covariance(w, x, y, z, s0, s1, s2, sig, (size_t)n, i);
+        store_covariance(w, x, y, z, s0, s1, s2, sig, (size_t)n, p);
         if (params) {  // the activated GaussianScene parameters, for verification
             double* p = params + 8 * (size_t)i;
             p[0] = s0; p[1] = s1; p[2] = s2; p[3] = o;
@@ -137,8 +147,9 @@ __device__ __forceinline__ void warp_or_and(unsigned long long& o, unsigned long
 // 0.02 margins, so the screen stays conservative.
 __device__ __forceinline__ Rec32 screen_record(double mx, double my, double ia, double ib,
                                                double ic, double ca, double cc, double o,
-                                               double alpha_floor, bool alive) {
+                                               double alpha_floor, bool alive, unsigned int oid) {
     Rec32 s;
+    s.oid = oid;
     s.mx = (float)mx;
     s.my = (float)my;
     s.a = (float)ia;
@@ -157,16 +168,13 @@ __device__ __forceinline__ Rec32 screen_record(double mx, double my, double ia, 
                              (hx * hx + hy * hy);
         const float margin = 0.02f + 1e-6f * spread;
         s.cut = -L - margin;
-        s.hx = hx;
-        s.hy = hy;
+        s.hxy = pack_hxy(hx, hy);  // rounded up: still conservative
     } else if (alpha_floor > 0.0) {
         s.cut = __int_as_float(0x7f800000);  // +inf: never passes
-        s.hx = 0.0f;
-        s.hy = 0.0f;
+        s.hxy = pack_hxy(0.0f, 0.0f);
     } else {
         s.cut = __int_as_float(0xff800000);  // -inf: exact blend, no screen
-        s.hx = __int_as_float(0x7f800000);
-        s.hy = __int_as_float(0x7f800000);
+        s.hxy = pack_hxy(INFINITY, INFINITY);
     }
     return s;
 }
@@ -181,8 +189,9 @@ __device__ __forceinline__ Rec32 screen_record(double mx, double my, double ia, 
 // such samples no weight and no transmittance update, contributions.py:148).
 // Exact blend (hx = +inf) keeps the rectangle.  C2: 22% fewer instances.
 __device__ __forceinline__ unsigned long long floor_box_rect(unsigned long long rc, const Rec32& s) {
-    if (rc == ~0ull || !(s.hx < INFINITY) || !(s.hy < INFINITY)) return rc;
-    const float lx = s.mx - s.hx, hx = s.mx + s.hx, ly = s.my - s.hy, hy = s.my + s.hy;
+    const float shx = rec_hx(s), shy = rec_hy(s);
+    if (rc == ~0ull || !(shx < INFINITY) || !(shy < INFINITY)) return rc;
+    const float lx = s.mx - shx, hx = s.mx + shx, ly = s.my - shy, hy = s.my + shy;
     // exact in float64: float + half-integer, then a power-of-two divide
     const double bx0 = ceil(((double)lx - 15.5) / 16.0), bx1 = floor(((double)hx - 0.5) / 16.0);
     const double by0 = ceil(((double)ly - 15.5) / 16.0), by1 = floor(((double)hy - 0.5) / 16.0);
@@ -225,6 +234,9 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
     for (int it = 0; it < iters; ++it) {
         const int i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
         if (i < n) {
+            // slot i holds input Gaussian ex.perm[i]: member, exports and the
+            // record's oid are by input id
+            const unsigned int gin = ex.perm ? ex.perm[i] : (unsigned int)i;
             double m0 = gmx[i], m1 = gmy[i], m2 = gmz[i];
             // cam = means @ rot.T + t   (scene.py:266)
             double x = (m0 * W[0] + m1 * W[1] + m2 * W[2]) + W[3];
@@ -288,7 +300,7 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
             }
             double o = opac[i];
             unsigned long long key = ~0ull, rc = ~0ull;
-            if (ex.member && !ex.member[i]) alive = false;  // not in the rendered subset
+            if (ex.member && !ex.member[gin]) alive = false;  // not in the rendered subset
             if (alive) {
                 ++c_emit;
                 key = f64_sort_key(z);
@@ -308,20 +320,20 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
             q.c = ic;
             q.o = o;
             r64[i] = q;
-            const Rec32 s = screen_record(mxp, myp, ia, ib, ic, a, c, o, alpha_floor, alive);
+            const Rec32 s = screen_record(mxp, myp, ia, ib, ic, a, c, o, alpha_floor, alive, gin);
             r32[i] = s;
             // binning for a floored walk: only tiles the raster's strip test can accept
             if (cull_floor && alpha_floor > 0.0) rc = floor_box_rect(rc, s);
             rect[i] = rc;
             if (ex.alive) {
-                ex.alive[i] = alive ? 1 : 0;
-                ex.mean2d[2 * i] = mxp;
-                ex.mean2d[2 * i + 1] = myp;
-                ex.conic[3 * i] = ia;
-                ex.conic[3 * i + 1] = ib;
-                ex.conic[3 * i + 2] = ic;
-                ex.depth[i] = z;
-                ex.radius[i] = (int64_t)rad;
+                ex.alive[gin] = alive ? 1 : 0;
+                ex.mean2d[2 * (size_t)gin] = mxp;
+                ex.mean2d[2 * (size_t)gin + 1] = myp;
+                ex.conic[3 * (size_t)gin] = ia;
+                ex.conic[3 * (size_t)gin + 1] = ib;
+                ex.conic[3 * (size_t)gin + 2] = ic;
+                ex.depth[gin] = z;
+                ex.radius[gin] = (int64_t)rad;
             }
         }
     }
@@ -365,21 +377,24 @@ __global__ void view_begin_kernel(ViewCounters* vc) {
 void launch_view_begin(ViewCounters* vc, cudaStream_t st) { view_begin_kernel<<<1, 32, 0, st>>>(vc); }
 
 void launch_scene_setup(int n, const double* means, const double* quats, const double* scales,
-                        double* mx, double* my, double* mz, double* sig, cudaStream_t st) {
+                        const double* opac_in, const unsigned int* perm, double* mx, double* my,
+                        double* mz, double* sig, double* opac, cudaStream_t st) {
     if (n <= 0) return;
     int grid = (n + 255) / 256;
     if (grid > 4096) grid = 4096;
-    scene_setup_kernel<<<grid, 256, 0, st>>>(n, means, quats, scales, mx, my, mz, sig);
+    scene_setup_kernel<<<grid, 256, 0, st>>>(n, means, quats, scales, opac_in, perm, mx, my, mz,
+                                             sig, opac);
 }
 
 void launch_scene_setup_ply(int n, const float* verts, int stride, const PlyOffsets& off,
-                            double* mx, double* my, double* mz, double* sig, double* opac,
-                            unsigned long long* bad, double* params, cudaStream_t st) {
+                            const unsigned int* perm, double* mx, double* my, double* mz,
+                            double* sig, double* opac, unsigned long long* bad, double* params,
+                            cudaStream_t st) {
     if (n <= 0) return;
     int grid = (n + 255) / 256;
     if (grid > 4096) grid = 4096;
-    scene_setup_ply_kernel<<<grid, 256, 0, st>>>(n, verts, stride, off, mx, my, mz, sig, opac, bad,
-                                                 params);
+    scene_setup_ply_kernel<<<grid, 256, 0, st>>>(n, verts, stride, off, perm, mx, my, mz, sig, opac,
+                                                 bad, params);
 }
 
 void launch_project(int n, const double* mx, const double* my, const double* mz,
@@ -420,14 +435,13 @@ __global__ void splat_records_kernel(int k, const double* __restrict__ mean2d,
         r64[i] = q;
         const double det = ia * ic - ib * ib;  // conic = inverse covariance
         const bool ok = det > 0.0;
-        r32[i] = screen_record(mx, my, ia, ib, ic, ok ? ic / det : 0.0, ok ? ia / det : 0.0, o,
-                               alpha_floor, true);
+        Rec32 s = screen_record(mx, my, ia, ib, ic, ok ? ic / det : 0.0, ok ? ia / det : 0.0, o,
+                                alpha_floor, true, (unsigned int)i);  // oid: the splat (channel row)
         if (!ok && alpha_floor > 0.0) {  // degenerate conic: no finite screen box
-            Rec32 s = r32[i];
             s.cut = __int_as_float(0xff800000);
-            s.hx = s.hy = __int_as_float(0x7f800000);
-            r32[i] = s;
+            s.hxy = pack_hxy(INFINITY, INFINITY);
         }
+        r32[i] = s;
         k64[i] = f64_sort_key(depth[i]);
     }
 }

@@ -63,7 +63,8 @@ static_assert(kBW == 8 || kBW == 16, "warp pixel blocks are 2 x 16 or 4 x 8");
 struct WarpSmem {
     Rec64 rec[kMini];        // float64 records of the mini-batch's hits
     unsigned int cm[kRing];  // candidate pixels of the hit (bit = lane)
-    unsigned int gid[kRing];
+    unsigned int gid[kRing];  // scene slot of the hit (record index)
+    unsigned int oid[kRing];  // its input Gaussian id (accumulator / channel row, Rec32::oid)
     unsigned short queue[kMini * 32];
     unsigned int gmask[kMaxGroups];  // the warp's label groups (fixed for the walk)
     unsigned int glab[kMaxGroups];
@@ -273,8 +274,8 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
         }
         if (idx + 64 < n_list) g_next2 = list[idx + 64];
         if (idx < n_list) {
-            if (!(u_hi < s.mx - s.hx || u_lo > s.mx + s.hx || v_hi < s.my - s.hy ||
-                  v_lo > s.my + s.hy)) {
+            const float hx = rec_hx(s), hy = rec_hy(s);
+            if (!(u_hi < s.mx - hx || u_lo > s.mx + hx || v_hi < s.my - hy || v_lo > s.my + hy)) {
                 cand = block_candidates(s, v_lo, xb);
             }
         }
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
             const int slot = (head + cnt + __popc(bal & lt_mask)) & (kRing - 1);
             W.cm[slot] = cand;
             W.gid[slot] = g;
+            W.oid[slot] = s.oid;
         }
         cnt += __popc(bal);
         __syncwarp();
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                             if (kRender) {
                                 // rasterizer.py:184-191, summed in list order per pixel
                                 const unsigned int g = W.gid[(head + k) & (kRing - 1)];
+                                const size_t gi = W.oid[(head + k) & (kRing - 1)];  // by input id
                                 const double z = depth_of_key(a.sort.keys.k64[g]);
                                 r_acc = __dadd_rn(r_acc, w);
                                 d_acc = __dadd_rn(d_acc, __dmul_rn(z, w));
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                                     if (ch < n_ch)
                                         v_acc[ch] = __dadd_rn(
                                             v_acc[ch],
-                                            __dmul_rn(w, a.render.channel[(size_t)g * n_ch + ch]));
+                                            __dmul_rn(w, a.render.channel[gi * n_ch + ch]));
                             }
                         }
                         myval[k * kRowStride + lane] = w;
@@ -395,10 +398,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         const double w = __dmul_rn(alpha, T);              // :150
                         T = __dmul_rn(T, __dsub_rn(1.0, alpha));           // :155
                         if (w > 0.0 && lbl_ok) {
-                            FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians);
-                            acc_add<kFixed>(acc, acc_fx,
-                                            (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + label,
-                                            w);
+                            const unsigned int row = W.oid[(head + k) & (kRing - 1)];
+                            FS_CHECK(row < (unsigned)a.n_gaussians);
+                            acc_add<kFixed>(acc, acc_fx, (size_t)row * n_obj + label, w);
                             ++atom;
                         }
                         if (T < tf_eff) {                                   // :156-157
@@ -427,9 +429,9 @@ __global__ void __launch_bounds__(kThreads, 4) raster_kernel(RasterArgs a) {
                         for (int o = kMini; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                         const bool fire = lane < kMini && k < nm && v > 0.0 && gl < (unsigned)a.num_objects;
                         if (fire) {
-                            FS_CHECK(W.gid[(head + k) & (kRing - 1)] < (unsigned)a.n_gaussians);
-                            acc_add<kFixed>(acc, acc_fx,
-                                            (size_t)W.gid[(head + k) & (kRing - 1)] * n_obj + gl, v);
+                            const unsigned int row = W.oid[(head + k) & (kRing - 1)];
+                            FS_CHECK(row < (unsigned)a.n_gaussians);
+                            acc_add<kFixed>(acc, acc_fx, (size_t)row * n_obj + gl, v);
                             ++atom;
                         }
                     }
