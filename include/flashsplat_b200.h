@@ -121,7 +121,10 @@ int fs_set_timing(fs_context *ctx, int enable);
 
 /* Upload a GaussianScene (scene.py:71-110, arrays already validated and the
  * quaternions normalised).  Replaces the per-view f64 input handling of
- * _project_arrays (scene.py:252-278). */
+ * _project_arrays (scene.py:252-278).  The resident copy is stored in spatial
+ * (Morton) order for locality; every output of every entry point -- tile
+ * lists, exports, accumulator rows, labels -- stays indexed by the caller's
+ * Gaussian index (set FS_SCENE_ORDER=0 in the environment to keep input order). */
 int fs_set_scene(fs_context *ctx, int64_t n, const double *means, const double *quats,
                  const double *scales, const double *opacities);
 
