@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--views", type=int, default=None, help="override the view count")
     ap.add_argument("--gaussians", type=int, default=None, help="override the Gaussian count")
-    ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--streams", type=int, default=6)
     ap.add_argument("--iid", action="store_true",
                     help="worst case: iid uniform labels per pixel instead of object silhouettes")
     ap.add_argument("--no-e2e", action="store_true")
@@ -477,7 +477,7 @@ def main():
         return
 
     # ---- roofline of the dominant kernel (raster-accumulate) ----
-    # The timed steps overlap views on 4 streams, so per-kernel event times
+    # The timed steps overlap views on several streams, so per-kernel event times
     # there include other streams' work.  The kernel's own duration is taken
     # from one more (untimed for `value`) pass on a 1-stream context with CUDA
     # events around every raster launch on its stream.

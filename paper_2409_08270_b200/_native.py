@@ -211,7 +211,7 @@ class DeviceBuffer:
 class Context:
     """fs_context: one device, its streams, workspaces and the resident scene."""
 
-    def __init__(self, device: int = 0, streams: int = 4):
+    def __init__(self, device: int = 0, streams: int = 6):
         L = load()
         h = ctypes.c_void_p()
         rc = L.fs_create(int(device), int(streams), ctypes.byref(h))
