@@ -369,3 +369,42 @@ def test_multi_device_instance_overflow_retry():
     ref = oracle.accumulate(scene.means, scene.rotations, scene.scales, scene.opacities, cams,
                             [m.labels for _, m in pairs], 2, threads=8)
     np.testing.assert_allclose(out, ref, rtol=1e-6, atol=1e-9)
+
+
+def test_spatial_scene_order_is_invisible(monkeypatch):
+    """The resident scene is stored in Morton order (fs_order.cu); FS_SCENE_ORDER=0
+    keeps input order.  Both must give the same results: bit-identical fixed-point
+    matrices and labels, identical tile lists and projection exports, identical
+    renders and scene masks."""
+    from paper_2409_08270_b200 import Assignment, render_scene_mask, render_view
+    wl = _workload(seed=36, n=20000, views=4, w=160, h=120, e=3)
+    pairs = wl.pairs()
+    ctx = _native.context(0)
+    rng = np.random.default_rng(15)
+    ch = rng.random((len(wl.scene), 3))
+    memb = np.zeros((3, len(wl.scene)), np.uint8)
+    memb[rng.integers(0, 3, len(wl.scene)), np.arange(len(wl.scene))] = 1
+    out = {}
+    for order in ("1", "0"):
+        monkeypatch.setenv("FS_SCENE_ORDER", order)
+        ctx._scene_key = None  # re-upload under this setting
+        M, asn = solve(wl.scene, pairs, 3, 0.2, "scene")
+        with ctx.lock:
+            ctx.set_scene(wl.scene)
+            proj = ctx.project(wl.views[0])
+            offs, items = ctx.bin(wl.views[0])
+        r = render_view(wl.scene, wl.views[0], ch)
+        mask = render_scene_mask(wl.scene, Assignment(mode="scene", gamma=0.0, membership=memb),
+                                 wl.views[0], 0.3).labels
+        out[order] = (M.values, asn.membership, proj, offs, items, r, mask)
+        ctx._scene_key = None
+    a, b = out["1"], out["0"]
+    assert a[0].tobytes() == b[0].tobytes() and a[0].sum() > 0
+    assert np.array_equal(a[1], b[1])
+    for k in range(5):
+        assert np.array_equal(a[2][k], b[2][k]), k
+    assert list(a[2][5]) == list(b[2][5])
+    assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+    assert np.array_equal(a[5].alpha, b[5].alpha) and np.array_equal(a[5].depth, b[5].depth)
+    assert np.array_equal(a[5].value, b[5].value)
+    assert np.array_equal(a[6], b[6])
