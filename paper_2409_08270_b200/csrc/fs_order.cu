@@ -96,6 +96,12 @@ __global__ void bbox_init_kernel(unsigned long long* box) {
     if (threadIdx.x < 6) box[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
 }
 
+#ifndef FS_MORTON_BITS
+#define FS_MORTON_BITS 10  // per axis (<= 10: 30-bit codes)
+#endif
+constexpr int kBits = FS_MORTON_BITS;
+constexpr double kCells = (double)((1 << kBits) - 1);
+
 // 10 bits -> every third bit of 30
 __device__ __forceinline__ unsigned int spread3(unsigned int x) {
     x &= 0x3ffu;
@@ -114,7 +120,7 @@ __global__ void morton_kernel(int n, MeanSource src, const unsigned long long* _
         const bool any = box[a] <= box[3 + a];
         lo[a] = any ? val_of(box[a]) : 0.0;
         const double ext = any ? val_of(box[3 + a]) - lo[a] : 0.0;
-        scale[a] = ext > 0.0 ? 1023.0 / ext : 0.0;
+        scale[a] = ext > 0.0 ? kCells / ext : 0.0;
     }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         double c[3];
@@ -123,7 +129,7 @@ __global__ void morton_kernel(int n, MeanSource src, const unsigned long long* _
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const double t = (c[a] - lo[a]) * scale[a];  // NaN / inf clamp below
-            q[a] = t >= 1023.0 ? 1023u : (t > 0.0 ? (unsigned int)t : 0u);
+            q[a] = t >= kCells ? (unsigned int)kCells : (t > 0.0 ? (unsigned int)t : 0u);
         }
         code[i] = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
         idx[i] = (unsigned int)i;
@@ -137,7 +143,7 @@ cudaError_t order_from(int n, MeanSource src, unsigned int* perm, int num_sms, c
     void* temp = nullptr;
     size_t temp_bytes = 0;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, code, code_sorted, idx,
-                                                    perm, n, 0, 30, st);
+                                                    perm, n, 0, 3 * kBits, st);
     if (e != cudaSuccess) return e;
     const size_t n1 = (size_t)n;
     if ((e = cudaMallocAsync(reinterpret_cast<void**>(&box), 6 * sizeof(unsigned long long), st)) ||
@@ -153,7 +159,7 @@ cudaError_t order_from(int n, MeanSource src, unsigned int* perm, int num_sms, c
     morton_kernel<<<grid, 256, 0, st>>>(n, src, box, code, idx);
     if ((e = cudaGetLastError())) return e;
     if ((e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, code, code_sorted, idx, perm, n, 0,
-                                             30, st)))
+                                             3 * kBits, st)))
         return e;
     cudaFreeAsync(box, st);
     cudaFreeAsync(code, st);
