@@ -430,8 +430,7 @@ def main():
         if group is not None:
             dist.barrier()
         # each solve timed on its own (events around it); the line reports the
-        # median solve -- a host-side stall in one solve (seen once in ~40 runs:
-        # 0.7 s) should not stand for the path -- next to the mean and every rep
+        # median solve next to the mean and every rep
         rep_s = []
         for _ in range(reps):
             ctx_cached = _native.context(local)

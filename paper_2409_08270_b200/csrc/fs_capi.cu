@@ -123,6 +123,8 @@ struct fs_context {
     // (FS_SCENE_ORDER=0, for A/B measurements)
     unsigned int* perm = nullptr;
     bool perm_on = false;
+    void* order_scratch = nullptr;  // Morton codes + radix-sort scratch (grow-only)
+    size_t order_scratch_bytes = 0;
     double* up_opac = nullptr;    // opacity staging (permuted by the setup kernel)
     double* up_means = nullptr;   // AoS staging of the scene upload
     double* up_quats = nullptr;
@@ -417,6 +419,18 @@ fs::BinBuffers bin_buffers(fs::Work& w, int n, fs::ViewCounters* vc = nullptr) {
 
 // The resident scene's slot -> input id map, or nullptr when it is in input order.
 const unsigned int* scene_perm(const fs_context* ctx) { return ctx->perm_on ? ctx->perm : nullptr; }
+
+// Grow-only scratch of the scene-order step (no per-call device allocation).
+int ensure_order_scratch(fs_context* ctx, long long n) {
+    const size_t need = fs::scene_order_scratch_bytes((int)n);
+    if (need <= ctx->order_scratch_bytes) return FS_OK;
+    if (ctx->order_scratch) CK(cudaFree(ctx->order_scratch));
+    ctx->order_scratch = nullptr;
+    ctx->order_scratch_bytes = 0;
+    CK(cudaMalloc(&ctx->order_scratch, need));
+    ctx->order_scratch_bytes = need;
+    return FS_OK;
+}
 
 // Spatial scene order (fs_order.cu) unless FS_SCENE_ORDER=0.
 bool scene_order_enabled() {
@@ -837,6 +851,14 @@ int fs_create(int device, int n_streams, fs_context** out) {
                               "B200 (sm_100a) only", device, prop.name, prop.major, prop.minor);
     }
     ctx->num_sms = prop.multiProcessorCount;
+    // fs_assign's stream-ordered scratch (cudaMallocAsync) comes from the device's
+    // default pool; keep freed blocks there instead of trimming them back at every
+    // synchronisation -- re-mapping trimmed memory stalled calls for up to 0.8 s
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        unsigned long long keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     e = fs::raster_configure();
     if (e == cudaSuccess) e = fs::bin_configure();
     if (e != cudaSuccess) {
@@ -866,7 +888,7 @@ void fs_destroy(fs_context* ctx) {
     for (void* p : {(void*)ctx->mx, (void*)ctx->my, (void*)ctx->mz, (void*)ctx->sig,
                     (void*)ctx->opac, (void*)ctx->view_log,
                     (void*)ctx->up_means, (void*)ctx->up_quats, (void*)ctx->up_scales,
-                    (void*)ctx->up_opac, (void*)ctx->perm,
+                    (void*)ctx->up_opac, (void*)ctx->perm, ctx->order_scratch,
                     (void*)ctx->rn_f64, (void*)ctx->rn_in, (void*)ctx->rn_member,
                     (void*)ctx->rn_u32, (void*)ctx->rn_labels, (void*)ctx->rn_rect,
                     (void*)ctx->cnt})
@@ -1028,7 +1050,11 @@ int fs_set_scene(fs_context* ctx, int64_t n, const double* means, const double* 
         (rc = upload(ctx, ctx->up_opac, opacities, 8 * (size_t)n, st)))
         return rc;
     ctx->perm_on = scene_order_enabled();
-    if (ctx->perm_on) CK(fs::launch_scene_order((int)n, ctx->up_means, ctx->perm, ctx->num_sms, st));
+    if (ctx->perm_on) {
+        if ((rc = ensure_order_scratch(ctx, n))) return rc;
+        CK(fs::launch_scene_order((int)n, ctx->up_means, ctx->perm, ctx->order_scratch,
+                                  ctx->order_scratch_bytes, ctx->num_sms, st));
+    }
     fs::launch_scene_setup((int)n, ctx->up_means, ctx->up_quats, ctx->up_scales, ctx->up_opac,
                            scene_perm(ctx), ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, st);
     CK(cudaGetLastError());
@@ -1076,9 +1102,12 @@ int fs_set_scene_ply(fs_context* ctx, int64_t n, const void* verts, int stride_f
     double* dparams = nullptr;
     if (params) CK(cudaMallocAsync(reinterpret_cast<void**>(&dparams), 64 * (size_t)n, st));
     ctx->perm_on = scene_order_enabled();
-    if (ctx->perm_on)
+    if (ctx->perm_on) {
+        if ((rc = ensure_order_scratch(ctx, n))) return rc;
         CK(fs::launch_scene_order_ply((int)n, ctx->ply_raw, stride_floats, off, ctx->perm,
-                                      ctx->num_sms, st));
+                                      ctx->order_scratch, ctx->order_scratch_bytes, ctx->num_sms,
+                                      st));
+    }
     fs::launch_scene_setup_ply((int)n, ctx->ply_raw, stride_floats, off, scene_perm(ctx), ctx->mx,
                                ctx->my, ctx->mz, ctx->sig, ctx->opac, ctx->ply_bad, dparams, st);
     CK(cudaGetLastError());

@@ -37,11 +37,14 @@ void launch_scene_setup(int n, const double* means, const double* quats, const d
                         const double* opac_in, const unsigned int* perm, double* mx, double* my,
                         double* mz, double* sig, double* opac, cudaStream_t st);
 // ---- fs_order.cu ----
-// Spatial (Morton) order of the scene: perm[p] = input id of slot p.
-cudaError_t launch_scene_order(int n, const double* means_aos, unsigned int* perm, int num_sms,
-                               cudaStream_t st);
+// Spatial (Morton) order of the scene: perm[p] = input id of slot p.  scratch:
+// a device buffer of scene_order_scratch_bytes(n) bytes owned by the caller.
+size_t scene_order_scratch_bytes(int n);
+cudaError_t launch_scene_order(int n, const double* means_aos, unsigned int* perm, void* scratch,
+                               size_t scratch_bytes, int num_sms, cudaStream_t st);
 cudaError_t launch_scene_order_ply(int n, const float* verts, int stride, const PlyOffsets& off,
-                                   unsigned int* perm, int num_sms, cudaStream_t st);
+                                   unsigned int* perm, void* scratch, size_t scratch_bytes,
+                                   int num_sms, cudaStream_t st);
 void launch_project(int n, const double* mx, const double* my, const double* mz,
                     const double* sig, const double* opac, const Camera& cam, double alpha_floor,
                     int cull_floor, unsigned long long* keys, unsigned long long* rect,

@@ -136,50 +136,59 @@ __global__ void morton_kernel(int n, MeanSource src, const unsigned long long* _
     }
 }
 
-cudaError_t order_from(int n, MeanSource src, unsigned int* perm, int num_sms, cudaStream_t st) {
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t cub_temp_bytes(int n) {
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (unsigned int*)nullptr, (unsigned int*)nullptr,
+                                    (unsigned int*)nullptr, (unsigned int*)nullptr, n, 0,
+                                    3 * kBits);
+    return temp;
+}
+
+// Scratch carved from one caller-owned device buffer (grow-only in the context):
+// per-call cudaMallocAsync / cudaFreeAsync here stalled whole solves for up to
+// 0.8 s now and then (pool trimming), so nothing is allocated per call.
+cudaError_t order_from(int n, MeanSource src, unsigned int* perm, void* scratch,
+                       size_t scratch_bytes, int num_sms, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    unsigned long long* box = nullptr;
-    unsigned int *code = nullptr, *code_sorted = nullptr, *idx = nullptr;
-    void* temp = nullptr;
-    size_t temp_bytes = 0;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, code, code_sorted, idx,
-                                                    perm, n, 0, 3 * kBits, st);
-    if (e != cudaSuccess) return e;
-    const size_t n1 = (size_t)n;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&box), 6 * sizeof(unsigned long long), st)) ||
-        (e = cudaMallocAsync(reinterpret_cast<void**>(&code), 4 * n1, st)) ||
-        (e = cudaMallocAsync(reinterpret_cast<void**>(&code_sorted), 4 * n1, st)) ||
-        (e = cudaMallocAsync(reinterpret_cast<void**>(&idx), 4 * n1, st)) ||
-        (e = cudaMallocAsync(&temp, temp_bytes, st)))
-        return e;
+    const size_t n4 = align256(4 * (size_t)n), temp_bytes = cub_temp_bytes(n);
+    if (scratch_bytes < 256 + 3 * n4 + temp_bytes) return cudaErrorInvalidValue;
+    char* p = static_cast<char*>(scratch);
+    auto* box = reinterpret_cast<unsigned long long*>(p);
+    auto* code = reinterpret_cast<unsigned int*>(p + 256);
+    auto* code_sorted = reinterpret_cast<unsigned int*>(p + 256 + n4);
+    auto* idx = reinterpret_cast<unsigned int*>(p + 256 + 2 * n4);
+    void* temp = p + 256 + 3 * n4;
+    size_t tb = temp_bytes;
     bbox_init_kernel<<<1, 32, 0, st>>>(box);
     int grid = (n + 255) / 256;
     if (grid > num_sms * 8) grid = num_sms * 8;
     bbox_kernel<<<grid, 256, 0, st>>>(n, src, box);
     morton_kernel<<<grid, 256, 0, st>>>(n, src, box, code, idx);
-    if ((e = cudaGetLastError())) return e;
-    if ((e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, code, code_sorted, idx, perm, n, 0,
-                                             3 * kBits, st)))
-        return e;
-    cudaFreeAsync(box, st);
-    cudaFreeAsync(code, st);
-    cudaFreeAsync(code_sorted, st);
-    cudaFreeAsync(idx, st);
-    return cudaFreeAsync(temp, st);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cub::DeviceRadixSort::SortPairs(temp, tb, code, code_sorted, idx, perm, n, 0, 3 * kBits,
+                                           st);
 }
 
 }  // namespace
 
-cudaError_t launch_scene_order(int n, const double* means_aos, unsigned int* perm, int num_sms,
-                               cudaStream_t st) {
+size_t scene_order_scratch_bytes(int n) {
+    return n <= 0 ? 0 : 256 + 3 * align256(4 * (size_t)n) + cub_temp_bytes(n);
+}
+
+cudaError_t launch_scene_order(int n, const double* means_aos, unsigned int* perm, void* scratch,
+                               size_t scratch_bytes, int num_sms, cudaStream_t st) {
     MeanSource src{means_aos, nullptr, 0, 0, 0, 0};
-    return order_from(n, src, perm, num_sms, st);
+    return order_from(n, src, perm, scratch, scratch_bytes, num_sms, st);
 }
 
 cudaError_t launch_scene_order_ply(int n, const float* verts, int stride, const PlyOffsets& off,
-                                   unsigned int* perm, int num_sms, cudaStream_t st) {
+                                   unsigned int* perm, void* scratch, size_t scratch_bytes,
+                                   int num_sms, cudaStream_t st) {
     MeanSource src{nullptr, verts, stride, off.k[0], off.k[1], off.k[2]};
-    return order_from(n, src, perm, num_sms, st);
+    return order_from(n, src, perm, scratch, scratch_bytes, num_sms, st);
 }
 
 }  // namespace fs
