@@ -392,7 +392,7 @@ class Context:
     def buffer(self, role: str, nbytes: int) -> "DeviceBuffer":
         """Grow-only device scratch owned by the context, keyed by role."""
         buf = self._buffers.get(role)
-        if buf is None or buf.nbytes < nbytes:
+        if buf is None or buf.ptr is None or buf.nbytes < nbytes:  # (re)allocate if released
             if buf is not None:
                 buf.release()
             buf = DeviceBuffer(self, max(int(nbytes), 1))

@@ -36,7 +36,6 @@ for rep in range(3):
     t0 = time.perf_counter()
     _native.assign(out, 0.0, _native.MODE_BINARY if E == 2 else _native.MODE_SCENE)
     t["assign_host"] = time.perf_counter() - t0
-    acc.release()
     s = LabelSolver(wl.scene)
     ctx._scene_key = None
     t0 = time.perf_counter()
