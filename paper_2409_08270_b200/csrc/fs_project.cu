@@ -311,20 +311,24 @@ __global__ void __launch_bounds__(256, 4) project_kernel(
                 if (!transparent) rc = tile_rect(mxp, myp, rad, tx_n, ty_n);
             }
             keys[i] = key;
-            // walk records (float64 exact, float32 screen)
-            Rec64 q;
-            q.mx = mxp;
-            q.my = myp;
-            q.a = ia;
-            q.b = ib;
-            q.c = ic;
-            q.o = o;
-            r64[i] = q;
             const Rec32 s = screen_record(mxp, myp, ia, ib, ic, a, c, o, alpha_floor, alive, gin);
-            r32[i] = s;
             // binning for a floored walk: only tiles the raster's strip test can accept
             if (cull_floor && alpha_floor > 0.0) rc = floor_box_rect(rc, s);
             rect[i] = rc;
+            // walk records (float64 exact, float32 screen) -- only for splats that are
+            // binned: culled and fully transparent ones are never read, so their 80 B
+            // are not written (views that see part of the scene skip most of them)
+            if (rc != ~0ull) {
+                Rec64 q;
+                q.mx = mxp;
+                q.my = myp;
+                q.a = ia;
+                q.b = ib;
+                q.c = ic;
+                q.o = o;
+                r64[i] = q;
+                r32[i] = s;
+            }
             if (ex.alive) {
                 ex.alive[gin] = alive ? 1 : 0;
                 ex.mean2d[2 * (size_t)gin] = mxp;
