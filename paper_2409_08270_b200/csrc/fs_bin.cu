@@ -291,7 +291,16 @@ __global__ void splat_keys_kernel(int k, const double* __restrict__ mean2d,
 
 }  // namespace
 
+// Most binning blocks a launch uses (the count matrix is sized for it): two
+// 1 024-thread blocks per SM when the binning has the GPU to itself.
 int bin_blocks(int num_sms) { return 2 * num_sms; }
+
+// Blocks for a binning that runs beside other streams' raster launches (the
+// accumulate view loop): a third of the SMs.  Fewer, longer blocks leave the
+// raster CTAs of the other views their SMs and shrink the count matrix the
+// scan walks -- C2 solve 70.0 -> 67.1 ms, C4 310 -> 303 ms against 2 per SM
+// (37-49 blocks best; 18 or fewer starve the binning).
+int bin_blocks_overlapped(int num_sms) { return std::max(1, num_sms / 3); }
 
 cudaError_t bin_configure() {
     const int bytes = (int)(kMaxTiles * sizeof(unsigned int));
@@ -304,8 +313,8 @@ cudaError_t bin_configure() {
 }
 
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
-                cudaStream_t st) {
-    const int g = bin_blocks(num_sms);
+                cudaStream_t st, int blocks) {
+    const int g = blocks > 0 ? std::min(blocks, bin_blocks(num_sms)) : bin_blocks(num_sms);
     // tile-row bands whose per-block histograms fit shared memory (one band for
     // every image up to kMaxTiles tiles)
     const int ty_n = (ntiles + tiles_x - 1) / tiles_x;

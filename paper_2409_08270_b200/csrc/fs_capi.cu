@@ -455,9 +455,11 @@ fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr,
 // depth-ordered by the raster prologue or launch_tile_sort).
 // vc == nullptr: the workspace's counters, reset first; otherwise the caller's
 // zeroed slot (the accumulate loop's view log -- no reset/copy kernels per view).
+// bin_blocks: binning grid (0 = the full-GPU default; the accumulate loop passes
+// fewer when other streams' rasters run beside it).
 void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
                  int cull_floor, fs::ProjectExport ex, cudaEvent_t after_project = nullptr,
-                 fs::ViewCounters* vc = nullptr) {
+                 fs::ViewCounters* vc = nullptr, int bin_blocks = 0) {
     const int n = (int)ctx->n;
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     const bool own = vc == nullptr;
@@ -467,7 +469,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
                        cull_floor, w.k64, w.rect, w.r32, w.r64, vc, ex,
                        ctx->num_sms, w.stream, own);
     if (after_project) cudaEventRecord(after_project, w.stream);
-    fs::launch_bin(ntiles, tx, bin_buffers(w, n, vc), vc, ctx->num_sms, w.stream);
+    fs::launch_bin(ntiles, tx, bin_buffers(w, n, vc), vc, ctx->num_sms, w.stream, bin_blocks);
 }
 
 // Kernels one enqueue_view launches (for the stats' launch count).
@@ -478,7 +480,8 @@ void enqueue_view(fs_context* ctx, fs::Work& w, const fs::Camera& cam, const uin
                   int num_objects, double alpha_floor, double t_floor, int acc_kind, void* acc,
                   fs::ViewCounters* log, cudaEvent_t* ev = nullptr) {
     if (ev) cudaEventRecord(ev[0], w.stream);
-    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr, log);
+    const int blocks = ctx->work.size() > 1 ? fs::bin_blocks_overlapped(ctx->num_sms) : 0;
+    enqueue_bin(ctx, w, cam, alpha_floor, 1, fs::ProjectExport{}, ev ? ev[1] : nullptr, log, blocks);
     if (ev) cudaEventRecord(ev[2], w.stream);
     const int tx = fs::tiles_x_of(cam.width), ntiles = tx * fs::tiles_y_of(cam.height);
     fs::RasterArgs ra{};

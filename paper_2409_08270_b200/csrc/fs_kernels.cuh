@@ -74,10 +74,12 @@ struct BinBuffers {
     unsigned int capacity;
 };
 constexpr int kMaxTiles = 49152;        // tiles per binning band (per-block histograms in smem)
-int bin_blocks(int num_sms);
+int bin_blocks(int num_sms);             // most blocks a binning uses (count-matrix width)
+int bin_blocks_overlapped(int num_sms);  // blocks beside other streams' rasters
 cudaError_t bin_configure();
+// blocks: 0 = bin_blocks(num_sms)
 void launch_bin(int ntiles, int tiles_x, const BinBuffers& b, ViewCounters* vc, int num_sms,
-                cudaStream_t st);
+                cudaStream_t st, int blocks = 0);
 
 // The depth-ordered gids of the bucket starting at `begin` overwrite the first
 // half of the bucket's own instance bytes.
