@@ -456,7 +456,8 @@ fs::TileSortArgs tile_sort_args(fs::Work& w, const unsigned int* tie = nullptr,
 // vc == nullptr: the workspace's counters, reset first; otherwise the caller's
 // zeroed slot (the accumulate loop's view log -- no reset/copy kernels per view).
 // bin_blocks: binning grid (0 = the full-GPU default; the accumulate loop passes
-// fewer when other streams' rasters run beside it).
+// fewer when other streams' rasters run beside it, and the projection then
+// takes a smaller grid too).
 void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alpha_floor,
                  int cull_floor, fs::ProjectExport ex, cudaEvent_t after_project = nullptr,
                  fs::ViewCounters* vc = nullptr, int bin_blocks = 0) {
@@ -467,7 +468,7 @@ void enqueue_bin(fs_context* ctx, fs::Work& w, const fs::Camera& cam, double alp
     ex.perm = scene_perm(ctx);
     fs::launch_project(n, ctx->mx, ctx->my, ctx->mz, ctx->sig, ctx->opac, cam, alpha_floor,
                        cull_floor, w.k64, w.rect, w.r32, w.r64, vc, ex,
-                       ctx->num_sms, w.stream, own);
+                       ctx->num_sms, w.stream, own, bin_blocks > 0);
     if (after_project) cudaEventRecord(after_project, w.stream);
     fs::launch_bin(ntiles, tx, bin_buffers(w, n, vc), vc, ctx->num_sms, w.stream, bin_blocks);
 }

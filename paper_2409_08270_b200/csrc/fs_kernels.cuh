@@ -50,7 +50,7 @@ void launch_project(int n, const double* mx, const double* my, const double* mz,
                     int cull_floor, unsigned long long* keys, unsigned long long* rect,
                     Rec32* r32, Rec64* r64,
                     ViewCounters* vc, ProjectExport ex, int num_sms, cudaStream_t st,
-                    bool reset_counters = true);
+                    bool reset_counters = true, bool overlapped = false);
 void launch_view_begin(ViewCounters* vc, cudaStream_t st);
 void launch_splat_records(int k, const double* mean2d, const double* conic, const double* depth,
                           const double* opac, double alpha_floor, Rec32* r32, Rec64* r64,
