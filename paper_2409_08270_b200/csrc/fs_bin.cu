@@ -29,7 +29,10 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBinThreads = 1024;  // count / emit: latency-bound gid walks, full occupancy
+#ifndef FS_BIN_THREADS
+#define FS_BIN_THREADS 1024
+#endif
+constexpr int kBinThreads = FS_BIN_THREADS;  // count / emit: latency-bound gid walks
 constexpr int kUnroll = 4;         // gids per thread with their loads issued together
 
 __device__ __forceinline__ void gid_range(int n, int b, int g, int& lo, int& hi) {
@@ -300,7 +303,15 @@ int bin_blocks(int num_sms) { return 2 * num_sms; }
 // raster CTAs of the other views their SMs and shrink the count matrix the
 // scan walks -- C2 solve 70.0 -> 67.1 ms, C4 310 -> 303 ms against 2 per SM
 // (37-49 blocks best; 18 or fewer starve the binning).
-int bin_blocks_overlapped(int num_sms) { return std::max(1, num_sms / 3); }
+#ifndef FS_BIN_OVL_NUM
+#define FS_BIN_OVL_NUM 1
+#endif
+#ifndef FS_BIN_OVL_DEN
+#define FS_BIN_OVL_DEN 3
+#endif
+int bin_blocks_overlapped(int num_sms) {
+    return std::max(1, num_sms * FS_BIN_OVL_NUM / FS_BIN_OVL_DEN);
+}
 
 cudaError_t bin_configure() {
     const int bytes = (int)(kMaxTiles * sizeof(unsigned int));
