@@ -73,7 +73,7 @@ typedef struct {
     int64_t instances;        /* (view, tile, gaussian) binning instances */
     int64_t tile_steps;       /* list entries walked by the raster kernel */
     int64_t exact_evals;      /* float64 alpha evaluations */
-    int64_t atomics;          /* float64 accumulator atomics */
+    int64_t atomics;          /* accumulator adds (one RED, or two uint64 REDs for FS_ACC_FIXED) */
     int64_t retried_views;    /* views re-run after growing the instance buffers */
     int64_t launches;         /* kernels this call launched */
     int64_t label_error_view; /* first view with a label >= num_objects, or -1 */
